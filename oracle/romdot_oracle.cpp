@@ -1,0 +1,1605 @@
+// ============================================================================
+// romdot CPU ORACLE — TEST INFRASTRUCTURE ONLY.
+//
+// This file is a CPU restatement of the reference's basis-build path
+// (/root/reference/proj/src/{grid,krylov,basis}.cpp) used ONLY as the checker
+// by tests/, __graft_entry__.smoke() and bench.py's cpu_baseline / --impl
+// reference legs. Nothing in the product package (paper_1602_00138_b200/)
+// links, loads or calls it.
+//
+// Parity status: the reference cannot be compiled here (Eigen 3 and the
+// vendored doctest/CLI11 are absent), and it ships no golden
+// vectors. This restatement is pinned by porting the reference's own property
+// tests (test_krylov.cpp, test_basis.cpp, test_grid.cpp, acceptance.cpp C1/C4/
+// C7/C8) to tests/test_oracle_*.py, plus independent scipy cross-checks.
+//
+// Faithful parts (reduce exactly to the reference for 2D / constant D /
+// omega = 0 / MINRES):
+//   GridOp::apply                 <- grid.cpp:38-97   (Schur operator A~_* + diag(mu))
+//   minres_core                   <- krylov.cpp:17-98
+//   RecycleSpace::from_raw/append <- krylov.cpp:106-139
+//   initial_guess                 <- krylov.cpp:141-145
+//   recycled_minres               <- krylov.cpp:147-179
+//   smallest_eigenpairs           <- krylov.cpp:181-280
+//   GlobalBasis::{refresh,append,projected_coordinates,solve_projected}
+//                                 <- basis.cpp:37-112
+//   init_basis / init_basis_from  <- basis.cpp:114-155
+//   process_system                <- basis.cpp:157-207
+// Extensions (BASELINE.json): d = 3, variable D with
+// harmonic face means, complex shift i*h^2*omega/nu, recycled CG / COCG
+// (Chronopoulos-Gear form, CGS2 deflation), bilinear per-RHS recycle spaces
+// for complex-symmetric systems, candidate cap, column-pivoted Householder QR
+// (RRQR) compression at 1e-10 (acceptance.cpp:368-383 uses an SVD).
+// ============================================================================
+#include <algorithm>
+#include <cmath>
+#include <complex>
+#include <cstdint>
+#include <cstring>
+#include <functional>
+#include <limits>
+#include <memory>
+#include <random>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+namespace orc {
+
+using cd = std::complex<double>;
+
+struct ConfigError : std::runtime_error {
+    explicit ConfigError(const std::string& m) : std::runtime_error(m) {}
+};
+struct SolverError : std::runtime_error {
+    explicit SolverError(const std::string& m) : std::runtime_error(m) {}
+};
+
+// ---------------------------------------------------------------- scalars ---
+inline double cj(double x) { return x; }
+inline cd cj(cd x) { return std::conj(x); }
+inline double re(double x) { return x; }
+inline double re(cd x) { return x.real(); }
+inline double abs2(double x) { return x * x; }
+inline double abs2(cd x) { return x.real() * x.real() + x.imag() * x.imag(); }
+inline double sqrt_s(double x) { return std::sqrt(x); }
+inline cd sqrt_s(cd x) { return std::sqrt(x); }
+
+template <class T> T dotT(long n, const T* x, const T* y) {  // bilinear x^T y
+    T s = T(0);
+    for (long i = 0; i < n; ++i) s += x[i] * y[i];
+    return s;
+}
+template <class T> T dotH(long n, const T* x, const T* y) {  // Hermitian x^H y
+    T s = T(0);
+    for (long i = 0; i < n; ++i) s += cj(x[i]) * y[i];
+    return s;
+}
+template <class T> double nrm2(long n, const T* x) {
+    double s = 0.0;
+    for (long i = 0; i < n; ++i) s += abs2(x[i]);
+    return std::sqrt(s);
+}
+
+// ----------------------------------------------------- column-major matrix ---
+template <class T> struct Mat {
+    long r = 0, c = 0;
+    std::vector<T> a;
+    Mat() = default;
+    Mat(long rows, long cols) : r(rows), c(cols), a(static_cast<size_t>(rows * cols), T(0)) {}
+    T& operator()(long i, long j) { return a[i + j * r]; }
+    const T& operator()(long i, long j) const { return a[i + j * r]; }
+    T* col(long j) { return a.data() + j * r; }
+    const T* col(long j) const { return a.data() + j * r; }
+    void set_cols(long nc) { a.resize(static_cast<size_t>(r * nc), T(0)); c = nc; }
+    void remove_col(long j) {
+        for (long k = j; k + 1 < c; ++k) std::memcpy(col(k), col(k + 1), sizeof(T) * r);
+        set_cols(c - 1);
+    }
+};
+
+template <class T> using Vec = std::vector<T>;
+
+// ------------------------------------------------------------- operators ---
+// Generic matrix-free operator (reference LinOp, types.hpp:18), with an
+// optional direct solver used only by the eigen seed.
+template <class T> struct LinOp {
+    long n = 0;
+    std::function<void(const T*, T*)> apply;
+    std::function<void(const T*, T*)> solve;  // A^-1 x (eigen seed only)
+    double lam_max = 0.0;                     // Gershgorin bound (krylov.cpp:190-195)
+};
+
+// Grid Schur operator, restating grid.cpp:38-97 and extending it (App. A).
+// Unknowns are the interior nodes; axis d-1 is the Robin axis whose two
+// boundary layers are eliminated (Schur complement), every other axis has
+// homogeneous Dirichlet ghosts. Row p (h^2-scaled):
+//   (A x)_p = (sum_faces Df + mu_p [+ i shift]) x_p - sum_{interior q} D_pq x_q
+// with D_pq the harmonic mean of the two node values, Df = D_p toward a
+// Dirichlet ghost and Df = Dbg/(1+rho) toward an eliminated Robin layer
+// (= Dbg - Dbg*rho/(1+rho), the D2 G^-1 D1 correction of grid.cpp:86-93).
+struct GridOp {
+    int d = 2;
+    long N[3] = {1, 1, 1};
+    long n = 0;
+    double robin_face = 0.0;  // Dbg/(1+rho)
+    double shift = 0.0;       // h^2 omega/nu (imaginary diagonal)
+    std::vector<double> D, mu;
+
+    static double hm(double a, double b) { return 2.0 * a * b / (a + b); }
+
+    template <class T> void apply_one(const T* x, T* y) const {
+        const long s1 = N[0], s2 = N[0] * N[1];
+        const long n0 = N[0], n1 = N[1], n2 = N[2];
+        for (long k = 0; k < (d == 3 ? n2 : 1); ++k)
+            for (long j = 0; j < n1; ++j)
+                for (long i = 0; i < n0; ++i) {
+                    const long p = i + j * s1 + k * s2;
+                    const double Dp = D[p];
+                    double diag = 0.0;
+                    T acc = T(0);
+                    // axis order 0,1,2 ; direction -, +  (must match the CUDA kernel)
+                    for (int ax = 0; ax < d; ++ax) {
+                        const long idx = ax == 0 ? i : (ax == 1 ? j : k);
+                        const long len = ax == 0 ? n0 : (ax == 1 ? n1 : n2);
+                        const long st = ax == 0 ? 1 : (ax == 1 ? s1 : s2);
+                        const bool robin = (ax == d - 1);
+                        for (int dir = -1; dir <= 1; dir += 2) {
+                            const long q = idx + dir;
+                            if (q >= 0 && q < len) {
+                                const double Df = hm(Dp, D[p + dir * st]);
+                                diag += Df;
+                                acc += Df * x[p + dir * st];
+                            } else if (robin) {
+                                diag += robin_face;
+                            } else {
+                                diag += Dp;
+                            }
+                        }
+                    }
+                    y[p] = diag_term<T>(diag + mu[p]) * x[p] - acc;
+                }
+    }
+    template <class T> T diag_term(double dr) const;
+
+    // Explicit row for direct solvers / Gershgorin: diag and (col, -Df) list.
+    void row(long p, double& diag, std::vector<std::pair<long, double>>& off) const {
+        off.clear();
+        const long s1 = N[0], s2 = N[0] * N[1];
+        long c[3] = {p % N[0], (p / s1) % N[1], d == 3 ? p / s2 : 0};
+        const double Dp = D[p];
+        diag = 0.0;
+        for (int ax = 0; ax < d; ++ax) {
+            const long st = ax == 0 ? 1 : (ax == 1 ? s1 : s2);
+            for (int dir = -1; dir <= 1; dir += 2) {
+                const long q = c[ax] + dir;
+                if (q >= 0 && q < N[ax]) {
+                    const double Df = hm(Dp, D[p + dir * st]);
+                    diag += Df;
+                    off.emplace_back(p + dir * st, -Df);
+                } else if (ax == d - 1) {
+                    diag += robin_face;
+                } else {
+                    diag += Dp;
+                }
+            }
+        }
+        diag += mu[p];
+    }
+
+    double gershgorin() const {
+        double lm = 0.0;
+        std::vector<std::pair<long, double>> off;
+        for (long p = 0; p < n; ++p) {
+            double dg;
+            row(p, dg, off);
+            double s = std::abs(dg) + (shift != 0.0 ? std::abs(shift) : 0.0);
+            for (auto& o : off) s += std::abs(o.second);
+            lm = std::max(lm, s);
+        }
+        return lm;
+    }
+};
+template <> inline double GridOp::diag_term<double>(double dr) const { return dr; }
+template <> inline cd GridOp::diag_term<cd>(double dr) const { return cd(dr, shift); }
+
+// Banded Cholesky of the (real, SPD) grid operator: the exact direct solve the
+// reference gets from SimplicialLDLT (krylov.cpp:185), feasible for 2D and
+// small 3D grids (bandwidth N0 resp. N0*N1).
+struct BandChol {
+    long n = 0, bw = 0;
+    std::vector<double> L;  // L[(k)*n + i] = L(i, i-k), k = 0..bw
+    bool build(const GridOp& op) {
+        n = op.n;
+        bw = op.d == 2 ? op.N[0] : op.N[0] * op.N[1];
+        L.assign(static_cast<size_t>(n * (bw + 1)), 0.0);
+        std::vector<std::pair<long, double>> off;
+        for (long p = 0; p < n; ++p) {
+            double dg;
+            op.row(p, dg, off);
+            L[p] = dg;
+            for (auto& o : off)
+                if (o.first < p) L[(p - o.first) * n + p] = o.second;
+        }
+        for (long j = 0; j < n; ++j) {
+            double s = L[j];
+            for (long k = 1; k <= bw && j - k >= 0; ++k) s -= L[k * n + j] * L[k * n + j];
+            if (!(s > 0.0)) return false;
+            const double ljj = std::sqrt(s);
+            L[j] = ljj;
+            for (long i = j + 1; i <= std::min(n - 1, j + bw); ++i) {
+                double v = L[(i - j) * n + i];
+                for (long k = 1; i - j + k <= bw && j - k >= 0; ++k)
+                    v -= L[(i - j + k) * n + i] * L[k * n + j];
+                L[(i - j) * n + i] = v / ljj;
+            }
+        }
+        return true;
+    }
+    void solve(const double* b, double* x) const {
+        for (long i = 0; i < n; ++i) {
+            double s = b[i];
+            for (long k = 1; k <= bw && i - k >= 0; ++k) s -= L[k * n + i] * x[i - k];
+            x[i] = s / L[i];
+        }
+        for (long i = n - 1; i >= 0; --i) {
+            double s = x[i];
+            for (long k = 1; k <= bw && i + k < n; ++k) s -= L[k * n + i + k] * x[i + k];
+            x[i] = s / L[i];
+        }
+    }
+};
+
+// ---------------------------------------------------------- dense kernels ---
+// y -= K c ; c = K^op w  with op = T (bilinear) or H (Hermitian)
+template <class T> void gemv_op(const Mat<T>& K, long cols, const T* w, T* c, bool herm) {
+    for (long j = 0; j < cols; ++j) c[j] = herm ? dotH(K.r, K.col(j), w) : dotT(K.r, K.col(j), w);
+}
+template <class T> void sub_Kc(const Mat<T>& K, long cols, const T* c, T* y) {
+    for (long j = 0; j < cols; ++j) {
+        const T cjv = c[j];
+        const T* kc = K.col(j);
+        for (long i = 0; i < K.r; ++i) y[i] -= kc[i] * cjv;
+    }
+}
+
+// Householder thin QR (LAPACK geqr2/ung2r conventions, Hermitian). Stands in
+// for Eigen::HouseholderQR at basis.cpp:16-22 / krylov.cpp:109-113.
+template <class T> void thin_qr(const Mat<T>& M, Mat<T>& Q, Mat<T>& R) {
+    const long n = M.r, m = M.c;
+    Mat<T> A = M;
+    std::vector<T> tau(m, T(0));
+    for (long j = 0; j < m && j < n; ++j) {
+        T alpha = A(j, j);
+        double xn2 = 0.0;
+        for (long i = j + 1; i < n; ++i) xn2 += abs2(A(i, j));
+        if (xn2 == 0.0 && std::imag(cd(alpha)) == 0.0) {
+            tau[j] = T(0);
+        } else {
+            const double bnorm = std::sqrt(abs2(alpha) + xn2);
+            const double beta = re(alpha) >= 0.0 ? -bnorm : bnorm;
+            tau[j] = (T(beta) - alpha) / T(beta);
+            const T scal = T(1) / (alpha - T(beta));
+            for (long i = j + 1; i < n; ++i) A(i, j) *= scal;
+            A(j, j) = T(beta);
+        }
+        // apply H_j^H = I - conj(tau) v v^H to trailing columns
+        if (tau[j] != T(0)) {
+            for (long k = j + 1; k < m; ++k) {
+                T s = A(j, k);
+                for (long i = j + 1; i < n; ++i) s += cj(A(i, j)) * A(i, k);
+                s *= cj(tau[j]);
+                A(j, k) -= s;
+                for (long i = j + 1; i < n; ++i) A(i, k) -= s * A(i, j);
+            }
+        }
+    }
+    R = Mat<T>(m, m);
+    for (long j = 0; j < m; ++j)
+        for (long i = 0; i <= j && i < n; ++i) R(i, j) = A(i, j);
+    Q = Mat<T>(n, m);
+    for (long i = 0; i < m && i < n; ++i) Q(i, i) = T(1);
+    for (long j = std::min(m, n) - 1; j >= 0; --j) {
+        if (tau[j] == T(0)) continue;
+        for (long k = j; k < m; ++k) {
+            T s = Q(j, k);
+            for (long i = j + 1; i < n; ++i) s += cj(A(i, j)) * Q(i, k);
+            s *= tau[j];
+            Q(j, k) -= s;
+            for (long i = j + 1; i < n; ++i) Q(i, k) -= s * A(i, j);
+        }
+    }
+}
+
+// Column-pivoted Householder QR (LAPACK geqp3-style norm downdating) on the
+// column-normalised candidate basis: the BASELINE RRQR (App. A9).
+template <class T>
+long qrcp(const Mat<T>& M0, double tol, std::vector<long>& perm, Mat<T>& Rout, Mat<T>& Qk,
+          std::vector<double>& rdiag, bool normalize) {
+    const long n = M0.r, m = M0.c;
+    Mat<T> A = M0;
+    for (long j = 0; j < m && normalize; ++j) {
+        const double nj = nrm2(n, A.col(j));
+        if (nj > 0.0)
+            for (long i = 0; i < n; ++i) A(i, j) /= nj;
+    }
+    perm.resize(m);
+    for (long j = 0; j < m; ++j) perm[j] = j;
+    std::vector<double> vn1(m), vn2(m);
+    for (long j = 0; j < m; ++j) vn1[j] = vn2[j] = nrm2(n, A.col(j));
+    const double tol3z = std::sqrt(std::numeric_limits<double>::epsilon());
+    const long kmax = std::min(n, m);
+    std::vector<T> tau(kmax, T(0));
+    for (long j = 0; j < kmax; ++j) {
+        long pv = j;
+        for (long k = j + 1; k < m; ++k)
+            if (vn1[k] > vn1[pv]) pv = k;
+        if (pv != j) {
+            for (long i = 0; i < n; ++i) std::swap(A(i, j), A(i, pv));
+            std::swap(perm[j], perm[pv]);
+            vn1[pv] = vn1[j];
+            vn2[pv] = vn2[j];
+        }
+        T alpha = A(j, j);
+        double xn2 = 0.0;
+        for (long i = j + 1; i < n; ++i) xn2 += abs2(A(i, j));
+        if (xn2 == 0.0 && std::imag(cd(alpha)) == 0.0) {
+            tau[j] = T(0);
+        } else {
+            const double bnorm = std::sqrt(abs2(alpha) + xn2);
+            const double beta = re(alpha) >= 0.0 ? -bnorm : bnorm;
+            tau[j] = (T(beta) - alpha) / T(beta);
+            const T scal = T(1) / (alpha - T(beta));
+            for (long i = j + 1; i < n; ++i) A(i, j) *= scal;
+            A(j, j) = T(beta);
+        }
+        for (long k = j + 1; k < m; ++k) {
+            if (tau[j] != T(0)) {
+                T s = A(j, k);
+                for (long i = j + 1; i < n; ++i) s += cj(A(i, j)) * A(i, k);
+                s *= cj(tau[j]);
+                A(j, k) -= s;
+                for (long i = j + 1; i < n; ++i) A(i, k) -= s * A(i, j);
+            }
+            if (vn1[k] != 0.0) {
+                double t = std::abs(cd(A(j, k))) / vn1[k];
+                t = std::max(0.0, 1.0 - t * t);
+                const double t2 = t * (vn1[k] / vn2[k]) * (vn1[k] / vn2[k]);
+                if (t2 <= tol3z) {
+                    double s2 = 0.0;
+                    for (long i = j + 1; i < n; ++i) s2 += abs2(A(i, k));
+                    vn1[k] = std::sqrt(s2);
+                    vn2[k] = vn1[k];
+                } else {
+                    vn1[k] *= std::sqrt(t);
+                }
+            }
+        }
+    }
+    Rout = Mat<T>(kmax, m);
+    for (long j = 0; j < m; ++j)
+        for (long i = 0; i <= std::min(j, kmax - 1); ++i) Rout(i, j) = A(i, j);
+    rdiag.resize(kmax);
+    for (long i = 0; i < kmax; ++i) rdiag[i] = std::abs(cd(A(i, i)));
+    long rank = 0;
+    while (rank < kmax && rdiag[rank] > tol * rdiag[0]) ++rank;
+    Qk = Mat<T>(n, rank);
+    for (long i = 0; i < rank; ++i) Qk(i, i) = T(1);
+    for (long j = rank - 1; j >= 0; --j) {
+        if (tau[j] == T(0)) continue;
+        for (long k = j; k < rank; ++k) {
+            T s = Qk(j, k);
+            for (long i = j + 1; i < n; ++i) s += cj(A(i, j)) * Qk(i, k);
+            s *= tau[j];
+            Qk(j, k) -= s;
+            for (long i = j + 1; i < n; ++i) Qk(i, k) -= s * A(i, j);
+        }
+    }
+    return rank;
+}
+
+// ------------------------------------------------------------ reports ---
+struct SolveReport {
+    int iterations = 0;
+    std::vector<double> hist;
+    bool converged = false;
+    double correction_norm = 0.0;
+};
+
+// Paige-Saunders MINRES, restating minres_core (krylov.cpp:17-98) verbatim.
+inline void minres_core(const LinOp<double>& op, const double* b, double tol, long maxit,
+                        double b_scale, const std::function<void(double*)>& reorth,
+                        std::vector<double>& x, SolveReport& rep) {
+    const long n = op.n;
+    x.assign(n, 0.0);
+    rep = SolveReport();
+    const double beta1 = nrm2(n, b);
+    const double scale = b_scale > 0.0 ? b_scale : beta1;
+    if (beta1 == 0.0 || scale == 0.0) {
+        rep.converged = true;
+        rep.hist.push_back(0.0);
+        return;
+    }
+    double relres = beta1 / scale;
+    rep.hist.push_back(relres);
+    if (relres <= tol) {
+        rep.converged = true;
+        return;
+    }
+    std::vector<double> v(n), v_old(n, 0.0), d_old(n, 0.0), d_oold(n, 0.0), p(n), d_new(n);
+    for (long i = 0; i < n; ++i) v[i] = b[i] / beta1;
+    double c_old2 = 1.0, s_old2 = 0.0, c_old = 1.0, s_old = 0.0;
+    double phibar = beta1, beta = 0.0, best = relres;
+    int stagnant = 0;
+    for (long k = 1; k <= maxit; ++k) {
+        op.apply(v.data(), p.data());
+        const double alpha = dotT(n, v.data(), p.data());
+        for (long i = 0; i < n; ++i) p[i] -= alpha * v[i] + beta * v_old[i];
+        if (reorth) reorth(p.data());
+        const double beta_next = nrm2(n, p.data());
+        const double eps = s_old2 * beta;
+        const double delta_bar = c_old2 * beta;
+        const double delta = c_old * delta_bar + s_old * alpha;
+        const double gamma_bar = -s_old * delta_bar + c_old * alpha;
+        const double gamma = std::hypot(gamma_bar, beta_next);
+        if (gamma == 0.0) break;
+        const double c = gamma_bar / gamma;
+        const double s = beta_next / gamma;
+        for (long i = 0; i < n; ++i) d_new[i] = (v[i] - delta * d_old[i] - eps * d_oold[i]) / gamma;
+        const double cp = c * phibar;
+        for (long i = 0; i < n; ++i) x[i] += cp * d_new[i];
+        phibar = -s * phibar;
+        relres = std::abs(phibar) / scale;
+        rep.iterations = static_cast<int>(k);
+        rep.hist.push_back(relres);
+        if (!std::isfinite(relres)) {
+            rep.converged = false;
+            break;
+        }
+        if (relres <= tol) {
+            rep.converged = true;
+            break;
+        }
+        if (relres < best * (1.0 - 1e-12)) {
+            best = relres;
+            stagnant = 0;
+        } else if (++stagnant >= 50) {
+            break;
+        }
+        if (beta_next <= 1e-300) break;
+        v_old = v;
+        for (long i = 0; i < n; ++i) v[i] = p[i] / beta_next;
+        beta = beta_next;
+        d_oold = d_old;
+        d_old = d_new;
+        c_old2 = c_old;
+        s_old2 = s_old;
+        c_old = c;
+        s_old = s;
+    }
+}
+
+// -------------------------------------------------------- recycle space ---
+// (U, K) with A U = K and K^T K = I (krylov.hpp:17-37). Real: Householder
+// from_raw as in krylov.cpp:106-115. Complex symmetric: bilinear (T-)
+// orthonormal K (K^T K = I unconjugated) so P = I - K K^T keeps P A P
+// complex symmetric, built by bilinear CGS2.
+template <class T> struct RecycleSpace {
+    Mat<T> U, K;
+    long cols() const { return K.c; }
+
+    bool append(const T* u, const T* k);  // krylov.cpp:117-139
+
+    static RecycleSpace from_raw(const Mat<T>& W, const Mat<T>& AW);
+};
+
+template <> inline RecycleSpace<double> RecycleSpace<double>::from_raw(const Mat<double>& W,
+                                                                       const Mat<double>& AW) {
+    RecycleSpace rs;
+    rs.U = Mat<double>(W.r, 0);
+    rs.K = Mat<double>(W.r, 0);
+    if (W.c == 0) return rs;
+    Mat<double> Q, R;
+    thin_qr(AW, Q, R);
+    rs.K = Q;
+    rs.U = Mat<double>(W.r, W.c);
+    for (long j = 0; j < W.c; ++j) {  // U = W R^-1 (R^T U^T = W^T)
+        double* uj = rs.U.col(j);
+        std::memcpy(uj, W.col(j), sizeof(double) * W.r);
+        for (long i = 0; i < j; ++i) {
+            const double rij = R(i, j);
+            const double* ui = rs.U.col(i);
+            for (long t = 0; t < W.r; ++t) uj[t] -= ui[t] * rij;
+        }
+        for (long t = 0; t < W.r; ++t) uj[t] /= R(j, j);
+    }
+    return rs;
+}
+
+template <> inline RecycleSpace<cd> RecycleSpace<cd>::from_raw(const Mat<cd>& W, const Mat<cd>& AW) {
+    RecycleSpace rs;
+    rs.U = Mat<cd>(W.r, 0);
+    rs.K = Mat<cd>(W.r, 0);
+    const long n = W.r;
+    for (long j = 0; j < W.c; ++j) {
+        // bilinear CGS2 of column j; never rejects (from_raw keeps every column)
+        const long c = rs.K.c;
+        std::vector<cd> q(AW.col(j), AW.col(j) + n), c1(c), c2(c);
+        gemv_op(rs.K, c, q.data(), c1.data(), false);
+        sub_Kc(rs.K, c, c1.data(), q.data());
+        gemv_op(rs.K, c, q.data(), c2.data(), false);
+        sub_Kc(rs.K, c, c2.data(), q.data());
+        for (long t = 0; t < c; ++t) c1[t] += c2[t];
+        const cd rho = sqrt_s(dotT(n, q.data(), q.data()));
+        rs.K.set_cols(c + 1);
+        rs.U.set_cols(c + 1);
+        cd* kc = rs.K.col(c);
+        cd* uc = rs.U.col(c);
+        for (long t = 0; t < n; ++t) kc[t] = q[t] / rho;
+        std::memcpy(uc, W.col(j), sizeof(cd) * n);
+        sub_Kc(rs.U, c, c1.data(), uc);
+        for (long t = 0; t < n; ++t) uc[t] /= rho;
+    }
+    return rs;
+}
+
+template <class T> bool RecycleSpace<T>::append(const T* u, const T* k) {
+    const long n = K.r;
+    const long c = K.c;
+    const bool herm = false;  // bilinear for complex, plain for real
+    if (c == 0) {
+        const T rho = sqrt_s(dotT(n, k, k));
+        if (std::abs(cd(rho)) <= 1e-300) return false;
+        K.set_cols(1);
+        U.set_cols(1);
+        for (long t = 0; t < n; ++t) {
+            K(t, 0) = k[t] / rho;
+            U(t, 0) = u[t] / rho;
+        }
+        return true;
+    }
+    std::vector<T> q(k, k + n), c1(c), c2(c);
+    gemv_op(K, c, q.data(), c1.data(), herm);
+    sub_Kc(K, c, c1.data(), q.data());
+    gemv_op(K, c, q.data(), c2.data(), herm);
+    sub_Kc(K, c, c2.data(), q.data());
+    for (long t = 0; t < c; ++t) c1[t] += c2[t];
+    const T rho = sqrt_s(dotT(n, q.data(), q.data()));
+    if (std::abs(cd(rho)) <= 1e-12 * nrm2(n, k)) return false;
+    std::vector<T> un(u, u + n);
+    sub_Kc(U, c, c1.data(), un.data());
+    K.set_cols(c + 1);
+    U.set_cols(c + 1);
+    for (long t = 0; t < n; ++t) {
+        K(t, c) = q[t] / rho;
+        U(t, c) = un[t] / rho;
+    }
+    return true;
+}
+
+// z = U K^T b, r = b - K K^T b (krylov.cpp:141-145)
+template <class T> void initial_guess(const RecycleSpace<T>& rs, const T* b, T* z, T* r) {
+    const long n = rs.K.r, c = rs.cols();
+    std::vector<T> cc(c);
+    gemv_op(rs.K, c, b, cc.data(), false);
+    for (long i = 0; i < n; ++i) {
+        z[i] = T(0);
+        r[i] = b[i];
+    }
+    for (long j = 0; j < c; ++j)
+        for (long i = 0; i < n; ++i) {
+            z[i] += rs.U(i, j) * cc[j];
+            r[i] -= rs.K(i, j) * cc[j];
+        }
+}
+
+template <class T> struct RecycledResult {
+    std::vector<T> correction, new_direction, image;
+    SolveReport report;
+};
+
+// Deflated MINRES, restating recycled_minres (krylov.cpp:147-179) verbatim:
+// Lanczos on (I - K K^T) A with each Lanczos vector re-projected.
+inline RecycledResult<double> recycled_minres(const LinOp<double>& A, const RecycleSpace<double>& rs,
+                                              const double* rhs, double tol, long maxit,
+                                              double rhs_scale) {
+    const long n = A.n, c = rs.cols();
+    const bool deflated = c > 0;
+    std::vector<double> tmp(c);
+    auto project = [&](double* w) {
+        if (!deflated) return;
+        gemv_op(rs.K, c, w, tmp.data(), false);
+        sub_Kc(rs.K, c, tmp.data(), w);
+    };
+    std::vector<double> r0(rhs, rhs + n);
+    project(r0.data());
+    const double scale = rhs_scale > 0.0 ? rhs_scale : nrm2(n, rhs);
+    LinOp<double> op;
+    op.n = n;
+    op.apply = [&](const double* v, double* w) {
+        A.apply(v, w);
+        project(w);
+    };
+    RecycledResult<double> res;
+    minres_core(op, r0.data(), tol, maxit, scale, project, res.new_direction, res.report);
+    res.image.resize(n);
+    A.apply(res.new_direction.data(), res.image.data());
+    res.correction = res.new_direction;
+    if (deflated && nrm2(n, res.new_direction.data()) > 0.0) {
+        std::vector<double> cc(c);
+        gemv_op(rs.K, c, res.image.data(), cc.data(), false);
+        for (long j = 0; j < c; ++j)
+            for (long i = 0; i < n; ++i) res.correction[i] -= rs.U(i, j) * cc[j];
+    }
+    res.report.correction_norm = nrm2(n, res.correction.data());
+    return res;
+}
+
+// Recycled CG / COCG (extension). Chronopoulos-Gear CG on
+// P A P restricted to Range(P), P = I - K K^T (bilinear for complex), one
+// merged reduction {r^T r, r^T A r, r^H r} per iteration, CGS2 deflation of
+// the operator image (the two projections per step of krylov.cpp:161-166).
+// Convergence: ||rhs - A g|| / rhs_scale <= tol, as in krylov.cpp:159.
+// g = y + U (K^T rhs - K^T A y) solves A g = rhs over Range([U, Krylov]).
+template <class T>
+RecycledResult<T> recycled_cg(const LinOp<T>& A, const RecycleSpace<T>& rs, const T* rhs, double tol,
+                              long maxit, double rhs_scale) {
+    const long n = A.n, c = rs.cols();
+    std::vector<T> r(rhs, rhs + n), e(c, T(0)), c1(c), c2(c);
+    if (c > 0) {
+        gemv_op(rs.K, c, r.data(), c1.data(), false);
+        sub_Kc(rs.K, c, c1.data(), r.data());
+        gemv_op(rs.K, c, r.data(), c2.data(), false);
+        sub_Kc(rs.K, c, c2.data(), r.data());
+        for (long j = 0; j < c; ++j) e[j] = c1[j] + c2[j];
+    }
+    const double scale = rhs_scale > 0.0 ? rhs_scale : nrm2(n, rhs);
+    RecycledResult<T> res;
+    SolveReport& rep = res.report;
+    std::vector<T> y(n, T(0)), p(n, T(0)), s(n, T(0)), w(n);
+    double rn = nrm2(n, r.data());
+    double relres = scale > 0.0 ? rn / scale : 0.0;
+    rep.hist.push_back(relres);
+    if (rn == 0.0 || scale == 0.0 || relres <= tol) {
+        rep.converged = true;
+    } else {
+        double best = relres;
+        int stagnant = 0;
+        T alpha_prev = T(0), gamma_prev = T(0);
+        for (long it = 0; it < maxit; ++it) {
+            A.apply(r.data(), w.data());
+            const T gamma = dotT(n, r.data(), r.data());
+            const T delta = dotT(n, r.data(), w.data());
+            T alpha, beta;
+            if (it == 0) {
+                beta = T(0);
+                alpha = gamma / delta;
+            } else {
+                beta = gamma / gamma_prev;
+                alpha = gamma / (delta - beta * gamma / alpha_prev);
+            }
+            if (c > 0) {
+                gemv_op(rs.K, c, w.data(), c1.data(), false);
+                sub_Kc(rs.K, c, c1.data(), w.data());
+                gemv_op(rs.K, c, w.data(), c2.data(), false);
+                sub_Kc(rs.K, c, c2.data(), w.data());
+            }
+            for (long i = 0; i < n; ++i) {
+                p[i] = r[i] + beta * p[i];
+                s[i] = w[i] + beta * s[i];
+                y[i] += alpha * p[i];
+                r[i] -= alpha * s[i];
+            }
+            gamma_prev = gamma;
+            alpha_prev = alpha;
+            rep.iterations = static_cast<int>(it + 1);
+            relres = nrm2(n, r.data()) / scale;
+            rep.hist.push_back(relres);
+            if (!std::isfinite(relres)) {
+                rep.converged = false;
+                break;
+            }
+            if (relres <= tol) {
+                rep.converged = true;
+                break;
+            }
+            if (relres < best * (1.0 - 1e-12)) {
+                best = relres;
+                stagnant = 0;
+            } else if (++stagnant >= 50) {
+                break;
+            }
+        }
+    }
+    res.new_direction = y;
+    res.image.resize(n);
+    A.apply(y.data(), res.image.data());
+    res.correction = y;
+    if (c > 0) {
+        std::vector<T> cc(c);
+        gemv_op(rs.K, c, res.image.data(), cc.data(), false);
+        for (long j = 0; j < c; ++j) cc[j] = e[j] - cc[j];
+        for (long j = 0; j < c; ++j)
+            for (long i = 0; i < n; ++i) res.correction[i] += rs.U(i, j) * cc[j];
+    }
+    rep.correction_norm = nrm2(n, res.correction.data());
+    return res;
+}
+
+// --------------------------------------------------------- eigen seed ---
+// Shift-invert Lanczos with full two-pass reorthogonalisation, restating
+// smallest_eigenpairs (krylov.cpp:181-280); the start vector uses the same
+// mt19937_64(12345) + std::normal_distribution stream as the reference.
+inline void smallest_eigenpairs(const LinOp<double>& A, long k, double tol, std::vector<double>& lam,
+                                Mat<double>& Uout) {
+    const long n = A.n;
+    if (k < 1 || k > n) throw ConfigError("eigensolver: k out of range");
+    const double lam_max = A.lam_max;
+    std::mt19937_64 rng(12345);
+    std::normal_distribution<double> gauss;
+    auto random_vec = [&](std::vector<double>& v) {
+        v.resize(n);
+        for (long i = 0; i < n; ++i) v[i] = gauss(rng);
+    };
+    Mat<double> V(n, std::min(n, std::max(2 * k + 30, 60L)));
+    std::vector<double> alphas, betas, v, w(n), tmp;
+    random_vec(v);
+    {
+        const double nv = nrm2(n, v.data());
+        for (auto& t : v) t /= nv;
+    }
+    std::memcpy(V.col(0), v.data(), sizeof(double) * n);
+    long m = 0;
+    auto ritz_converged = [&]() -> bool {
+        if (m < k) return false;
+        // symmetric tridiagonal eigen-decomposition by Jacobi (m is small)
+        Mat<double> T(m, m), Z(m, m);
+        for (long i = 0; i < m; ++i) {
+            T(i, i) = alphas[i];
+            if (i + 1 < m) T(i, i + 1) = T(i + 1, i) = betas[i];
+            Z(i, i) = 1.0;
+        }
+        for (int sweep = 0; sweep < 100; ++sweep) {
+            double off = 0.0;
+            for (long p = 0; p < m; ++p)
+                for (long q = p + 1; q < m; ++q) off += T(p, q) * T(p, q);
+            if (off < 1e-30) break;
+            for (long p = 0; p < m; ++p)
+                for (long q = p + 1; q < m; ++q) {
+                    if (std::abs(T(p, q)) < 1e-300) continue;
+                    const double th = (T(q, q) - T(p, p)) / (2.0 * T(p, q));
+                    const double t = (th >= 0 ? 1.0 : -1.0) / (std::abs(th) + std::sqrt(th * th + 1.0));
+                    const double cs = 1.0 / std::sqrt(t * t + 1.0), sn = t * cs;
+                    for (long r = 0; r < m; ++r) {
+                        const double a = T(r, p), b = T(r, q);
+                        T(r, p) = cs * a - sn * b;
+                        T(r, q) = sn * a + cs * b;
+                    }
+                    for (long r = 0; r < m; ++r) {
+                        const double a = T(p, r), b = T(q, r);
+                        T(p, r) = cs * a - sn * b;
+                        T(q, r) = sn * a + cs * b;
+                    }
+                    for (long r = 0; r < m; ++r) {
+                        const double a = Z(r, p), b = Z(r, q);
+                        Z(r, p) = cs * a - sn * b;
+                        Z(r, q) = sn * a + cs * b;
+                    }
+                }
+        }
+        std::vector<long> ord(m);
+        for (long i = 0; i < m; ++i) ord[i] = i;
+        std::sort(ord.begin(), ord.end(), [&](long a, long b) { return T(a, a) > T(b, b); });
+        Mat<double> U(n, k);
+        std::vector<double> lm(k), Au(n);
+        for (long i = 0; i < k; ++i) {
+            double* u = U.col(i);
+            for (long t = 0; t < m; ++t) {
+                const double z = Z(t, ord[i]);
+                const double* vt = V.col(t);
+                for (long s = 0; s < n; ++s) u[s] += vt[s] * z;
+            }
+            const double nu = nrm2(n, u);
+            for (long s = 0; s < n; ++s) u[s] /= nu;
+        }
+        for (long i = 0; i < k; ++i) {
+            A.apply(U.col(i), Au.data());
+            lm[i] = dotT(n, U.col(i), Au.data());
+            double rr = 0.0;
+            for (long s = 0; s < n; ++s) rr += (Au[s] - lm[i] * U(s, i)) * (Au[s] - lm[i] * U(s, i));
+            if (std::sqrt(rr) > tol * lam_max) return false;
+        }
+        lam = lm;
+        Uout = U;
+        return true;
+    };
+    const long check_every = std::max(k, 10L);
+    while (m < n) {
+        if (V.c == m) V.set_cols(std::min(n, 2 * m));
+        A.solve(V.col(m), w.data());
+        const double alpha = dotT(n, V.col(m), w.data());
+        for (long i = 0; i < n; ++i) w[i] -= alpha * V(i, m);
+        if (m > 0)
+            for (long i = 0; i < n; ++i) w[i] -= betas[m - 1] * V(i, m - 1);
+        for (int pass = 0; pass < 2; ++pass) {
+            tmp.assign(m + 1, 0.0);
+            gemv_op(V, m + 1, w.data(), tmp.data(), false);
+            sub_Kc(V, m + 1, tmp.data(), w.data());
+        }
+        alphas.push_back(alpha);
+        ++m;
+        double beta = nrm2(n, w.data());
+        if (beta <= 1e-13 * std::abs(alpha)) {
+            if (m >= n) {
+                betas.push_back(0.0);
+                break;
+            }
+            random_vec(w);
+            for (int pass = 0; pass < 2; ++pass) {
+                tmp.assign(m, 0.0);
+                gemv_op(V, m, w.data(), tmp.data(), false);
+                sub_Kc(V, m, tmp.data(), w.data());
+            }
+            beta = 0.0;
+            const double nw = nrm2(n, w.data());
+            for (auto& t : w) t /= nw;
+        } else {
+            for (auto& t : w) t /= beta;
+        }
+        if (m < n) {
+            betas.push_back(beta);
+            if (V.c == m) V.set_cols(std::min(n, 2 * m));
+            std::memcpy(V.col(m), w.data(), sizeof(double) * n);
+        }
+        if ((m % check_every == 0 || m == n) && ritz_converged()) return;
+    }
+    if (ritz_converged()) return;
+    throw SolverError("eigensolver: Lanczos did not converge");
+}
+
+// ----------------------------------------------------------- global basis ---
+// GlobalBasis (basis.hpp:28-64, basis.cpp:37-112). Hermitian image QR for the
+// complex case (the LS-optimal global check).
+constexpr uint8_t kColEigenvector = 0, kColInitialSolution = 1, kColCorrection = 2;
+constexpr double kInnerSafety = 0.25;  // basis.cpp:27
+
+struct BuildLogRow {
+    int system = 0, rhs = 0;
+    double init_relres = 0.0;
+    int iterations = 0;
+    bool appended = false;
+};
+
+template <class T> struct GlobalBasis {
+    Mat<T> V, Kimg, R, Ktil;
+    std::vector<uint8_t> markers;
+    long ku = 0;
+    std::vector<std::vector<int>> spaces;  // PerRhsSpaces (basis.hpp:68-70)
+    long cap = 0;                          // candidate cap (App. A10); 0 = unbounded
+
+    long cols() const { return V.c; }
+
+    void drop_column(long c) {
+        V.remove_col(c);
+        markers.erase(markers.begin() + c);
+        // Remap per-RHS indices (the reference leaves them stale).
+        for (auto& s : spaces) {
+            std::vector<int> out;
+            for (int idx : s) {
+                if (idx == c) continue;
+                out.push_back(idx > c ? idx - 1 : idx);
+            }
+            s = out;
+        }
+    }
+
+    // basis.cpp:37-76, with A_i V recomputed by the operator (variable D).
+    void refresh(const LinOp<T>& A) {
+        while (true) {
+            const long r = V.c, n = V.r;
+            Ktil = Mat<T>(n, r);
+            for (long j = 0; j < r; ++j) A.apply(V.col(j), Ktil.col(j));
+            const long a = std::min(ku, r);
+            Kimg = Mat<T>(n, r);
+            R = Mat<T>(r, r);
+            Mat<T> Qa(n, 0);
+            if (a > 0) {
+                Mat<T> Ka(n, a), Ra;
+                std::memcpy(Ka.col(0), Ktil.col(0), sizeof(T) * n * a);
+                thin_qr(Ka, Qa, Ra);
+                std::memcpy(Kimg.col(0), Qa.col(0), sizeof(T) * n * a);
+                for (long j = 0; j < a; ++j)
+                    for (long i = 0; i <= j; ++i) R(i, j) = Ra(i, j);
+            }
+            long deficient = -1;
+            if (r > a) {
+                Mat<T> B(n, r - a);
+                std::memcpy(B.col(0), Ktil.col(a), sizeof(T) * n * (r - a));
+                Mat<T> C(a, r - a);
+                for (long j = 0; j < r - a; ++j) {
+                    gemv_op(Qa, a, B.col(j), C.col(j), true);
+                    sub_Kc(Qa, a, C.col(j), B.col(j));
+                }
+                Mat<T> Qb, Rb;
+                thin_qr(B, Qb, Rb);
+                std::memcpy(Kimg.col(a), Qb.col(0), sizeof(T) * n * (r - a));
+                for (long j = 0; j < r - a; ++j) {
+                    for (long i = 0; i < a; ++i) R(i, a + j) = C(i, j);
+                    for (long i = 0; i <= j; ++i) R(a + i, a + j) = Rb(i, j);
+                }
+                for (long i = a; i < r; ++i)
+                    if (std::abs(cd(R(i, i))) <= 1e-12 * nrm2(n, Ktil.col(i))) {
+                        deficient = i;
+                        break;
+                    }
+            }
+            if (deficient < 0) return;
+            drop_column(deficient);
+        }
+    }
+
+    // basis.cpp:78-103; z = A_i y is passed in (variable D: no A_* shortcut).
+    bool append(const T* y, const T* z, uint8_t marker) {
+        const long n = V.r, r = V.c;
+        std::vector<T> c(r), c2(r), q(z, z + n);
+        gemv_op(Kimg, r, q.data(), c.data(), true);
+        sub_Kc(Kimg, r, c.data(), q.data());
+        gemv_op(Kimg, r, q.data(), c2.data(), true);
+        sub_Kc(Kimg, r, c2.data(), q.data());
+        for (long i = 0; i < r; ++i) c[i] += c2[i];
+        const double rho = nrm2(n, q.data());
+        if (rho <= 1e-12 * nrm2(n, z)) return false;
+        V.set_cols(r + 1);
+        std::memcpy(V.col(r), y, sizeof(T) * n);
+        Ktil.set_cols(r + 1);
+        std::memcpy(Ktil.col(r), z, sizeof(T) * n);
+        Kimg.set_cols(r + 1);
+        for (long i = 0; i < n; ++i) Kimg(i, r) = q[i] / rho;
+        Mat<T> R2(r + 1, r + 1);
+        for (long j = 0; j < r; ++j)
+            for (long i = 0; i <= j; ++i) R2(i, j) = R(i, j);
+        for (long i = 0; i < r; ++i) R2(i, r) = c[i];
+        R2(r, r) = T(rho);
+        R = R2;
+        markers.push_back(marker);
+        return true;
+    }
+
+    std::vector<T> projected_coordinates(const T* b) const {
+        const long r = V.c;
+        std::vector<T> w(r);
+        gemv_op(Kimg, r, b, w.data(), true);
+        for (long i = r - 1; i >= 0; --i) {
+            T s = w[i];
+            for (long j = i + 1; j < r; ++j) s -= R(i, j) * w[j];
+            w[i] = s / R(i, i);
+        }
+        return w;
+    }
+
+    std::vector<T> solve_projected(const T* b) const {
+        const long n = V.r, r = V.c;
+        std::vector<T> c = projected_coordinates(b), x(n, T(0));
+        for (long j = 0; j < r; ++j)
+            for (long i = 0; i < n; ++i) x[i] += V(i, j) * c[j];
+        return x;
+    }
+};
+
+// basis.cpp:114-134
+template <class T> void init_basis_from(GlobalBasis<T>& gb, const Mat<T>& U0, const Mat<T>& X0) {
+    const long n = U0.r, ku = U0.c, nrhs = X0.c;
+    gb.V = Mat<T>(n, ku + nrhs);
+    if (ku) std::memcpy(gb.V.col(0), U0.col(0), sizeof(T) * n * ku);
+    if (nrhs) std::memcpy(gb.V.col(ku), X0.col(0), sizeof(T) * n * nrhs);
+    gb.markers.assign(ku, kColEigenvector);
+    gb.markers.insert(gb.markers.end(), nrhs, kColInitialSolution);
+    gb.ku = ku;
+    gb.spaces.assign(nrhs, {});
+    for (long j = 0; j < nrhs; ++j) {
+        for (long i = 0; i < ku; ++i) gb.spaces[j].push_back(static_cast<int>(i));
+        gb.spaces[j].push_back(static_cast<int>(ku + j));
+    }
+}
+
+enum Method { kMinres = 0, kCG = 1 };
+
+template <class T> RecycledResult<T> inner_solve(int method, const LinOp<T>& A, const RecycleSpace<T>& rs,
+                                                 const T* rhs, double tol, long maxit, double scale);
+template <> inline RecycledResult<double> inner_solve<double>(int method, const LinOp<double>& A,
+                                                              const RecycleSpace<double>& rs,
+                                                              const double* rhs, double tol, long maxit,
+                                                              double scale) {
+    if (method == kMinres) return recycled_minres(A, rs, rhs, tol, maxit, scale);
+    return recycled_cg(A, rs, rhs, tol, maxit, scale);
+}
+template <> inline RecycledResult<cd> inner_solve<cd>(int method, const LinOp<cd>& A,
+                                                      const RecycleSpace<cd>& rs, const cd* rhs,
+                                                      double tol, long maxit, double scale) {
+    if (method == kMinres) throw ConfigError("MINRES is real-only (reference scope); use COCG");
+    return recycled_cg(A, rs, rhs, tol, maxit, scale);
+}
+
+struct ProcessStats {
+    long inner_iterations = 0, appends = 0;
+};
+
+// process_system (basis.cpp:157-207). B has one nonzero per column
+// (grid.cpp:146-158): b_j = bval[j] e_{bidx[j]}.
+template <class T>
+void process_system(GlobalBasis<T>& gb, const LinOp<T>& A, long nrhs, const long* bidx, const double* bval,
+                    double tol, int system_index, long maxit, int method, Mat<T>& X,
+                    std::vector<BuildLogRow>& log, ProcessStats& st) {
+    const long n = A.n;
+    if (maxit <= 0) maxit = 2 * n;
+    gb.refresh(A);
+    X = Mat<T>(n, nrhs);
+    log.clear();
+    st = ProcessStats();
+    std::vector<T> b(n, T(0)), rj(n);
+    for (long j = 0; j < nrhs; ++j) {
+        std::fill(b.begin(), b.end(), T(0));
+        b[bidx[j]] = T(bval[j]);
+        const double bnorm = nrm2(n, b.data());
+        const long r = gb.cols();
+        std::vector<T> w(r);
+        gemv_op(gb.Kimg, r, b.data(), w.data(), true);
+        rj = b;
+        sub_Kc(gb.Kimg, r, w.data(), rj.data());
+        BuildLogRow row;
+        row.system = system_index;
+        row.rhs = static_cast<int>(j);
+        row.init_relres = nrm2(n, rj.data()) / bnorm;
+        if (row.init_relres <= tol) {
+            auto x = gb.solve_projected(b.data());
+            std::memcpy(X.col(j), x.data(), sizeof(T) * n);
+        } else {
+            auto& idx = gb.spaces[j];
+            Mat<T> W(n, static_cast<long>(idx.size())), AW(n, static_cast<long>(idx.size()));
+            for (size_t t = 0; t < idx.size(); ++t) {
+                std::memcpy(W.col(t), gb.V.col(idx[t]), sizeof(T) * n);
+                std::memcpy(AW.col(t), gb.Ktil.col(idx[t]), sizeof(T) * n);
+            }
+            const RecycleSpace<T> rs = RecycleSpace<T>::from_raw(W, AW);
+            auto solved = inner_solve<T>(method, A, rs, rj.data(), kInnerSafety * tol, maxit, bnorm);
+            if (!solved.report.converged)
+                throw SolverError("process_system: correction solve failed at system " +
+                                  std::to_string(system_index) + ", rhs " + std::to_string(j));
+            auto xp = gb.solve_projected(b.data());
+            for (long i = 0; i < n; ++i) X(i, j) = solved.correction[i] + xp[i];
+            row.iterations = solved.report.iterations;
+            st.inner_iterations += row.iterations;
+            const bool room = gb.cap <= 0 || gb.cols() < gb.cap;
+            if (room && gb.append(solved.new_direction.data(), solved.image.data(), kColCorrection)) {
+                idx.push_back(static_cast<int>(gb.cols() - 1));
+                row.appended = true;
+                ++st.appends;
+            }
+        }
+        log.push_back(row);
+    }
+}
+
+}  // namespace orc
+
+// =============================================================== C ABI ===
+// Flat entry points for tests/ (ctypes). Scalars: dtype 0 = float64,
+// 1 = complex128 (interleaved re/im, numpy layout). Errors: return != 0 and
+// orc_last_error() holds the message (2 config, 3 solver).
+using namespace orc;
+
+namespace {
+thread_local std::string g_err;
+
+struct OpHandle {
+    int dtype = 0;
+    bool grid = false;
+    GridOp g;
+    std::vector<double> dense_r;  // dense real matrix (tests)
+    std::vector<cd> dense_c;
+    long n = 0;
+    std::unique_ptr<BandChol> chol;
+    std::vector<double> chol_dense;  // dense Cholesky factor (tests)
+    LinOp<double> lr;
+    LinOp<cd> lc;
+};
+
+
+struct BasisHandle {
+    int dtype = 0;
+    GlobalBasis<double> r;
+    GlobalBasis<cd> c;
+};
+
+struct RSHandle {
+    int dtype = 0;
+    RecycleSpace<double> r;
+    RecycleSpace<cd> c;
+};
+
+template <class F> int guard(F&& f) {
+    try {
+        f();
+        return 0;
+    } catch (const ConfigError& e) {
+        g_err = e.what();
+        return 2;
+    } catch (const SolverError& e) {
+        g_err = e.what();
+        return 3;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return 1;
+    }
+}
+
+void dense_solve_setup(OpHandle* h) {
+    // Cholesky of a dense real SPD test matrix (SimplicialLDLT stand-in).
+    const long n = h->n;
+    h->chol_dense = h->dense_r;
+    auto& L = h->chol_dense;
+    for (long j = 0; j < n; ++j) {
+        double s = L[j + j * n];
+        for (long k = 0; k < j; ++k) s -= L[j + k * n] * L[j + k * n];
+        if (!(s > 0.0)) throw SolverError("eigensolver: factorization of A failed (not SPD?)");
+        const double ljj = std::sqrt(s);
+        L[j + j * n] = ljj;
+        for (long i = j + 1; i < n; ++i) {
+            double v = L[i + j * n];
+            for (long k = 0; k < j; ++k) v -= L[i + k * n] * L[j + k * n];
+            L[i + j * n] = v / ljj;
+        }
+    }
+    h->lr.solve = [h, n](const double* b, double* x) {
+        const auto& L = h->chol_dense;
+        for (long i = 0; i < n; ++i) {
+            double s = b[i];
+            for (long k = 0; k < i; ++k) s -= L[i + k * n] * x[k];
+            x[i] = s / L[i + i * n];
+        }
+        for (long i = n - 1; i >= 0; --i) {
+            double s = x[i];
+            for (long k = i + 1; k < n; ++k) s -= L[k + i * n] * x[k];
+            x[i] = s / L[i + i * n];
+        }
+    };
+}
+
+void grid_solve_setup(OpHandle* h) {
+    const GridOp& g = h->g;
+    const long bw = g.d == 2 ? g.N[0] : g.N[0] * g.N[1];
+    if (static_cast<double>(g.n) * (bw + 1) <= 6.0e7) {
+        h->chol = std::make_unique<BandChol>();
+        if (!h->chol->build(g)) throw SolverError("eigensolver: factorization of A failed (not SPD?)");
+        BandChol* c = h->chol.get();
+        h->lr.solve = [c](const double* b, double* x) { c->solve(b, x); };
+    } else {
+        // Large 3D grids: inner CG to 1e-14 (no sparse direct solver).
+        LinOp<double>* A = &h->lr;
+        h->lr.solve = [A](const double* b, double* x) {
+            RecycleSpace<double> none;
+            none.U = Mat<double>(A->n, 0);
+            none.K = Mat<double>(A->n, 0);
+            auto res = recycled_cg(*A, none, b, 1e-14, 20 * A->n, 0.0);
+            std::memcpy(x, res.correction.data(), sizeof(double) * A->n);
+        };
+    }
+}
+
+void fill_report(const SolveReport& rep, int* its, int* conv, double* hist, long hist_cap, long* hist_len,
+                 double* corr_norm) {
+    if (its) *its = rep.iterations;
+    if (conv) *conv = rep.converged ? 1 : 0;
+    if (hist_len) *hist_len = static_cast<long>(rep.hist.size());
+    if (hist)
+        for (long i = 0; i < std::min<long>(hist_cap, static_cast<long>(rep.hist.size())); ++i)
+            hist[i] = rep.hist[i];
+    if (corr_norm) *corr_norm = rep.correction_norm;
+}
+
+template <class T> Mat<T> mat_from(const void* p, long r, long c) {
+    Mat<T> M(r, c);
+    if (r * c != 0) std::memcpy(M.a.data(), p, sizeof(T) * r * c);
+    return M;
+}
+template <class T> void mat_to(const Mat<T>& M, void* p) {
+    if (M.r * M.c != 0) std::memcpy(p, M.a.data(), sizeof(T) * M.r * M.c);
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* orc_last_error() { return g_err.c_str(); }
+
+void orc_normal_stream(uint64_t seed, long count, double* out) {
+    // NormalStream (config.cpp:249-271): xorshift64* + Box-Muller, spare kept.
+    uint64_t state = seed ? seed : 0x9e3779b97f4a7c15ull;
+    bool have = false;
+    double spare = 0.0;
+    for (long t = 0; t < count; ++t) {
+        if (have) {
+            have = false;
+            out[t] = spare;
+            continue;
+        }
+        auto uniform = [&]() {
+            state ^= state >> 12;
+            state ^= state << 25;
+            state ^= state >> 27;
+            const uint64_t z = state * 0x2545f4914f6cdd1dull;
+            return (static_cast<double>(z >> 11) + 1.0) * 0x1.0p-53;
+        };
+        const double u1 = uniform();
+        const double u2 = uniform();
+        const double radius = std::sqrt(-2.0 * std::log(u1));
+        const double angle = 2.0 * M_PI * u2;
+        spare = radius * std::sin(angle);
+        have = true;
+        out[t] = radius * std::cos(angle);
+    }
+}
+
+void* orc_op_grid(int dtype, int d, const long* N, double robin_face, double shift, const double* D,
+                  const double* mu) {
+    auto* h = new OpHandle();
+    h->dtype = dtype;
+    h->grid = true;
+    GridOp& g = h->g;
+    g.d = d;
+    g.N[0] = N[0];
+    g.N[1] = N[1];
+    g.N[2] = d == 3 ? N[2] : 1;
+    g.n = g.N[0] * g.N[1] * g.N[2];
+    g.robin_face = robin_face;
+    g.shift = shift;
+    g.D.assign(D, D + g.n);
+    g.mu.assign(mu, mu + g.n);
+    h->n = g.n;
+    h->lr.n = h->lc.n = g.n;
+    h->lr.apply = [h](const double* x, double* y) { h->g.apply_one<double>(x, y); };
+    h->lc.apply = [h](const cd* x, cd* y) { h->g.apply_one<cd>(x, y); };
+    h->lr.lam_max = h->lc.lam_max = g.gershgorin();
+    return h;
+}
+
+void* orc_op_dense(int dtype, long n, const void* A) {
+    auto* h = new OpHandle();
+    h->dtype = dtype;
+    h->n = n;
+    h->lr.n = h->lc.n = n;
+    if (dtype == 0) {
+        h->dense_r.assign(static_cast<const double*>(A), static_cast<const double*>(A) + n * n);
+        h->lr.apply = [h, n](const double* x, double* y) {
+            for (long i = 0; i < n; ++i) y[i] = 0.0;
+            for (long j = 0; j < n; ++j)
+                for (long i = 0; i < n; ++i) y[i] += h->dense_r[i + j * n] * x[j];
+        };
+        double lm = 0.0;
+        for (long i = 0; i < n; ++i) {
+            double s = 0.0;
+            for (long j = 0; j < n; ++j) s += std::abs(h->dense_r[i + j * n]);
+            lm = std::max(lm, s);
+        }
+        h->lr.lam_max = lm;
+    } else {
+        h->dense_c.assign(static_cast<const cd*>(A), static_cast<const cd*>(A) + n * n);
+        h->lc.apply = [h, n](const cd* x, cd* y) {
+            for (long i = 0; i < n; ++i) y[i] = 0.0;
+            for (long j = 0; j < n; ++j)
+                for (long i = 0; i < n; ++i) y[i] += h->dense_c[i + j * n] * x[j];
+        };
+    }
+    return h;
+}
+
+double orc_op_lam_max(void* op) { return static_cast<OpHandle*>(op)->lr.lam_max; }
+
+int orc_op_apply(void* op, const void* x, void* y, long ncols) {
+    auto* h = static_cast<OpHandle*>(op);
+    return guard([&] {
+        for (long j = 0; j < ncols; ++j) {
+            if (h->dtype == 0)
+                h->lr.apply(static_cast<const double*>(x) + j * h->n, static_cast<double*>(y) + j * h->n);
+            else
+                h->lc.apply(static_cast<const cd*>(x) + j * h->n, static_cast<cd*>(y) + j * h->n);
+        }
+    });
+}
+
+void orc_free_op(void* op) { delete static_cast<OpHandle*>(op); }
+
+int orc_minres(void* op, const double* b, double tol, long maxit, double* x, int* its, int* conv, double* hist,
+               long hist_cap, long* hist_len) {
+    auto* h = static_cast<OpHandle*>(op);
+    return guard([&] {
+        std::vector<double> xv;
+        SolveReport rep;
+        minres_core(h->lr, b, tol, maxit, 0.0, nullptr, xv, rep);
+        std::memcpy(x, xv.data(), sizeof(double) * h->n);
+        fill_report(rep, its, conv, hist, hist_cap, hist_len, nullptr);
+    });
+}
+
+void* orc_rs_from_raw(int dtype, long n, long c, const void* W, const void* AW) {
+    auto* h = new RSHandle();
+    h->dtype = dtype;
+    if (dtype == 0)
+        h->r = RecycleSpace<double>::from_raw(mat_from<double>(W, n, c), mat_from<double>(AW, n, c));
+    else
+        h->c = RecycleSpace<cd>::from_raw(mat_from<cd>(W, n, c), mat_from<cd>(AW, n, c));
+    return h;
+}
+int orc_rs_append(void* rs, const void* u, const void* k) {
+    auto* h = static_cast<RSHandle*>(rs);
+    if (h->dtype == 0) return h->r.append(static_cast<const double*>(u), static_cast<const double*>(k)) ? 1 : 0;
+    return h->c.append(static_cast<const cd*>(u), static_cast<const cd*>(k)) ? 1 : 0;
+}
+long orc_rs_cols(void* rs) {
+    auto* h = static_cast<RSHandle*>(rs);
+    return h->dtype == 0 ? h->r.cols() : h->c.cols();
+}
+void orc_rs_get(void* rs, void* U, void* K) {
+    auto* h = static_cast<RSHandle*>(rs);
+    if (h->dtype == 0) {
+        mat_to(h->r.U, U);
+        mat_to(h->r.K, K);
+    } else {
+        mat_to(h->c.U, U);
+        mat_to(h->c.K, K);
+    }
+}
+void orc_rs_initial_guess(void* rs, const void* b, void* z, void* r) {
+    auto* h = static_cast<RSHandle*>(rs);
+    if (h->dtype == 0)
+        initial_guess(h->r, static_cast<const double*>(b), static_cast<double*>(z), static_cast<double*>(r));
+    else
+        initial_guess(h->c, static_cast<const cd*>(b), static_cast<cd*>(z), static_cast<cd*>(r));
+}
+void orc_free_rs(void* rs) { delete static_cast<RSHandle*>(rs); }
+
+// method 0 = recycled MINRES (reference), 1 = recycled CG/COCG. rs may be NULL.
+int orc_recycled_solve(int method, void* op, void* rs, const void* rhs, double tol, long maxit, double scale,
+                       void* corr, void* newdir, void* image, int* its, int* conv, double* hist, long hist_cap,
+                       long* hist_len, double* corr_norm) {
+    auto* h = static_cast<OpHandle*>(op);
+    auto* r = static_cast<RSHandle*>(rs);
+    return guard([&] {
+        const long n = h->n;
+        if (h->dtype == 0) {
+            RecycleSpace<double> empty;
+            empty.U = Mat<double>(n, 0);
+            empty.K = Mat<double>(n, 0);
+            const RecycleSpace<double>& sp = r ? r->r : empty;
+            auto res = inner_solve<double>(method, h->lr, sp, static_cast<const double*>(rhs), tol, maxit, scale);
+            std::memcpy(corr, res.correction.data(), sizeof(double) * n);
+            std::memcpy(newdir, res.new_direction.data(), sizeof(double) * n);
+            std::memcpy(image, res.image.data(), sizeof(double) * n);
+            fill_report(res.report, its, conv, hist, hist_cap, hist_len, corr_norm);
+        } else {
+            RecycleSpace<cd> empty;
+            empty.U = Mat<cd>(n, 0);
+            empty.K = Mat<cd>(n, 0);
+            const RecycleSpace<cd>& sp = r ? r->c : empty;
+            auto res = inner_solve<cd>(method, h->lc, sp, static_cast<const cd*>(rhs), tol, maxit, scale);
+            std::memcpy(corr, res.correction.data(), sizeof(cd) * n);
+            std::memcpy(newdir, res.new_direction.data(), sizeof(cd) * n);
+            std::memcpy(image, res.image.data(), sizeof(cd) * n);
+            fill_report(res.report, its, conv, hist, hist_cap, hist_len, corr_norm);
+        }
+    });
+}
+
+int orc_eigs(void* op, long k, double tol, double* lam, double* U) {
+    auto* h = static_cast<OpHandle*>(op);
+    return guard([&] {
+        if (!h->lr.solve) {
+            if (h->grid)
+                grid_solve_setup(h);
+            else
+                dense_solve_setup(h);
+        }
+        std::vector<double> lm;
+        Mat<double> Uo;
+        smallest_eigenpairs(h->lr, k, tol, lm, Uo);
+        std::memcpy(lam, lm.data(), sizeof(double) * k);
+        mat_to(Uo, U);
+    });
+}
+
+void* orc_basis_from(int dtype, long n, long ku, long nrhs, const void* U0, const void* X0, long cap) {
+    auto* h = new BasisHandle();
+    h->dtype = dtype;
+    if (dtype == 0) {
+        init_basis_from(h->r, mat_from<double>(U0, n, ku), mat_from<double>(X0, n, nrhs));
+        h->r.cap = cap;
+    } else {
+        init_basis_from(h->c, mat_from<cd>(U0, n, ku), mat_from<cd>(X0, n, nrhs));
+        h->c.cap = cap;
+    }
+    return h;
+}
+void orc_free_basis(void* b) { delete static_cast<BasisHandle*>(b); }
+long orc_basis_cols(void* b) {
+    auto* h = static_cast<BasisHandle*>(b);
+    return h->dtype == 0 ? h->r.cols() : h->c.cols();
+}
+long orc_basis_ku(void* b) {
+    auto* h = static_cast<BasisHandle*>(b);
+    return h->dtype == 0 ? h->r.ku : h->c.ku;
+}
+// which: 0 V, 1 K_img, 2 R, 3 K~ (A_i V)
+int orc_basis_get(void* b, int which, void* out) {
+    auto* h = static_cast<BasisHandle*>(b);
+    return guard([&] {
+        if (h->dtype == 0) {
+            const Mat<double>* m[4] = {&h->r.V, &h->r.Kimg, &h->r.R, &h->r.Ktil};
+            mat_to(*m[which], out);
+        } else {
+            const Mat<cd>* m[4] = {&h->c.V, &h->c.Kimg, &h->c.R, &h->c.Ktil};
+            mat_to(*m[which], out);
+        }
+    });
+}
+void orc_basis_markers(void* b, uint8_t* out) {
+    auto* h = static_cast<BasisHandle*>(b);
+    const auto& mk = h->dtype == 0 ? h->r.markers : h->c.markers;
+    std::memcpy(out, mk.data(), mk.size());
+}
+long orc_basis_space(void* b, long j, int* out) {
+    auto* h = static_cast<BasisHandle*>(b);
+    const auto& sp = h->dtype == 0 ? h->r.spaces : h->c.spaces;
+    if (j < 0 || j >= static_cast<long>(sp.size())) return -1;
+    if (out)
+        for (size_t t = 0; t < sp[j].size(); ++t) out[t] = sp[j][t];
+    return static_cast<long>(sp[j].size());
+}
+int orc_basis_refresh(void* b, void* op) {
+    auto* h = static_cast<BasisHandle*>(b);
+    auto* o = static_cast<OpHandle*>(op);
+    return guard([&] {
+        if (h->dtype == 0)
+            h->r.refresh(o->lr);
+        else
+            h->c.refresh(o->lc);
+    });
+}
+int orc_basis_append(void* b, const void* y, const void* z, int marker) {
+    auto* h = static_cast<BasisHandle*>(b);
+    if (h->dtype == 0)
+        return h->r.append(static_cast<const double*>(y), static_cast<const double*>(z), static_cast<uint8_t>(marker))
+                   ? 1
+                   : 0;
+    return h->c.append(static_cast<const cd*>(y), static_cast<const cd*>(z), static_cast<uint8_t>(marker)) ? 1 : 0;
+}
+void orc_basis_solve_projected(void* b, const void* rhs, void* x, void* coords) {
+    auto* h = static_cast<BasisHandle*>(b);
+    if (h->dtype == 0) {
+        auto xv = h->r.solve_projected(static_cast<const double*>(rhs));
+        std::memcpy(x, xv.data(), sizeof(double) * xv.size());
+        if (coords) {
+            auto c = h->r.projected_coordinates(static_cast<const double*>(rhs));
+            std::memcpy(coords, c.data(), sizeof(double) * c.size());
+        }
+    } else {
+        auto xv = h->c.solve_projected(static_cast<const cd*>(rhs));
+        std::memcpy(x, xv.data(), sizeof(cd) * xv.size());
+        if (coords) {
+            auto c = h->c.projected_coordinates(static_cast<const cd*>(rhs));
+            std::memcpy(coords, c.data(), sizeof(cd) * c.size());
+        }
+    }
+}
+
+// log: nrhs rows x 5 doubles {system, rhs, init_relres, iterations, appended}
+int orc_process_system(void* b, void* op, long nrhs, const long* bidx, const double* bval, double tol,
+                       int system_index, long maxit, int method, void* X, double* log, long* inner_its,
+                       long* appends) {
+    auto* h = static_cast<BasisHandle*>(b);
+    auto* o = static_cast<OpHandle*>(op);
+    return guard([&] {
+        std::vector<BuildLogRow> lg;
+        ProcessStats st;
+        if (h->dtype == 0) {
+            Mat<double> Xm;
+            process_system(h->r, o->lr, nrhs, bidx, bval, tol, system_index, maxit, method, Xm, lg, st);
+            mat_to(Xm, X);
+        } else {
+            Mat<cd> Xm;
+            process_system(h->c, o->lc, nrhs, bidx, bval, tol, system_index, maxit, method, Xm, lg, st);
+            mat_to(Xm, X);
+        }
+        for (size_t t = 0; t < lg.size(); ++t) {
+            log[5 * t + 0] = lg[t].system;
+            log[5 * t + 1] = lg[t].rhs;
+            log[5 * t + 2] = lg[t].init_relres;
+            log[5 * t + 3] = lg[t].iterations;
+            log[5 * t + 4] = lg[t].appended ? 1.0 : 0.0;
+        }
+        if (inner_its) *inner_its = st.inner_iterations;
+        if (appends) *appends = st.appends;
+    });
+}
+
+// X0 solves of init_basis (basis.cpp:141-149): method 0 MINRES, 1 CG/COCG.
+int orc_initial_solutions(void* op, long nrhs, const long* bidx, const double* bval, double tol, int method,
+                          void* X0, long* total_its) {
+    auto* h = static_cast<OpHandle*>(op);
+    return guard([&] {
+        const long n = h->n;
+        const long maxit = 2 * n;
+        long tot = 0;
+        for (long j = 0; j < nrhs; ++j) {
+            if (h->dtype == 0) {
+                std::vector<double> b(n, 0.0);
+                b[bidx[j]] = bval[j];
+                RecycleSpace<double> none;
+                none.U = Mat<double>(n, 0);
+                none.K = Mat<double>(n, 0);
+                std::vector<double> x;
+                SolveReport rep;
+                if (method == kMinres) {
+                    minres_core(h->lr, b.data(), kInnerSafety * tol, maxit, 0.0, nullptr, x, rep);
+                } else {
+                    auto res = recycled_cg(h->lr, none, b.data(), kInnerSafety * tol, maxit, 0.0);
+                    x = res.correction;
+                    rep = res.report;
+                }
+                if (!rep.converged)
+                    throw SolverError("init_basis: solver failed on initial solution column " + std::to_string(j));
+                std::memcpy(static_cast<double*>(X0) + j * n, x.data(), sizeof(double) * n);
+                tot += rep.iterations;
+            } else {
+                std::vector<cd> b(n, cd(0));
+                b[bidx[j]] = bval[j];
+                RecycleSpace<cd> none;
+                none.U = Mat<cd>(n, 0);
+                none.K = Mat<cd>(n, 0);
+                auto res = recycled_cg(h->lc, none, b.data(), kInnerSafety * tol, maxit, 0.0);
+                if (!res.report.converged)
+                    throw SolverError("init_basis: solver failed on initial solution column " + std::to_string(j));
+                std::memcpy(static_cast<cd*>(X0) + j * n, res.correction.data(), sizeof(cd) * n);
+                tot += res.report.iterations;
+            }
+        }
+        if (total_its) *total_its = tot;
+    });
+}
+
+int orc_thin_qr(int dtype, long n, long m, const void* A, void* Q, void* R) {
+    return guard([&] {
+        if (dtype == 0) {
+            Mat<double> q, r;
+            thin_qr(mat_from<double>(A, n, m), q, r);
+            mat_to(q, Q);
+            mat_to(r, R);
+        } else {
+            Mat<cd> q, r;
+            thin_qr(mat_from<cd>(A, n, m), q, r);
+            mat_to(q, Q);
+            mat_to(r, R);
+        }
+    });
+}
+
+// RRQR compression: rank, permutation, |R_ii|, Q (n x rank) of the retained span.
+int orc_qrcp(int dtype, long n, long m, const void* A, double tol, int normalize, long* rank, long* perm,
+             double* rdiag, void* Q) {
+    return guard([&] {
+        std::vector<long> pv;
+        std::vector<double> rd;
+        if (dtype == 0) {
+            Mat<double> R, Qk;
+            *rank = qrcp(mat_from<double>(A, n, m), tol, pv, R, Qk, rd, normalize != 0);
+            if (Q) mat_to(Qk, Q);
+        } else {
+            Mat<cd> R, Qk;
+            *rank = qrcp(mat_from<cd>(A, n, m), tol, pv, R, Qk, rd, normalize != 0);
+            if (Q) mat_to(Qk, Q);
+        }
+        for (long j = 0; j < m; ++j) perm[j] = pv[j];
+        for (size_t j = 0; j < rd.size(); ++j) rdiag[j] = rd[j];
+    });
+}
+
+}  // extern "C"
