@@ -1,0 +1,128 @@
+/*
+ * romdot_b200 -- C ABI of the B200-native recycled-Krylov global-basis builder.
+ *
+ * Plain pointers and sizes only; no torch, Eigen or CUDA types cross this
+ * boundary. Every entry point returns an int status:
+ *   0 OK, 2 config error (reference ConfigError), 3 solver error (reference
+ *   SolverError: non-convergence, breakdown), 4 IO error, 5 CUDA error,
+ *   1 other. rd_last_error() returns the message of the last failure on the
+ *   calling thread. No C++ exception crosses this boundary.
+ *
+ * dtype: 0 = float64 (SPD systems, omega = 0), 1 = complex128 (interleaved
+ * re/im; complex-symmetric systems, omega != 0).
+ * where: 0 = host pointers (copied in / out inside the call),
+ *        1 = device pointers (borrowed, never freed; stream-ordered).
+ * Matrices are column-major with leading dimension n (the node count).
+ *
+ * The reference interface each entry point replaces is cited per function
+ * (paths relative to the reference repository's proj/ directory).
+ */
+#ifndef ROMDOT_B200_H
+#define ROMDOT_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct rd_ctx rd_ctx;     /* device, stream, reduction workspace */
+typedef struct rd_op rd_op;       /* Schur operator A~(p) on the device */
+typedef struct rd_basis rd_basis; /* GlobalBasis + PerRhsSpaces on the device */
+
+typedef struct rd_report {
+    int iterations;      /* SolveReport::iterations   (include/romdot/krylov.hpp:10-15) */
+    int converged;       /* SolveReport::converged */
+    double correction_norm;
+    double final_relres;
+} rd_report;
+
+/* ------------------------------------------------------------ context --- */
+int rd_ctx_create(int device, rd_ctx** out);
+void rd_ctx_destroy(rd_ctx* ctx);
+const char* rd_last_error(void);
+int rd_ctx_sync(rd_ctx* ctx);
+/* Device time (ms) between the last two rd_ctx_mark() calls (CUDA events on the ctx stream). */
+int rd_ctx_mark(rd_ctx* ctx);
+double rd_ctx_elapsed_ms(rd_ctx* ctx);
+/* Number of this library's kernel launches issued on the context so far. */
+long rd_ctx_launches(rd_ctx* ctx);
+/* Raw stream handle (cudaStream_t) for interop. */
+void* rd_ctx_stream(rd_ctx* ctx);
+
+/* ----------------------------------------------------------- operator --- */
+/* Replaces SchurOperator (include/romdot/grid.hpp:100-114, src/grid.cpp:86-105)
+ * and the LinOp plug-in (include/romdot/types.hpp:18). d = 2 or 3; N[d-1] is
+ * the Robin axis. robin_face = Dbg/(1+rho), rho = 2*A*Dbg/h.                 */
+int rd_op_create(rd_ctx* ctx, int d, const long* N, double robin_face, rd_op** out);
+void rd_op_destroy(rd_op* op);
+/* Per-system coefficient fields: node D, h^2 mu_a, shift = h^2 omega/nu.
+ * Replaces the mu_scaled argument of SchurOperator::apply (src/grid.cpp:95). */
+int rd_op_set_fields(rd_op* op, const double* D, const double* mu, double shift, int where);
+/* y[:, j] = A x[:, j], j < ncols (SchurOperator::apply, src/grid.cpp:95-97). */
+int rd_op_apply(rd_op* op, int dtype, const void* x, void* y, long ncols, int where);
+double rd_op_lam_max(rd_op* op); /* Gershgorin bound (src/krylov.cpp:190-195) */
+
+/* ------------------------------------------------------------ solvers --- */
+/* Recycled CG / COCG on the correction equation with recycle space (U, K),
+ * A U = K, K^T K = I (bilinear for complex). c = 0: plain CG / COCG.
+ * Replaces recycled_minres (include/romdot/krylov.hpp:57-58, src/krylov.cpp:147-179)
+ * and minres (krylov.hpp:44): convergence ||rhs - A g|| / rhs_scale <= tol.
+ * Outputs: g (correction), y (new direction y_m), image (A y_m).
+ * hist (optional, hist_cap entries) receives the relative residual history.  */
+int rd_recycled_solve(rd_op* op, int dtype, const void* U, const void* K, long c, const void* rhs, double tol,
+                      long maxit, double rhs_scale, void* g, void* y, void* image, rd_report* rep, double* hist,
+                      long hist_cap, int where);
+/* RecycleSpace::from_raw (src/krylov.cpp:106-115): K = orth(AW) (bilinear for
+ * complex), U = W R^-1. Writes U, K (n x c). */
+int rd_recycle_space_from_raw(rd_ctx* ctx, int dtype, long n, long c, const void* W, const void* AW, void* U,
+                              void* K, int where);
+
+/* X0 of init_basis (src/basis.cpp:141-149): one CG/COCG solve per column of
+ * B_concat (one nonzero per column: bidx, bval) at 0.25 * tol, maxit = 2n.   */
+int rd_initial_solutions(rd_op* op, int dtype, long nrhs, const long* bidx, const double* bval, double tol,
+                         void* X0, int where, long* total_iterations);
+
+/* smallest_eigenpairs (src/krylov.cpp:181-280): k smallest eigenpairs of the
+ * real SPD operator (fields at omega = 0), shift-invert Lanczos with inner CG. */
+int rd_smallest_eigenpairs(rd_op* op, long k, double tol, double* lambda, void* U, int where);
+
+/* -------------------------------------------------------- global basis --- */
+/* init_basis_from (src/basis.cpp:114-134): V = [U0, X0], markers, per-RHS
+ * spaces. cap = candidate-column cap (0 = unbounded).                       */
+int rd_basis_create(rd_ctx* ctx, int dtype, long n, long ku, long nrhs, const void* U0, const void* X0, long cap,
+                    int where, rd_basis** out);
+void rd_basis_destroy(rd_basis* b);
+long rd_basis_cols(rd_basis* b);
+long rd_basis_eig_block(rd_basis* b);
+/* which: 0 V, 1 K_img, 2 R (cols x cols), 3 W = V R^-1. Host output. */
+int rd_basis_get(rd_basis* b, int which, void* out);
+/* Device pointer of V / K_img / W (valid until the next call that grows the basis). */
+void* rd_basis_device_ptr(rd_basis* b, int which);
+int rd_basis_markers(rd_basis* b, uint8_t* out);
+long rd_basis_space(rd_basis* b, long j, int* out);
+/* GlobalBasis::refresh (src/basis.cpp:37-76) for the operator's current fields. */
+int rd_basis_refresh(rd_basis* b, rd_op* op);
+/* GlobalBasis::append (src/basis.cpp:78-103); z = A_i y. *appended = 0|1.   */
+int rd_basis_append(rd_basis* b, const void* y, const void* z, int marker, int where, int* appended);
+/* solve_projected / projected_coordinates (src/basis.cpp:105-112).          */
+int rd_basis_solve_projected(rd_basis* b, const void* rhs, void* x, void* coords, int where);
+/* process_system (src/basis.cpp:157-207). log: nrhs rows x 5 doubles
+ * {system, rhs, init_relres, iterations, appended} (BuildLogRow, basis.hpp:17-23).
+ * X (n x nrhs) may be NULL.                                                  */
+int rd_process_system(rd_basis* b, rd_op* op, long nrhs, const long* bidx, const double* bval, double tol,
+                      int system_index, long maxit, void* X, int where, double* log, long* inner_iterations,
+                      long* appends);
+
+/* ---------------------------------------------------------- compression --- */
+/* Rank-revealing compression of the n x m candidate basis (acceptance.cpp:368-383
+ * truncation rule, BASELINE RRQR): column-normalised (if normalize) pivoted QR
+ * at relative tolerance tol. Outputs rank, perm (m), rdiag (m), Q (n x rank). */
+int rd_rrqr(rd_ctx* ctx, int dtype, long n, long m, const void* A, double tol, int normalize, long* rank,
+            long* perm, double* rdiag, void* Q, int where);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* ROMDOT_B200_H */

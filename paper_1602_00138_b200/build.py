@@ -1,0 +1,46 @@
+"""Build the in-tree CUDA library libromdot_b200.so for sm_100a (nvcc)."""
+import os
+import subprocess
+import sys
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(HERE)
+SO = os.path.join(HERE, "libromdot_b200.so")
+SRCS = [os.path.join(HERE, "csrc", f) for f in ("romdot.cu",)]
+DEPS = SRCS + [os.path.join(HERE, "csrc", f) for f in ("common.cuh", "kernels.cuh", "dense.cuh")] + \
+    [os.path.join(ROOT, "include", "romdot_b200.h")]
+
+NVCC_FLAGS = ["-O3", "-std=c++17", "-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo",
+              "-Xcompiler", "-fPIC", "-shared", "--expt-relaxed-constexpr", "-Xptxas", "-v"]
+
+
+def nvcc():
+    c = os.environ.get("NVCC")
+    if c:
+        return c
+    return "/usr/local/cuda/bin/nvcc" if os.path.exists("/usr/local/cuda/bin/nvcc") else "nvcc"
+
+
+def needs_build() -> bool:
+    if not os.path.exists(SO):
+        return True
+    t = os.path.getmtime(SO)
+    return any(os.path.getmtime(d) > t for d in DEPS if os.path.exists(d))
+
+
+def build(force: bool = False, verbose: bool = False) -> str:
+    if force or needs_build():
+        cmd = [nvcc()] + NVCC_FLAGS + ["-o", SO] + SRCS
+        res = subprocess.run(cmd, capture_output=True, text=True)
+        if res.returncode != 0:
+            sys.stderr.write(res.stdout + res.stderr)
+            raise RuntimeError("nvcc failed building libromdot_b200.so")
+        with open(os.path.join(HERE, "csrc", "ptxas.log"), "w") as f:
+            f.write(res.stderr)
+        if verbose:
+            sys.stderr.write(res.stderr)
+    return SO
+
+
+if __name__ == "__main__":
+    print(build(force="--force" in sys.argv, verbose=True))

@@ -1,0 +1,494 @@
+// Device kernels of the recycled-Krylov basis build (sm_100a).
+//
+//  K1  stencil apply           y = A(p) x, 5/7-point variable-D Schur operator
+//                              (restates SchurOperator::apply, grid.cpp:95-97,
+//                              generalised per SURVEY.md App. A), multi-column
+//                              with an optional column gather (A_i U_j).
+//  K2  cg_stencil_dots         fused inner-iteration head: w = A r, the merged
+//                              reduction {r^T r, r^T w, r^H r} and the scalar
+//                              recurrence (alpha, beta, convergence, stagnation)
+//                              in the last block -- one grid reduction.
+//  K3  ts_T / ts_NT / ts_N     tall-skinny recycle-space projections that stream
+//                              the n x c basis once per call: c = op(K)^T x,
+//                              fused {x' = x - K c1 ; c2 = op(K)^T x'}, and
+//                              x - K c. op = T (bilinear) or H (Hermitian).
+//  K4  cg_update               q = w' - K c2 fused with the CG vector updates.
+//  plus small vector kernels (norms, gathers, column scaling).
+#pragma once
+
+#include "common.cuh"
+
+namespace rd {
+
+// ----------------------------------------------------------- operator ---
+struct OpDev {
+    int d;
+    int N0, N1, N2;
+    long n;
+    double robin_face;  // Dbg / (1 + rho)
+    double shift;       // h^2 omega/nu (imaginary diagonal)
+    const double* D;
+    const double* mu;
+};
+
+__device__ __forceinline__ double hmean(double a, double b) { return 2.0 * (a * b) / (a + b); }
+
+template <class T> __device__ __forceinline__ T diag_apply(double dr, double shift, T x);
+template <> __device__ __forceinline__ double diag_apply<double>(double dr, double, double x) { return dr * x; }
+template <> __device__ __forceinline__ cplx diag_apply<cplx>(double dr, double s, cplx x) {
+    return make_double2(dr * x.x - s * x.y, dr * x.y + s * x.x);
+}
+template <class T> __device__ __forceinline__ T axpy_real(double a, T x, T acc);
+template <> __device__ __forceinline__ double axpy_real<double>(double a, double x, double acc) { return acc + a * x; }
+template <> __device__ __forceinline__ cplx axpy_real<cplx>(double a, cplx x, cplx acc) {
+    return make_double2(acc.x + a * x.x, acc.y + a * x.y);
+}
+
+// Row p of A x. Face order (axis 0 -, +, axis 1 -, +, axis 2 -, +) matches the
+// oracle (the CPU checker under oracle/, GridOp::apply_one).
+template <class T>
+__device__ __forceinline__ T stencil_row(const OpDev& op, const T* __restrict__ x, long p, int i, int j, int k) {
+    const double* __restrict__ D = op.D;
+    const double Dp = __ldg(D + p);
+    double diag = 0.0;
+    T acc = Sc<T>::zero();
+    // axis 0 (lateral, Dirichlet ghosts)
+    if (i > 0) {
+        const double f = hmean(Dp, __ldg(D + p - 1));
+        diag += f;
+        acc = axpy_real(f, x[p - 1], acc);
+    } else {
+        diag += Dp;
+    }
+    if (i < op.N0 - 1) {
+        const double f = hmean(Dp, __ldg(D + p + 1));
+        diag += f;
+        acc = axpy_real(f, x[p + 1], acc);
+    } else {
+        diag += Dp;
+    }
+    // axis 1
+    const long s1 = op.N0;
+    const bool robin1 = (op.d == 2);
+    if (j > 0) {
+        const double f = hmean(Dp, __ldg(D + p - s1));
+        diag += f;
+        acc = axpy_real(f, x[p - s1], acc);
+    } else {
+        diag += robin1 ? op.robin_face : Dp;
+    }
+    if (j < op.N1 - 1) {
+        const double f = hmean(Dp, __ldg(D + p + s1));
+        diag += f;
+        acc = axpy_real(f, x[p + s1], acc);
+    } else {
+        diag += robin1 ? op.robin_face : Dp;
+    }
+    if (op.d == 3) {
+        const long s2 = (long)op.N0 * op.N1;
+        if (k > 0) {
+            const double f = hmean(Dp, __ldg(D + p - s2));
+            diag += f;
+            acc = axpy_real(f, x[p - s2], acc);
+        } else {
+            diag += op.robin_face;
+        }
+        if (k < op.N2 - 1) {
+            const double f = hmean(Dp, __ldg(D + p + s2));
+            diag += f;
+            acc = axpy_real(f, x[p + s2], acc);
+        } else {
+            diag += op.robin_face;
+        }
+    }
+    return Sc<T>::sub(diag_apply<T>(diag + __ldg(op.mu + p), op.shift, x[p]), acc);
+}
+
+__device__ __forceinline__ void node_coords(const OpDev& op, long p, int& i, int& j, int& k) {
+    i = (int)(p % op.N0);
+    const long q = p / op.N0;
+    j = (int)(q % op.N1);
+    k = (int)(q / op.N1);
+}
+
+// y[:, c] = A x[:, xcol ? xcol[c] : c]  (blockIdx.y = column)
+template <class T>
+__global__ void __launch_bounds__(256) stencil_kernel(OpDev op, const T* __restrict__ x, long ldx,
+                                                      const int* __restrict__ xcol, T* __restrict__ y, long ldy) {
+    const int c = blockIdx.y;
+    const T* xc = x + (size_t)(xcol ? xcol[c] : c) * ldx;
+    T* yc = y + (size_t)c * ldy;
+    for (long p = blockIdx.x * (long)blockDim.x + threadIdx.x; p < op.n; p += (long)gridDim.x * blockDim.x) {
+        int i, j, k;
+        node_coords(op, p, i, j, k);
+        yc[p] = stencil_row<T>(op, xc, p, i, j, k);
+    }
+}
+
+// ------------------------------------------------------------ CG state ---
+// Scalars of one recycled CG / COCG solve (Chronopoulos-Gear recurrence).
+struct CGState {
+    double2 alpha, beta, alpha_prev, gamma_prev, gamma;
+    double scale, tol, best, relres;
+    int it, maxit, stagnant, done, converged, hist_cap, pad0, pad1;
+};
+
+template <class T> __device__ __forceinline__ T ld2(double2 v);
+template <> __device__ __forceinline__ double ld2<double>(double2 v) { return v.x; }
+template <> __device__ __forceinline__ cplx ld2<cplx>(double2 v) { return v; }
+template <class T> __device__ __forceinline__ double2 st2(T v);
+template <> __device__ __forceinline__ double2 st2<double>(double v) { return make_double2(v, 0.0); }
+template <> __device__ __forceinline__ double2 st2<cplx>(cplx v) { return v; }
+
+__device__ inline bool finite_(double v) { return isfinite(v); }
+
+// K2: w = A r ; partials of {r^T r (W), r^T w (W), r^H r (1)} ; last block runs
+// the scalar recurrence. One grid reduction per iteration.
+template <class T>
+__global__ void __launch_bounds__(256) cg_stencil_dots(OpDev op, const T* __restrict__ r, T* __restrict__ w,
+                                                       CGState* st, double* hist, GridRed red) {
+    if (st->done) return;
+    constexpr int W = Sc<T>::W;
+    T g = Sc<T>::zero(), dl = Sc<T>::zero();
+    double h = 0.0;
+    for (long p = blockIdx.x * (long)blockDim.x + threadIdx.x; p < op.n; p += (long)gridDim.x * blockDim.x) {
+        int i, j, k;
+        node_coords(op, p, i, j, k);
+        const T wp = stencil_row<T>(op, r, p, i, j, k);
+        w[p] = wp;
+        const T rp = r[p];
+        g = Sc<T>::fma(rp, rp, g);
+        dl = Sc<T>::fma(rp, wp, dl);
+        h += Sc<T>::abs2(rp);
+    }
+    __shared__ double s_red[32];
+    __shared__ double s_vals[2 * W + 1];
+    double v[2 * W + 1];
+    if constexpr (W == 1) {
+        v[0] = g;
+        v[1] = dl;
+        v[2] = h;
+    } else {
+        v[0] = ((cplx&)g).x;
+        v[1] = ((cplx&)g).y;
+        v[2] = ((cplx&)dl).x;
+        v[3] = ((cplx&)dl).y;
+        v[4] = h;
+    }
+#pragma unroll
+    for (int t = 0; t < 2 * W + 1; ++t) {
+        const double s = block_sum(v[t], s_red);
+        if (threadIdx.x == 0) s_vals[t] = s;
+    }
+    __syncthreads();
+    if (!grid_commit(red, s_vals, 2 * W + 1)) return;
+    __shared__ double s_tot[2 * W + 1];
+    grid_finish(red, 2 * W + 1, s_tot);
+    if (threadIdx.x != 0) return;
+    T gamma, delta;
+    if constexpr (W == 1) {
+        gamma = s_tot[0];
+        delta = s_tot[1];
+    } else {
+        gamma = make_double2(s_tot[0], s_tot[1]);
+        delta = make_double2(s_tot[2], s_tot[3]);
+    }
+    const double rho2 = s_tot[2 * W];
+    const int it = st->it;
+    const double relres = st->scale > 0.0 ? sqrt(rho2) / st->scale : 0.0;
+    st->relres = relres;
+    if (it < st->hist_cap) hist[it] = relres;
+    if (it == 0) {
+        st->best = relres;
+        if (rho2 == 0.0 || st->scale == 0.0 || relres <= st->tol) {
+            st->converged = 1;
+            st->done = 1;
+            return;
+        }
+    } else {
+        if (!finite_(relres)) {
+            st->done = 1;
+            return;
+        }
+        if (relres <= st->tol) {
+            st->converged = 1;
+            st->done = 1;
+            return;
+        }
+        if (relres < st->best * (1.0 - 1e-12)) {
+            st->best = relres;
+            st->stagnant = 0;
+        } else if (++st->stagnant >= 50) {
+            st->done = 1;
+            return;
+        }
+    }
+    if (it >= st->maxit) {
+        st->done = 1;
+        return;
+    }
+    T alpha, beta;
+    if (it == 0) {
+        beta = Sc<T>::zero();
+        alpha = Sc<T>::div(gamma, delta);
+    } else {
+        const T gp = ld2<T>(st->gamma_prev), ap = ld2<T>(st->alpha_prev);
+        beta = Sc<T>::div(gamma, gp);
+        alpha = Sc<T>::div(gamma, Sc<T>::sub(delta, Sc<T>::div(Sc<T>::mul(beta, gamma), ap)));
+    }
+    st->alpha = st2<T>(alpha);
+    st->beta = st2<T>(beta);
+    st->gamma = st2<T>(gamma);
+}
+
+// ------------------------------------------------- tall-skinny passes ---
+// Tile = 32 rows (one per lane); warp w of the 8 owns columns
+// [w*CPW, (w+1)*CPW) of the current column chunk. Per-lane accumulators live
+// across the block's grid-stride tiles; one warp reduction at the end.
+constexpr int TS_THREADS = 256;
+constexpr int TS_WARPS = 8;
+
+template <class T, bool HERM, int CPW>
+__device__ __forceinline__ void ts_finish_cols(T (&acc)[CPW], int c, int col0, GridRed red, double* out,
+                                               const double* flagdone) {
+    constexpr int W = Sc<T>::W;
+    __shared__ double s_vals[TS_WARPS * CPW * W];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+#pragma unroll
+    for (int jj = 0; jj < CPW; ++jj) {
+        double a[W];
+        if constexpr (W == 1) {
+            a[0] = (double&)acc[jj];
+        } else {
+            a[0] = ((cplx&)acc[jj]).x;
+            a[1] = ((cplx&)acc[jj]).y;
+        }
+#pragma unroll
+        for (int t = 0; t < W; ++t) {
+            const double s = warp_sum(a[t]);
+            if (lane == 0) s_vals[(wid * CPW + jj) * W + t] = s;
+        }
+    }
+    __syncthreads();
+    const int nv = c * W;
+    if (!grid_commit(red, s_vals, nv)) return;
+    grid_finish(red, nv, out + (size_t)col0 * W);
+}
+
+// out[col0 + j] = sum_i op(K[i, col0 + j]) x[i], j < c (c <= 8*CPW)
+template <class T, bool HERM, int CPW>
+__global__ void __launch_bounds__(TS_THREADS) ts_T(const T* __restrict__ K, long ldk, int c, int col0,
+                                                   const T* __restrict__ x, long n, GridRed red, double* out,
+                                                   const CGState* st) {
+    if (st && st->done) return;
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const int j0 = wid * CPW;
+    T acc[CPW];
+#pragma unroll
+    for (int jj = 0; jj < CPW; ++jj) acc[jj] = Sc<T>::zero();
+    const long ntiles = (n + 31) >> 5;
+    const T* Kc = K + (size_t)col0 * ldk;
+    for (long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        const long row = (tile << 5) + lane;
+        if (row < n) {
+            const T xv = x[row];
+            T kv[CPW];
+#pragma unroll
+            for (int jj = 0; jj < CPW; ++jj)
+                kv[jj] = (j0 + jj < c) ? Kc[(size_t)(j0 + jj) * ldk + row] : Sc<T>::zero();
+#pragma unroll
+            for (int jj = 0; jj < CPW; ++jj) acc[jj] = opfma<T, HERM>(kv[jj], xv, acc[jj]);
+        }
+    }
+    ts_finish_cols<T, HERM, CPW>(acc, c, col0, red, out, nullptr);
+}
+
+// Fused CGS pass: xo = x - K c1 (c1 = cin, device), out = op(K)^T xo.
+template <class T, bool HERM, int CPW>
+__global__ void __launch_bounds__(TS_THREADS) ts_NT(const T* __restrict__ K, long ldk, int c,
+                                                    const T* __restrict__ x, T* __restrict__ xo, long n,
+                                                    const double* __restrict__ cin, GridRed red, double* out,
+                                                    const CGState* st) {
+    if (st && st->done) return;
+    constexpr int W = Sc<T>::W;
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const int j0 = wid * CPW;
+    __shared__ T s_part[TS_WARPS][32];
+    T cw[CPW];
+#pragma unroll
+    for (int jj = 0; jj < CPW; ++jj) cw[jj] = (j0 + jj < c) ? Sc<T>::get(cin + (size_t)(j0 + jj) * W) : Sc<T>::zero();
+    T acc[CPW];
+#pragma unroll
+    for (int jj = 0; jj < CPW; ++jj) acc[jj] = Sc<T>::zero();
+    const long ntiles = (n + 31) >> 5;
+    for (long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        const long row = (tile << 5) + lane;
+        const bool ok = row < n;
+        T xv = ok ? x[row] : Sc<T>::zero();  // read before the barrier: xo may alias x
+        T kv[CPW];
+        T part = Sc<T>::zero();
+#pragma unroll
+        for (int jj = 0; jj < CPW; ++jj) {
+            kv[jj] = (ok && j0 + jj < c) ? K[(size_t)(j0 + jj) * ldk + row] : Sc<T>::zero();
+            part = Sc<T>::fma(kv[jj], cw[jj], part);
+        }
+        s_part[wid][lane] = part;
+        __syncthreads();
+        T sum = s_part[0][lane];
+#pragma unroll
+        for (int w2 = 1; w2 < TS_WARPS; ++w2) sum = Sc<T>::add(sum, s_part[w2][lane]);
+        xv = Sc<T>::sub(xv, sum);
+        if (wid == 0 && ok) xo[row] = xv;
+#pragma unroll
+        for (int jj = 0; jj < CPW; ++jj) acc[jj] = opfma<T, HERM>(kv[jj], xv, acc[jj]);
+        __syncthreads();
+    }
+    ts_finish_cols<T, HERM, CPW>(acc, c, 0, red, out, nullptr);
+}
+
+// xo = x - sum_j K[:, j] cin[j]  (thread per row, c read from shared memory)
+template <class T>
+__global__ void __launch_bounds__(256) ts_N(const T* __restrict__ K, long ldk, int c, const T* __restrict__ x,
+                                            T* __restrict__ xo, long n, const double* __restrict__ cin,
+                                            double csign, const CGState* st) {
+    if (st && st->done) return;
+    extern __shared__ double s_c[];
+    constexpr int W = Sc<T>::W;
+    for (int t = threadIdx.x; t < c * W; t += blockDim.x) s_c[t] = csign * cin[t];
+    __syncthreads();
+    for (long row = blockIdx.x * (long)blockDim.x + threadIdx.x; row < n; row += (long)gridDim.x * blockDim.x) {
+        T acc = Sc<T>::zero();
+        int j = 0;
+        for (; j + 4 <= c; j += 4) {
+            const T k0 = K[(size_t)j * ldk + row], k1 = K[(size_t)(j + 1) * ldk + row];
+            const T k2 = K[(size_t)(j + 2) * ldk + row], k3 = K[(size_t)(j + 3) * ldk + row];
+            acc = Sc<T>::fma(k0, Sc<T>::get(s_c + j * W), acc);
+            acc = Sc<T>::fma(k1, Sc<T>::get(s_c + (j + 1) * W), acc);
+            acc = Sc<T>::fma(k2, Sc<T>::get(s_c + (j + 2) * W), acc);
+            acc = Sc<T>::fma(k3, Sc<T>::get(s_c + (j + 3) * W), acc);
+        }
+        for (; j < c; ++j) acc = Sc<T>::fma(K[(size_t)j * ldk + row], Sc<T>::get(s_c + j * W), acc);
+        xo[row] = Sc<T>::sub(x[row], acc);
+    }
+}
+
+// K4: q = w - K c2 ; p = r + beta p ; s = q + beta s ; y += alpha p ; r -= alpha s
+template <class T>
+__global__ void __launch_bounds__(256) cg_update(const T* __restrict__ K, long ldk, int c, const T* __restrict__ w,
+                                                 long n, const double* __restrict__ c2, T* __restrict__ r,
+                                                 T* __restrict__ p, T* __restrict__ s, T* __restrict__ y,
+                                                 CGState* st) {
+    if (st->done) return;
+    extern __shared__ double s_c[];
+    constexpr int W = Sc<T>::W;
+    for (int t = threadIdx.x; t < c * W; t += blockDim.x) s_c[t] = c2[t];
+    __syncthreads();
+    const T alpha = ld2<T>(st->alpha), beta = ld2<T>(st->beta);
+    for (long row = blockIdx.x * (long)blockDim.x + threadIdx.x; row < n; row += (long)gridDim.x * blockDim.x) {
+        T acc = Sc<T>::zero();
+        int j = 0;
+        for (; j + 4 <= c; j += 4) {
+            const T k0 = K[(size_t)j * ldk + row], k1 = K[(size_t)(j + 1) * ldk + row];
+            const T k2 = K[(size_t)(j + 2) * ldk + row], k3 = K[(size_t)(j + 3) * ldk + row];
+            acc = Sc<T>::fma(k0, Sc<T>::get(s_c + j * W), acc);
+            acc = Sc<T>::fma(k1, Sc<T>::get(s_c + (j + 1) * W), acc);
+            acc = Sc<T>::fma(k2, Sc<T>::get(s_c + (j + 2) * W), acc);
+            acc = Sc<T>::fma(k3, Sc<T>::get(s_c + (j + 3) * W), acc);
+        }
+        for (; j < c; ++j) acc = Sc<T>::fma(K[(size_t)j * ldk + row], Sc<T>::get(s_c + j * W), acc);
+        const T q = Sc<T>::sub(w[row], acc);
+        const T pn = Sc<T>::fma(beta, p[row], r[row]);
+        const T sn = Sc<T>::fma(beta, s[row], q);
+        p[row] = pn;
+        s[row] = sn;
+        y[row] = Sc<T>::fma(alpha, pn, y[row]);
+        r[row] = Sc<T>::sub(r[row], Sc<T>::mul(alpha, sn));
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        st->gamma_prev = st->gamma;
+        st->alpha_prev = st->alpha;
+        st->it = st->it + 1;
+    }
+}
+
+// ------------------------------------------------------- vector utils ---
+// out[0] = ||x||^2 (Hermitian), out[1..] = optional bilinear x^T x (complex)
+template <class T>
+__global__ void __launch_bounds__(256) vec_norms(const T* __restrict__ x, long n, GridRed red, double* out) {
+    constexpr int W = Sc<T>::W;
+    double h = 0.0;
+    T b = Sc<T>::zero();
+    for (long i = blockIdx.x * (long)blockDim.x + threadIdx.x; i < n; i += (long)gridDim.x * blockDim.x) {
+        const T v = x[i];
+        h += Sc<T>::abs2(v);
+        b = Sc<T>::fma(v, v, b);
+    }
+    __shared__ double s_red[32];
+    __shared__ double s_vals[1 + W];
+    double v[1 + W];
+    v[0] = h;
+    if constexpr (W == 1) {
+        v[1] = b;
+    } else {
+        v[1] = ((cplx&)b).x;
+        v[2] = ((cplx&)b).y;
+    }
+#pragma unroll
+    for (int t = 0; t < 1 + W; ++t) {
+        const double s = block_sum(v[t], s_red);
+        if (threadIdx.x == 0) s_vals[t] = s;
+    }
+    __syncthreads();
+    if (!grid_commit(red, s_vals, 1 + W)) return;
+    grid_finish(red, 1 + W, out);
+}
+
+// y = x * (1/rho) with rho from device: mode 0 = sqrt(out[0]) (Hermitian norm),
+// mode 1 = complex sqrt of the bilinear x^T x (out[1], out[2]) (real: sqrt(out[1]))
+template <class T> __device__ __forceinline__ T inv_rho(const double* nrm, int mode);
+template <> __device__ __forceinline__ double inv_rho<double>(const double* nrm, int mode) {
+    return 1.0 / sqrt(mode == 0 ? nrm[0] : nrm[1]);
+}
+template <> __device__ __forceinline__ cplx inv_rho<cplx>(const double* nrm, int mode) {
+    if (mode == 0) return make_double2(1.0 / sqrt(nrm[0]), 0.0);
+    // principal sqrt of a + ib
+    const double a = nrm[1], b = nrm[2];
+    const double m = sqrt(a * a + b * b);
+    double sr = sqrt(0.5 * (m + a));
+    double si = sqrt(fmax(0.0, 0.5 * (m - a)));
+    if (b < 0) si = -si;
+    return Sc<cplx>::div(make_double2(1.0, 0.0), make_double2(sr, si));
+}
+
+template <class T>
+__global__ void vec_scale_by_rho(const T* __restrict__ x, T* __restrict__ y, long n, const double* nrm, int mode) {
+    const T s = inv_rho<T>(nrm, mode);
+    for (long i = blockIdx.x * (long)blockDim.x + threadIdx.x; i < n; i += (long)gridDim.x * blockDim.x)
+        y[i] = Sc<T>::mul(x[i], s);
+}
+
+// y = a*x + y (a device scalar pair, optional) -- generic axpy with host scalar
+template <class T>
+__global__ void vec_axpby(long n, double2 a, const T* __restrict__ x, double2 b, T* __restrict__ y) {
+    const T aa = ld2<T>(a), bb = ld2<T>(b);
+    for (long i = blockIdx.x * (long)blockDim.x + threadIdx.x; i < n; i += (long)gridDim.x * blockDim.x)
+        y[i] = Sc<T>::add(Sc<T>::mul(aa, x[i]), Sc<T>::mul(bb, y[i]));
+}
+
+// out[j] = op(K[idx, j]) * val   (row gather: K^op b for a single-nonzero b)
+template <class T, bool HERM>
+__global__ void row_gather(const T* __restrict__ K, long ldk, int c, long idx, double val, double* out) {
+    constexpr int W = Sc<T>::W;
+    for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < c; j += gridDim.x * blockDim.x) {
+        T k = K[(size_t)j * ldk + idx];
+        T v = opmul<T, HERM>(k, Sc<T>::from(val));
+        Sc<T>::put(out + (size_t)j * W, v);
+    }
+}
+
+// out = a - b (device double arrays), or out = a + b
+__global__ void dvec_addsub(int m, const double* a, const double* b, double sgn, double* out) {
+    for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < m; t += gridDim.x * blockDim.x) out[t] = a[t] + sgn * b[t];
+}
+
+}  // namespace rd

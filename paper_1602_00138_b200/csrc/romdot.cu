@@ -1,0 +1,1171 @@
+// Host runtime of the B200 basis builder: context, device operator, recycled
+// CG / COCG driver, device GlobalBasis, process_system and the C ABI
+// (include/romdot_b200.h). All control flow that the reference runs in
+// src/basis.cpp and src/krylov.cpp lives here in C++; all arithmetic on
+// n-vectors runs in the kernels of kernels.cuh / dense.cuh.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/romdot_b200.h"
+#include "dense.cuh"
+#include "kernels.cuh"
+
+namespace rd {
+
+struct ConfigError : std::runtime_error {
+    explicit ConfigError(const std::string& m) : std::runtime_error(m) {}
+};
+struct SolverError : std::runtime_error {
+    explicit SolverError(const std::string& m) : std::runtime_error(m) {}
+};
+struct CudaError : std::runtime_error {
+    explicit CudaError(const std::string& m) : std::runtime_error(m) {}
+};
+
+static thread_local std::string g_err;
+
+#define CK(x)                                                                                        \
+    do {                                                                                             \
+        cudaError_t e_ = (x);                                                                        \
+        if (e_ != cudaSuccess)                                                                       \
+            throw CudaError(std::string(#x) + ": " + cudaGetErrorString(e_) + " @" + __FILE__ + ":" + \
+                            std::to_string(__LINE__));                                               \
+    } while (0)
+
+template <class T> constexpr int dt_of();
+template <> constexpr int dt_of<double>() { return 0; }
+template <> constexpr int dt_of<cplx>() { return 1; }
+
+// ------------------------------------------------------------- buffers ---
+struct DevBuf {
+    void* p = nullptr;
+    size_t bytes = 0;
+    DevBuf() = default;
+    DevBuf(const DevBuf&) = delete;
+    DevBuf& operator=(const DevBuf&) = delete;
+    ~DevBuf() {
+        if (p) cudaFree(p);
+    }
+    void ensure(size_t b) {
+        if (b <= bytes) return;
+        if (p) CK(cudaFree(p));
+        p = nullptr;
+        CK(cudaMalloc(&p, b));
+        bytes = b;
+    }
+    template <class T> T* as() const { return static_cast<T*>(p); }
+};
+
+// ------------------------------------------------------------- context ---
+struct Ctx {
+    int device = 0;
+    int sms = 148;
+    cudaStream_t s = nullptr;
+    DevBuf partials, counter, scal, cgst, hist;
+    CGState* st_host = nullptr;  // pinned, 2 slots
+    cudaEvent_t ev[2] = {nullptr, nullptr};
+    cudaEvent_t mark[2] = {nullptr, nullptr};
+    int nmark = 0;
+    long launches = 0;
+    int hist_cap = 1 << 16;
+
+    void init(int dev) {
+        device = dev;
+        CK(cudaSetDevice(dev));
+        CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+        CK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+        partials.ensure(sizeof(double) * 4096 * 64);
+        counter.ensure(sizeof(unsigned) * 16);
+        CK(cudaMemset(counter.p, 0, counter.bytes));
+        scal.ensure(sizeof(double) * 64 * 1024);
+        cgst.ensure(sizeof(CGState));
+        hist.ensure(sizeof(double) * hist_cap);
+        CK(cudaMallocHost(&st_host, 2 * sizeof(CGState)));
+        for (auto& e : ev) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        for (auto& e : mark) CK(cudaEventCreate(&e));
+    }
+    ~Ctx() {
+        if (s) cudaStreamSynchronize(s);
+        if (st_host) cudaFreeHost(st_host);
+        for (auto& e : ev)
+            if (e) cudaEventDestroy(e);
+        for (auto& e : mark)
+            if (e) cudaEventDestroy(e);
+        if (s) cudaStreamDestroy(s);
+    }
+    GridRed red() const { return GridRed{partials.template as<double>(), counter.template as<unsigned>()}; }
+    // small device scratch: slot k of 8 slots of 8192 doubles
+    double* sc(int k) const { return scal.template as<double>() + (size_t)k * 8192; }
+    int grid_for(long n, int per = 256, int mult = 4) const {
+        const long b = (n + per - 1) / per;
+        return (int)std::max(1L, std::min<long>(b, (long)sms * mult));
+    }
+    void check_launch() {
+        ++launches;
+        CK(cudaGetLastError());
+    }
+    void sync() { CK(cudaStreamSynchronize(s)); }
+};
+
+// ------------------------------------------------------------ operator ---
+struct DevOp {
+    Ctx* ctx = nullptr;
+    OpDev d{};
+    DevBuf D, mu;
+    bool have_fields = false;
+    double lam_max = 0.0;
+    long n() const { return d.n; }
+};
+
+// ------------------------------------------------------ launch helpers ---
+template <class T> void launch_stencil(Ctx& c, const OpDev& op, const T* x, long ldx, const int* xcol, T* y,
+                                       long ldy, long ncols) {
+    if (ncols <= 0) return;
+    for (long c0 = 0; c0 < ncols; c0 += 65535) {
+        const int nc = (int)std::min(65535L, ncols - c0);
+        dim3 grid(c.grid_for(op.n, 256, 8), nc);
+        stencil_kernel<T><<<grid, 256, 0, c.s>>>(op, xcol ? x : x + (size_t)c0 * ldx, ldx, xcol ? xcol + c0 : nullptr,
+                                                 y + (size_t)c0 * ldy, ldy);
+        c.check_launch();
+    }
+}
+
+template <class T, bool HERM, int CPW>
+void ts_T_inst(Ctx& c, const T* K, long ldk, int cc, int col0, const T* x, long n, double* out, const CGState* st) {
+    const long ntiles = (n + 31) / 32;
+    const int grid = (int)std::max(1L, std::min<long>(ntiles, (long)c.sms * 2));
+    ts_T<T, HERM, CPW><<<grid, TS_THREADS, 0, c.s>>>(K, ldk, cc, col0, x, n, c.red(), out, st);
+    c.check_launch();
+}
+
+// out[j] = sum_i op(K_ij) x_i, j < ncol  (chunks of 128 columns)
+template <class T, bool HERM>
+void ts_T_launch(Ctx& c, const T* K, long ldk, long ncol, const T* x, long n, double* out, const CGState* st = nullptr) {
+    for (long col0 = 0; col0 < ncol; col0 += 128) {
+        const int cc = (int)std::min(128L, ncol - col0);
+        const int cpw = (cc + 7) / 8;
+        if (cpw <= 1)
+            ts_T_inst<T, HERM, 1>(c, K, ldk, cc, (int)col0, x, n, out, st);
+        else if (cpw <= 2)
+            ts_T_inst<T, HERM, 2>(c, K, ldk, cc, (int)col0, x, n, out, st);
+        else if (cpw <= 4)
+            ts_T_inst<T, HERM, 4>(c, K, ldk, cc, (int)col0, x, n, out, st);
+        else if (cpw <= 8)
+            ts_T_inst<T, HERM, 8>(c, K, ldk, cc, (int)col0, x, n, out, st);
+        else
+            ts_T_inst<T, HERM, 16>(c, K, ldk, cc, (int)col0, x, n, out, st);
+    }
+}
+
+template <class T, bool HERM, int CPW>
+void ts_NT_inst(Ctx& c, const T* K, long ldk, int cc, const T* x, T* xo, long n, const double* cin, double* out,
+                const CGState* st) {
+    const long ntiles = (n + 31) / 32;
+    const int grid = (int)std::max(1L, std::min<long>(ntiles, (long)c.sms * 2));
+    ts_NT<T, HERM, CPW><<<grid, TS_THREADS, 0, c.s>>>(K, ldk, cc, x, xo, n, cin, c.red(), out, st);
+    c.check_launch();
+}
+
+template <class T>
+void ts_N_launch(Ctx& c, const T* K, long ldk, long ncol, const T* x, T* xo, long n, const double* cin,
+                 double csign = 1.0, const CGState* st = nullptr) {
+    const size_t smem = sizeof(double) * Sc<T>::W * std::max(1L, ncol);
+    if (smem > 48 * 1024) {
+        // very wide bases: chunk columns (x - K[:, a:b] c[a:b] accumulated in xo)
+        const T* src = x;
+        for (long c0 = 0; c0 < ncol; c0 += 1024) {
+            const long cc = std::min(1024L, ncol - c0);
+            ts_N_launch<T>(c, K + (size_t)c0 * ldk, ldk, cc, src, xo, n, cin + (size_t)c0 * Sc<T>::W, csign, st);
+            src = xo;
+        }
+        return;
+    }
+    ts_N<T><<<c.grid_for(n, 256, 8), 256, smem, c.s>>>(K, ldk, (int)ncol, x, xo, n, cin, csign, st);
+    c.check_launch();
+}
+
+// fused {xo = x - K c1 ; out = op(K)^T xo} for ncol <= 128, else N then T
+template <class T, bool HERM>
+void ts_NT_launch(Ctx& c, const T* K, long ldk, long ncol, const T* x, T* xo, long n, const double* cin,
+                  double* out, const CGState* st = nullptr) {
+    if (ncol > 128) {
+        ts_N_launch<T>(c, K, ldk, ncol, x, xo, n, cin, 1.0, st);
+        ts_T_launch<T, HERM>(c, K, ldk, ncol, xo, n, out, st);
+        return;
+    }
+    const int cc = (int)ncol;
+    const int cpw = (cc + 7) / 8;
+    if (cpw <= 1)
+        ts_NT_inst<T, HERM, 1>(c, K, ldk, cc, x, xo, n, cin, out, st);
+    else if (cpw <= 2)
+        ts_NT_inst<T, HERM, 2>(c, K, ldk, cc, x, xo, n, cin, out, st);
+    else if (cpw <= 4)
+        ts_NT_inst<T, HERM, 4>(c, K, ldk, cc, x, xo, n, cin, out, st);
+    else if (cpw <= 8)
+        ts_NT_inst<T, HERM, 8>(c, K, ldk, cc, x, xo, n, cin, out, st);
+    else
+        ts_NT_inst<T, HERM, 16>(c, K, ldk, cc, x, xo, n, cin, out, st);
+}
+
+// nrm[0] = ||x||^2, nrm[1..W] = x^T x
+template <class T> void launch_norms(Ctx& c, const T* x, long n, double* nrm) {
+    vec_norms<T><<<c.grid_for(n, 256, 2), 256, 0, c.s>>>(x, n, c.red(), nrm);
+    c.check_launch();
+}
+
+template <class T> void launch_scale(Ctx& c, const T* x, T* y, long n, const double* nrm, int mode) {
+    vec_scale_by_rho<T><<<c.grid_for(n, 256, 8), 256, 0, c.s>>>(x, y, n, nrm, mode);
+    c.check_launch();
+}
+
+inline void launch_addsub(Ctx& c, int m, const double* a, const double* b, double sgn, double* out) {
+    if (m <= 0) return;
+    dvec_addsub<<<(m + 255) / 256, 256, 0, c.s>>>(m, a, b, sgn, out);
+    c.check_launch();
+}
+
+// CGS2 of z against the first t columns of Q (op = H or T): q = (I - QQ^op)^2 z,
+// coef (device, t scalars) = Q^op z accumulated over both passes.
+template <class T, bool HERM>
+void cgs2(Ctx& c, const T* Q, long ldq, long t, const T* z, T* q, long n, double* coef, double* tmp1,
+          double* tmp2) {
+    constexpr int W = Sc<T>::W;
+    if (t == 0) {
+        if (q != z) CK(cudaMemcpyAsync(q, z, sizeof(T) * n, cudaMemcpyDeviceToDevice, c.s));
+        return;
+    }
+    ts_T_launch<T, HERM>(c, Q, ldq, t, z, n, tmp1);
+    ts_NT_launch<T, HERM>(c, Q, ldq, t, z, q, n, tmp1, tmp2);
+    ts_N_launch<T>(c, Q, ldq, t, q, q, n, tmp2);
+    launch_addsub(c, (int)(t * W), tmp1, tmp2, 1.0, coef);
+}
+
+// ---------------------------------------------------------- CG driver ---
+struct SolveOut {
+    int iterations = 0;
+    bool converged = false;
+    double final_relres = 0.0;
+    double correction_norm = 0.0;
+    std::vector<double> hist;
+};
+
+template <class T> struct Workspace {
+    DevBuf r, w, p, s, y, tmp, vec;
+    void ensure(long n) {
+        const size_t b = sizeof(T) * n;
+        r.ensure(b);
+        w.ensure(b);
+        p.ensure(b);
+        s.ensure(b);
+        y.ensure(b);
+        tmp.ensure(b);
+        vec.ensure(b);
+    }
+};
+
+// Recycled CG / COCG (the CPU checker under oracle/ restates the same recurrence).
+// rhs, U, K, g, y_out, image: device. g/y_out/image may alias workspace-free
+// buffers only.
+template <class T>
+SolveOut recycled_cg(Ctx& c, DevOp& op, const T* U, const T* K, long ncol, const T* rhs, double tol, long maxit,
+                     double rhs_scale, T* g, T* y_out, T* image, Workspace<T>& ws, bool want_hist) {
+    constexpr int W = Sc<T>::W;
+    const long n = op.n();
+    ws.ensure(n);
+    T* r = ws.r.template as<T>();
+    T* w = ws.w.template as<T>();
+    T* p = ws.p.template as<T>();
+    T* s = ws.s.template as<T>();
+    T* y = y_out;
+    double* e = c.sc(0);
+    double* c1 = c.sc(1);
+    double* c2 = c.sc(2);
+    double* nrm = c.sc(3);
+    if (ncol > 1024) throw ConfigError("recycle space wider than 1024 columns");
+    // r0 = P rhs (CGS2), e = K^T rhs
+    if (ncol > 0) {
+        cgs2<T, false>(c, K, n, ncol, rhs, r, n, e, c1, c2);
+    } else {
+        CK(cudaMemcpyAsync(r, rhs, sizeof(T) * n, cudaMemcpyDeviceToDevice, c.s));
+    }
+    double scale = rhs_scale;
+    if (!(scale > 0.0)) {
+        launch_norms<T>(c, rhs, n, nrm);
+        double h;
+        CK(cudaMemcpyAsync(&h, nrm, sizeof(double), cudaMemcpyDeviceToHost, c.s));
+        c.sync();
+        scale = std::sqrt(h);
+    }
+    CK(cudaMemsetAsync(y, 0, sizeof(T) * n, c.s));
+    CK(cudaMemsetAsync(p, 0, sizeof(T) * n, c.s));
+    CK(cudaMemsetAsync(s, 0, sizeof(T) * n, c.s));
+    CGState init{};
+    init.scale = scale;
+    init.tol = tol;
+    init.maxit = (int)std::min<long>(maxit, 0x7fffffff);
+    init.hist_cap = c.hist_cap;
+    CGState* st = c.cgst.template as<CGState>();
+    c.st_host[0] = init;
+    CK(cudaMemcpyAsync(st, &c.st_host[0], sizeof(CGState), cudaMemcpyHostToDevice, c.s));
+    CK(cudaStreamSynchronize(c.s));  // st_host slot reused below
+
+    const int grid_st = c.grid_for(n, 256, 2);
+    const size_t smem_c = sizeof(double) * W * std::max(1L, ncol);
+    const int batch = n < 200000 ? 16 : 8;
+    auto launch_batch = [&]() {
+        for (int b = 0; b < batch; ++b) {
+            cg_stencil_dots<T><<<grid_st, 256, 0, c.s>>>(op.d, r, w, st, c.hist.template as<double>(), c.red());
+            c.check_launch();
+            if (ncol > 0) {
+                ts_T_launch<T, false>(c, K, n, ncol, w, n, c1, st);
+                ts_NT_launch<T, false>(c, K, n, ncol, w, w, n, c1, c2, st);
+            }
+            cg_update<T><<<c.grid_for(n, 256, 8), 256, smem_c, c.s>>>(K, n, (int)ncol, w, n, c2, r, p, s, y, st);
+            c.check_launch();
+        }
+    };
+    // two batches in flight; poll the done flag of the older one
+    int slot = 0;
+    launch_batch();
+    CK(cudaMemcpyAsync(&c.st_host[0], st, sizeof(CGState), cudaMemcpyDeviceToHost, c.s));
+    CK(cudaEventRecord(c.ev[0], c.s));
+    launch_batch();
+    CK(cudaMemcpyAsync(&c.st_host[1], st, sizeof(CGState), cudaMemcpyDeviceToHost, c.s));
+    CK(cudaEventRecord(c.ev[1], c.s));
+    long guard = 0;
+    while (true) {
+        CK(cudaEventSynchronize(c.ev[slot]));
+        if (c.st_host[slot].done) break;
+        if (++guard > (maxit / batch) + 8) break;
+        launch_batch();
+        CK(cudaMemcpyAsync(&c.st_host[slot], st, sizeof(CGState), cudaMemcpyDeviceToHost, c.s));
+        CK(cudaEventRecord(c.ev[slot], c.s));
+        slot ^= 1;
+    }
+    CK(cudaMemcpyAsync(&c.st_host[0], st, sizeof(CGState), cudaMemcpyDeviceToHost, c.s));
+    c.sync();
+    const CGState fin = c.st_host[0];
+    SolveOut out;
+    out.iterations = fin.it;
+    out.converged = fin.converged != 0;
+    out.final_relres = fin.relres;
+    if (want_hist) {
+        const long m = std::min<long>(fin.it + 1, c.hist_cap);
+        out.hist.resize(m);
+        CK(cudaMemcpy(out.hist.data(), c.hist.p, sizeof(double) * m, cudaMemcpyDeviceToHost));
+    }
+    // image = A y ; g = y + U (e - K^T image)
+    launch_stencil<T>(c, op.d, y, n, nullptr, image, n, 1);
+    if (ncol > 0) {
+        ts_T_launch<T, false>(c, K, n, ncol, image, n, c1);
+        launch_addsub(c, (int)(ncol * W), c1, e, -1.0, c2);  // c2 = K^T image - e
+        ts_N_launch<T>(c, U, n, ncol, y, g, n, c2);           // g = y - U c2
+    } else if (g != y) {
+        CK(cudaMemcpyAsync(g, y, sizeof(T) * n, cudaMemcpyDeviceToDevice, c.s));
+    }
+    return out;
+}
+
+// RecycleSpace::from_raw on the device: sequential CGS2 (bilinear for complex)
+// of AW's columns; U = W R^-1 formed column by column. W columns are read
+// through `wcol` (indices into Wbase) when given.
+template <class T>
+void from_raw(Ctx& c, long n, long ncol, const T* Wbase, const int* wcol_host, const T* AW, T* U, T* K) {
+    constexpr int W = Sc<T>::W;
+    double* coef = c.sc(4);
+    double* t1 = c.sc(5);
+    double* t2 = c.sc(6);
+    double* nrm = c.sc(7);
+    for (long t = 0; t < ncol; ++t) {
+        T* kt = K + (size_t)t * n;
+        T* ut = U + (size_t)t * n;
+        const T* wsrc = Wbase + (size_t)(wcol_host ? wcol_host[t] : t) * n;
+        cgs2<T, false>(c, K, n, t, AW + (size_t)t * n, kt, n, coef, t1, t2);
+        launch_norms<T>(c, kt, n, nrm);
+        launch_scale<T>(c, kt, kt, n, nrm, 1);
+        if (t > 0)
+            ts_N_launch<T>(c, U, n, t, wsrc, ut, n, coef);
+        else
+            CK(cudaMemcpyAsync(ut, wsrc, sizeof(T) * n, cudaMemcpyDeviceToDevice, c.s));
+        launch_scale<T>(c, ut, ut, n, nrm, 1);
+    }
+    (void)W;
+}
+
+// ---------------------------------------------------------- global basis ---
+constexpr uint8_t kColEigenvector = 0, kColInitialSolution = 1, kColCorrection = 2;
+constexpr double kInnerSafety = 0.25;  // basis.cpp:27
+
+struct BasisBase {
+    virtual ~BasisBase() = default;
+};
+
+template <class T> struct DevBasis : BasisBase {
+    Ctx* ctx = nullptr;
+    long n = 0;
+    long cols = 0, capcols = 0, ku = 0, cap = 0;
+    DevBuf V, Wm, K;            // n x capcols each; W = V R^-1, K = K_img
+    std::vector<T> R;           // host, cols x cols column-major (ld = capcols)
+    std::vector<uint8_t> markers;
+    std::vector<std::vector<int>> spaces;
+    bool factored = false;
+    Workspace<T> ws;
+    DevBuf tmpv, tmpv2, AW, Ur, Kr, idx, X, bvec;
+
+    T* Vp() const { return V.template as<T>(); }
+    T* Wp() const { return Wm.template as<T>(); }
+    T* Kp() const { return K.template as<T>(); }
+
+    void reserve(long want) {
+        if (want <= capcols) return;
+        long nc = std::max(want, std::max(16L, capcols * 3 / 2));
+        if (cap > 0) nc = std::min(nc, std::max(want, cap));
+        auto grow = [&](DevBuf& b) {
+            DevBuf nb;
+            nb.ensure(sizeof(T) * n * nc);
+            if (b.p && cols > 0) CK(cudaMemcpyAsync(nb.p, b.p, sizeof(T) * n * cols, cudaMemcpyDeviceToDevice, ctx->s));
+            ctx->sync();
+            std::swap(b.p, nb.p);
+            std::swap(b.bytes, nb.bytes);
+        };
+        grow(V);
+        grow(Wm);
+        grow(K);
+        std::vector<T> R2((size_t)nc * nc, Sc<T>::zero());
+        for (long j = 0; j < cols; ++j)
+            for (long i = 0; i <= j; ++i) R2[i + j * nc] = R[i + j * capcols];
+        R.swap(R2);
+        capcols = nc;
+    }
+    T& Rat(long i, long j) { return R[i + j * capcols]; }
+
+    void drop_column(long cidx) {
+        // V columns shift left; per-RHS indices remapped (SURVEY §5 latent bug fixed)
+        for (long k = cidx; k + 1 < cols; ++k)
+            CK(cudaMemcpyAsync(Vp() + k * n, Vp() + (k + 1) * n, sizeof(T) * n, cudaMemcpyDeviceToDevice, ctx->s));
+        markers.erase(markers.begin() + cidx);
+        for (auto& sp : spaces) {
+            std::vector<int> o;
+            for (int v : sp) {
+                if (v == cidx) continue;
+                o.push_back(v > cidx ? v - 1 : v);
+            }
+            sp.swap(o);
+        }
+        --cols;
+    }
+
+    // Factor column j of V against K[:, :j] at the operator's current fields:
+    // z = A_i v_j, CGS2 (Hermitian), K_j = q/rho, W_j = (v_j - W c)/rho, R(:, j).
+    // Returns rho / ||z|| decision data; writes nothing if dropped.
+    bool factor_column(DevOp& op, long j, bool may_drop) {
+        Ctx& c = *ctx;
+        constexpr int W = Sc<T>::W;
+        tmpv.ensure(sizeof(T) * n);
+        T* z = tmpv.template as<T>();
+        T* vj = Vp() + (size_t)j * n;
+        launch_stencil<T>(c, op.d, vj, n, nullptr, z, n, 1);
+        return factor_image(j, vj, z, may_drop);
+        (void)W;
+    }
+
+    bool factor_image(long j, const T* vj, const T* z, bool may_drop) {
+        Ctx& c = *ctx;
+        constexpr int W = Sc<T>::W;
+        T* q = Kp() + (size_t)j * n;
+        double* coef = c.sc(4);
+        double* nrm = c.sc(7);
+        cgs2<T, true>(c, Kp(), n, j, z, q, n, coef, c.sc(5), c.sc(6));
+        launch_norms<T>(c, q, n, nrm);
+        launch_norms<T>(c, z, n, nrm + 8);
+        std::vector<double> hc(2 + (size_t)j * W);
+        CK(cudaMemcpyAsync(hc.data(), nrm, sizeof(double), cudaMemcpyDeviceToHost, c.s));
+        CK(cudaMemcpyAsync(hc.data() + 1, nrm + 8, sizeof(double), cudaMemcpyDeviceToHost, c.s));
+        if (j > 0) CK(cudaMemcpyAsync(hc.data() + 2, coef, sizeof(double) * j * W, cudaMemcpyDeviceToHost, c.s));
+        c.sync();
+        const double rho = std::sqrt(hc[0]);
+        const double zn = std::sqrt(hc[1]);
+        if (may_drop && rho <= 1e-12 * zn) return false;
+        launch_scale<T>(c, q, q, n, nrm, 0);
+        T* wj = Wp() + (size_t)j * n;
+        if (j > 0)
+            ts_N_launch<T>(c, Wp(), n, j, vj, wj, n, coef);
+        else if (wj != vj)
+            CK(cudaMemcpyAsync(wj, vj, sizeof(T) * n, cudaMemcpyDeviceToDevice, c.s));
+        launch_scale<T>(c, wj, wj, n, nrm, 0);
+        for (long i = 0; i < j; ++i) {
+            if constexpr (W == 1)
+                Rat(i, j) = hc[2 + i];
+            else
+                Rat(i, j) = make_double2(hc[2 + 2 * i], hc[3 + 2 * i]);
+        }
+        Rat(j, j) = Sc<T>::from(rho);
+        return true;
+    }
+
+    // GlobalBasis::refresh (basis.cpp:37-76): K_img R = A_i V with drop rule
+    // |R_ii| <= 1e-12 ||A_i v_i|| for i >= ku. Sequential CGS2 factorisation.
+    void refresh(DevOp& op) {
+        long j = 0;
+        while (j < cols) {
+            if (factor_column(op, j, j >= ku)) {
+                ++j;
+            } else {
+                drop_column(j);
+            }
+        }
+        factored = true;
+    }
+
+    bool append(const T* y, const T* z, uint8_t marker) {
+        if (cap > 0 && cols >= cap) return false;
+        reserve(cols + 1);
+        const long j = cols;
+        CK(cudaMemcpyAsync(Vp() + (size_t)j * n, y, sizeof(T) * n, cudaMemcpyDeviceToDevice, ctx->s));
+        if (!factor_image(j, Vp() + (size_t)j * n, z, true)) return false;
+        ++cols;
+        markers.push_back(marker);
+        return true;
+    }
+
+    // coords w = K^H b for b = val * e_idx (row gather), device out (cols*W)
+    void coords_single(long idx, double val, double* w) {
+        if (cols == 0) return;
+        row_gather<T, true><<<(int)((cols + 255) / 256), 256, 0, ctx->s>>>(Kp(), n, (int)cols, idx, val, w);
+        ctx->check_launch();
+    }
+};
+
+struct BasisHandle {
+    Ctx* ctx;
+    int dtype;
+    std::unique_ptr<DevBasis<double>> r;
+    std::unique_ptr<DevBasis<cplx>> c;
+};
+
+// process_system (basis.cpp:157-207)
+struct LogRow {
+    int system, rhs;
+    double init_relres;
+    int iterations;
+    bool appended;
+};
+
+template <class T>
+void process_system(DevBasis<T>& gb, DevOp& op, long nrhs, const long* bidx, const double* bval, double tol,
+                    int system_index, long maxit, T* Xdev, std::vector<LogRow>& log, long& inner_its,
+                    long& appends) {
+    Ctx& c = *gb.ctx;
+    constexpr int W = Sc<T>::W;
+    const long n = gb.n;
+    if (maxit <= 0) maxit = 2 * n;
+    gb.refresh(op);
+    log.clear();
+    inner_its = 0;
+    appends = 0;
+    gb.bvec.ensure(sizeof(T) * n);
+    gb.tmpv2.ensure(sizeof(T) * n);
+    T* b = gb.bvec.template as<T>();
+    T* rj = gb.tmpv2.template as<T>();
+    CK(cudaMemsetAsync(b, 0, sizeof(T) * n, c.s));
+    DevBuf wbuf, ybuf, gbuf, imbuf;
+    ybuf.ensure(sizeof(T) * n);
+    gbuf.ensure(sizeof(T) * n);
+    imbuf.ensure(sizeof(T) * n);
+    for (long j = 0; j < nrhs; ++j) {
+        const long bi = bidx[j];
+        const double bv = bval[j];
+        T bval_t = Sc<T>::from(bv);
+        CK(cudaMemcpyAsync(b + bi, &bval_t, sizeof(T), cudaMemcpyHostToDevice, c.s));
+        const double bnorm = std::fabs(bv);
+        const long r = gb.cols;
+        wbuf.ensure(sizeof(double) * W * std::max(1L, r) + 64);
+        double* w = wbuf.template as<double>();
+        gb.coords_single(bi, bv, w);
+        // r_j = b - K w
+        ts_N_launch<T>(c, gb.Kp(), n, r, b, rj, n, w);
+        double* nrm = c.sc(3);
+        launch_norms<T>(c, rj, n, nrm);
+        double h;
+        CK(cudaMemcpyAsync(&h, nrm, sizeof(double), cudaMemcpyDeviceToHost, c.s));
+        c.sync();
+        LogRow row{system_index, (int)j, std::sqrt(h) / bnorm, 0, false};
+        T* Xj = Xdev ? Xdev + (size_t)j * n : gbuf.template as<T>();
+        if (row.init_relres <= tol) {
+            CK(cudaMemsetAsync(gbuf.p, 0, sizeof(T) * n, c.s));
+            ts_N_launch<T>(c, gb.Wp(), n, r, gbuf.template as<T>(), Xj, n, w, -1.0);  // X_j = W w
+        } else {
+            auto& idx = gb.spaces[j];
+            const long cj = (long)idx.size();
+            gb.idx.ensure(sizeof(int) * std::max(1L, cj));
+            CK(cudaMemcpyAsync(gb.idx.p, idx.data(), sizeof(int) * cj, cudaMemcpyHostToDevice, c.s));
+            gb.AW.ensure(sizeof(T) * n * cj);
+            gb.Ur.ensure(sizeof(T) * n * cj);
+            gb.Kr.ensure(sizeof(T) * n * cj);
+            launch_stencil<T>(c, op.d, gb.Vp(), n, gb.idx.template as<int>(), gb.AW.template as<T>(), n, cj);
+            from_raw<T>(c, n, cj, gb.Vp(), idx.data(), gb.AW.template as<T>(), gb.Ur.template as<T>(), gb.Kr.template as<T>());
+            SolveOut so = recycled_cg<T>(c, op, gb.Ur.template as<T>(), gb.Kr.template as<T>(), cj, rj, kInnerSafety * tol, maxit,
+                                         bnorm, gbuf.template as<T>(), ybuf.template as<T>(), imbuf.template as<T>(), gb.ws, false);
+            if (!so.converged)
+                throw SolverError("process_system: correction solve failed at system " +
+                                  std::to_string(system_index) + ", rhs " + std::to_string(j));
+            ts_N_launch<T>(c, gb.Wp(), n, r, gbuf.template as<T>(), Xj, n, w, -1.0);  // X_j = g + W w
+            row.iterations = so.iterations;
+            inner_its += so.iterations;
+            if (gb.append(ybuf.template as<T>(), imbuf.template as<T>(), kColCorrection)) {
+                idx.push_back((int)(gb.cols - 1));
+                row.appended = true;
+                ++appends;
+            }
+        }
+        T zero = Sc<T>::zero();
+        CK(cudaMemcpyAsync(b + bi, &zero, sizeof(T), cudaMemcpyHostToDevice, c.s));
+        c.sync();
+        log.push_back(row);
+    }
+}
+
+}  // namespace rd
+
+// ================================================================ C ABI ===
+using namespace rd;
+
+struct rd_ctx {
+    Ctx c;
+};
+struct rd_op {
+    rd_ctx* ctx;
+    DevOp op;
+};
+struct rd_basis {
+    rd_ctx* ctx;
+    BasisHandle h;
+};
+
+namespace {
+
+template <class F> int guard(F&& f) {
+    try {
+        f();
+        return 0;
+    } catch (const rd::ConfigError& e) {
+        g_err = e.what();
+        return 2;
+    } catch (const rd::SolverError& e) {
+        g_err = e.what();
+        return 3;
+    } catch (const rd::CudaError& e) {
+        g_err = e.what();
+        return 5;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return 1;
+    }
+}
+
+// Stage a host or device buffer on the device (copy if host).
+struct Staged {
+    DevBuf own;
+    void* p = nullptr;
+    Staged(Ctx& c, const void* src, size_t bytes, int where) {
+        if (where == 1 || src == nullptr) {
+            p = const_cast<void*>(src);
+        } else {
+            own.ensure(std::max<size_t>(bytes, 16));
+            CK(cudaMemcpyAsync(own.p, src, bytes, cudaMemcpyHostToDevice, c.s));
+            p = own.p;
+        }
+    }
+};
+struct Out {
+    Ctx& c;
+    DevBuf own;
+    void* dst;
+    void* p;
+    size_t bytes;
+    int where;
+    Out(Ctx& cc, void* d, size_t b, int w) : c(cc), dst(d), p(nullptr), bytes(b), where(w) {
+        if (dst == nullptr) {
+            p = nullptr;
+        } else if (where == 1) {
+            p = dst;
+        } else {
+            own.ensure(std::max<size_t>(bytes, 16));
+            p = own.p;
+        }
+    }
+    void finish() {
+        if (dst && where == 0) {
+            CK(cudaMemcpyAsync(dst, p, bytes, cudaMemcpyDeviceToHost, c.s));
+            c.sync();
+        }
+    }
+};
+
+size_t esize(int dtype) { return dtype == 1 ? 16 : 8; }
+
+double gershgorin_host(const std::vector<double>& D, const std::vector<double>& mu, int d, const long* N,
+                       double robin_face, double shift) {
+    const long n0 = N[0], n1 = N[1], n2 = d == 3 ? N[2] : 1;
+    double lm = 0.0;
+    auto hm = [](double a, double b) { return 2.0 * (a * b) / (a + b); };
+    for (long k = 0; k < n2; ++k)
+        for (long j = 0; j < n1; ++j)
+            for (long i = 0; i < n0; ++i) {
+                const long p = i + n0 * (j + n1 * k);
+                double diag = mu[p], off = 0.0;
+                const long idx[3] = {i, j, k};
+                const long len[3] = {n0, n1, n2};
+                const long st[3] = {1, n0, n0 * n1};
+                for (int ax = 0; ax < d; ++ax)
+                    for (int dir = -1; dir <= 1; dir += 2) {
+                        const long q = idx[ax] + dir;
+                        if (q >= 0 && q < len[ax]) {
+                            const double f = hm(D[p], D[p + dir * st[ax]]);
+                            diag += f;
+                            off += f;
+                        } else {
+                            diag += (ax == d - 1) ? robin_face : D[p];
+                        }
+                    }
+                lm = std::max(lm, std::fabs(diag) + std::fabs(shift) + off);
+            }
+    return lm;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* rd_last_error(void) { return g_err.c_str(); }
+
+int rd_ctx_create(int device, rd_ctx** out) {
+    return guard([&] {
+        auto* c = new rd_ctx();
+        try {
+            c->c.init(device);
+        } catch (...) {
+            delete c;
+            throw;
+        }
+        *out = c;
+    });
+}
+void rd_ctx_destroy(rd_ctx* ctx) { delete ctx; }
+int rd_ctx_sync(rd_ctx* ctx) {
+    return guard([&] { ctx->c.sync(); });
+}
+int rd_ctx_mark(rd_ctx* ctx) {
+    return guard([&] {
+        Ctx& c = ctx->c;
+        cudaEvent_t e = c.mark[c.nmark & 1];
+        CK(cudaEventRecord(e, c.s));
+        ++c.nmark;
+    });
+}
+double rd_ctx_elapsed_ms(rd_ctx* ctx) {
+    Ctx& c = ctx->c;
+    if (c.nmark < 2) return -1.0;
+    cudaEvent_t a = c.mark[(c.nmark - 2) & 1], b = c.mark[(c.nmark - 1) & 1];
+    float ms = -1.f;
+    if (cudaEventSynchronize(b) != cudaSuccess) return -1.0;
+    if (cudaEventElapsedTime(&ms, a, b) != cudaSuccess) return -1.0;
+    return ms;
+}
+long rd_ctx_launches(rd_ctx* ctx) { return ctx->c.launches; }
+void* rd_ctx_stream(rd_ctx* ctx) { return (void*)ctx->c.s; }
+
+int rd_op_create(rd_ctx* ctx, int d, const long* N, double robin_face, rd_op** out) {
+    return guard([&] {
+        if (d != 2 && d != 3) throw rd::ConfigError("operator: d must be 2 or 3");
+        for (int a = 0; a < d; ++a)
+            if (N[a] < 2) throw rd::ConfigError("operator: every axis needs at least 2 nodes");
+        auto* o = new rd_op();
+        o->ctx = ctx;
+        o->op.ctx = &ctx->c;
+        OpDev& od = o->op.d;
+        od.d = d;
+        od.N0 = (int)N[0];
+        od.N1 = (int)N[1];
+        od.N2 = d == 3 ? (int)N[2] : 1;
+        od.n = (long)od.N0 * od.N1 * od.N2;
+        od.robin_face = robin_face;
+        od.shift = 0.0;
+        *out = o;
+    });
+}
+void rd_op_destroy(rd_op* op) { delete op; }
+
+int rd_op_set_fields(rd_op* o, const double* D, const double* mu, double shift, int where) {
+    return guard([&] {
+        Ctx& c = o->ctx->c;
+        const long n = o->op.d.n;
+        o->op.D.ensure(sizeof(double) * n);
+        o->op.mu.ensure(sizeof(double) * n);
+        const auto kind = where == 1 ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
+        CK(cudaMemcpyAsync(o->op.D.p, D, sizeof(double) * n, kind, c.s));
+        CK(cudaMemcpyAsync(o->op.mu.p, mu, sizeof(double) * n, kind, c.s));
+        o->op.d.D = o->op.D.template as<double>();
+        o->op.d.mu = o->op.mu.template as<double>();
+        o->op.d.shift = shift;
+        o->op.have_fields = true;
+        if (where == 0) {
+            std::vector<double> Dh(D, D + n), mh(mu, mu + n);
+            const long N[3] = {o->op.d.N0, o->op.d.N1, o->op.d.N2};
+            o->op.lam_max = gershgorin_host(Dh, mh, o->op.d.d, N, o->op.d.robin_face, shift);
+        } else {
+            o->op.lam_max = 0.0;  // computed lazily by the eigensolver
+        }
+    });
+}
+
+double rd_op_lam_max(rd_op* op) { return op->op.lam_max; }
+
+int rd_op_apply(rd_op* o, int dtype, const void* x, void* y, long ncols, int where) {
+    return guard([&] {
+        Ctx& c = o->ctx->c;
+        if (!o->op.have_fields) throw rd::ConfigError("operator: fields not set");
+        const long n = o->op.d.n;
+        const size_t bytes = esize(dtype) * n * ncols;
+        Staged xs(c, x, bytes, where);
+        Out ys(c, y, bytes, where);
+        if (dtype == 0)
+            launch_stencil<double>(c, o->op.d, (const double*)xs.p, n, nullptr, (double*)ys.p, n, ncols);
+        else
+            launch_stencil<cplx>(c, o->op.d, (const cplx*)xs.p, n, nullptr, (cplx*)ys.p, n, ncols);
+        ys.finish();
+        if (where == 1) c.sync();
+    });
+}
+
+int rd_recycled_solve(rd_op* o, int dtype, const void* U, const void* K, long c, const void* rhs, double tol,
+                      long maxit, double rhs_scale, void* g, void* y, void* image, rd_report* rep, double* hist,
+                      long hist_cap, int where) {
+    return guard([&] {
+        Ctx& cx = o->ctx->c;
+        if (!o->op.have_fields) throw rd::ConfigError("operator: fields not set");
+        const long n = o->op.d.n;
+        const size_t es = esize(dtype);
+        Staged Us(cx, c ? U : nullptr, es * n * c, where), Ks(cx, c ? K : nullptr, es * n * c, where);
+        Staged rs(cx, rhs, es * n, where);
+        Out gs(cx, g, es * n, where), ys(cx, y, es * n, where), is(cx, image, es * n, where);
+        DevBuf gt, yt, it;
+        void* gp = gs.p;
+        void* yp = ys.p;
+        void* ip = is.p;
+        if (!gp) {
+            gt.ensure(es * n);
+            gp = gt.p;
+        }
+        if (!yp) {
+            yt.ensure(es * n);
+            yp = yt.p;
+        }
+        if (!ip) {
+            it.ensure(es * n);
+            ip = it.p;
+        }
+        SolveOut so;
+        if (dtype == 0) {
+            Workspace<double> ws;
+            so = recycled_cg<double>(cx, o->op, (const double*)Us.p, (const double*)Ks.p, c, (const double*)rs.p, tol,
+                                     maxit, rhs_scale, (double*)gp, (double*)yp, (double*)ip, ws, hist != nullptr);
+        } else {
+            Workspace<cplx> ws;
+            so = recycled_cg<cplx>(cx, o->op, (const cplx*)Us.p, (const cplx*)Ks.p, c, (const cplx*)rs.p, tol, maxit,
+                                   rhs_scale, (cplx*)gp, (cplx*)yp, (cplx*)ip, ws, hist != nullptr);
+        }
+        // correction norm
+        double* nrm = cx.sc(3);
+        if (dtype == 0)
+            launch_norms<double>(cx, (const double*)gp, n, nrm);
+        else
+            launch_norms<cplx>(cx, (const cplx*)gp, n, nrm);
+        double h;
+        CK(cudaMemcpyAsync(&h, nrm, sizeof(double), cudaMemcpyDeviceToHost, cx.s));
+        gs.finish();
+        ys.finish();
+        is.finish();
+        cx.sync();
+        if (rep) {
+            rep->iterations = so.iterations;
+            rep->converged = so.converged ? 1 : 0;
+            rep->final_relres = so.final_relres;
+            rep->correction_norm = std::sqrt(h);
+        }
+        if (hist)
+            for (long i = 0; i < std::min<long>(hist_cap, (long)so.hist.size()); ++i) hist[i] = so.hist[i];
+    });
+}
+
+int rd_recycle_space_from_raw(rd_ctx* ctx, int dtype, long n, long c, const void* Wr, const void* AW, void* U,
+                              void* K, int where) {
+    return guard([&] {
+        Ctx& cx = ctx->c;
+        const size_t es = esize(dtype);
+        Staged Ws(cx, Wr, es * n * c, where), As(cx, AW, es * n * c, where);
+        Out Us(cx, U, es * n * c, where), Ks(cx, K, es * n * c, where);
+        if (dtype == 0)
+            from_raw<double>(cx, n, c, (const double*)Ws.p, nullptr, (const double*)As.p, (double*)Us.p,
+                             (double*)Ks.p);
+        else
+            from_raw<cplx>(cx, n, c, (const cplx*)Ws.p, nullptr, (const cplx*)As.p, (cplx*)Us.p, (cplx*)Ks.p);
+        Us.finish();
+        Ks.finish();
+        cx.sync();
+    });
+}
+
+int rd_initial_solutions(rd_op* o, int dtype, long nrhs, const long* bidx, const double* bval, double tol,
+                         void* X0, int where, long* total_iterations) {
+    return guard([&] {
+        Ctx& cx = o->ctx->c;
+        const long n = o->op.d.n;
+        const size_t es = esize(dtype);
+        Out Xs(cx, X0, es * n * nrhs, where);
+        DevBuf b, y, im, g;
+        b.ensure(es * n);
+        y.ensure(es * n);
+        im.ensure(es * n);
+        if (!Xs.p) g.ensure(es * n);
+        long tot = 0;
+        auto run = [&](auto tag) {
+            using T = decltype(tag);
+            Workspace<T> ws;
+            for (long j = 0; j < nrhs; ++j) {
+                CK(cudaMemsetAsync(b.p, 0, es * n, cx.s));
+                T v = Sc<T>::from(bval[j]);
+                CK(cudaMemcpyAsync(b.template as<T>() + bidx[j], &v, sizeof(T), cudaMemcpyHostToDevice, cx.s));
+                T* gj = Xs.p ? (T*)Xs.p + (size_t)j * n : g.template as<T>();
+                SolveOut so = recycled_cg<T>(cx, o->op, nullptr, nullptr, 0, b.template as<T>(), kInnerSafety * tol, 2 * n,
+                                             0.0, gj, y.template as<T>(), im.template as<T>(), ws, false);
+                if (!so.converged)
+                    throw rd::SolverError("init_basis: CG failed on initial solution column " + std::to_string(j));
+                tot += so.iterations;
+            }
+        };
+        if (dtype == 0)
+            run(double{});
+        else
+            run(cplx{});
+        Xs.finish();
+        cx.sync();
+        if (total_iterations) *total_iterations = tot;
+    });
+}
+
+int rd_basis_create(rd_ctx* ctx, int dtype, long n, long ku, long nrhs, const void* U0, const void* X0, long cap,
+                    int where, rd_basis** out) {
+    return guard([&] {
+        Ctx& cx = ctx->c;
+        auto* b = new rd_basis();
+        b->ctx = ctx;
+        b->h.ctx = &cx;
+        b->h.dtype = dtype;
+        auto setup = [&](auto& gb, auto tag) {
+            using T = decltype(tag);
+            gb.reset(new DevBasis<T>());
+            DevBasis<T>& B = *gb;
+            B.ctx = &cx;
+            B.n = n;
+            B.cap = cap;
+            B.ku = ku;
+            B.reserve(std::max(ku + nrhs, 16L));
+            const auto kind = where == 1 ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
+            if (ku) CK(cudaMemcpyAsync(B.Vp(), U0, sizeof(T) * n * ku, kind, cx.s));
+            if (nrhs) CK(cudaMemcpyAsync(B.Vp() + (size_t)n * ku, X0, sizeof(T) * n * nrhs, kind, cx.s));
+            B.cols = ku + nrhs;
+            B.markers.assign(ku, kColEigenvector);
+            B.markers.insert(B.markers.end(), nrhs, kColInitialSolution);
+            B.spaces.assign(nrhs, {});
+            for (long j = 0; j < nrhs; ++j) {
+                for (long i = 0; i < ku; ++i) B.spaces[j].push_back((int)i);
+                B.spaces[j].push_back((int)(ku + j));
+            }
+            cx.sync();
+        };
+        if (dtype == 0)
+            setup(b->h.r, double{});
+        else
+            setup(b->h.c, cplx{});
+        *out = b;
+    });
+}
+void rd_basis_destroy(rd_basis* b) { delete b; }
+
+#define BASIS_DISPATCH(b, ...)     \
+    if ((b)->h.dtype == 0) {       \
+        auto& B = *(b)->h.r;       \
+        __VA_ARGS__;               \
+    } else {                       \
+        auto& B = *(b)->h.c;       \
+        __VA_ARGS__;               \
+    }
+
+long rd_basis_cols(rd_basis* b) {
+    long v = 0;
+    BASIS_DISPATCH(b, v = B.cols);
+    return v;
+}
+long rd_basis_eig_block(rd_basis* b) {
+    long v = 0;
+    BASIS_DISPATCH(b, v = B.ku);
+    return v;
+}
+void* rd_basis_device_ptr(rd_basis* b, int which) {
+    void* p = nullptr;
+    BASIS_DISPATCH(b, p = which == 0 ? (void*)B.Vp() : which == 1 ? (void*)B.Kp() : (void*)B.Wp());
+    return p;
+}
+int rd_basis_get(rd_basis* b, int which, void* out) {
+    return guard([&] {
+        BASIS_DISPATCH(b, {
+            using T = std::remove_reference_t<decltype(B.R[0])>;
+            if (which == 2) {
+                T* o = (T*)out;
+                for (long j = 0; j < B.cols; ++j)
+                    for (long i = 0; i < B.cols; ++i) o[i + j * B.cols] = i <= j ? B.Rat(i, j) : Sc<T>::zero();
+            } else {
+                const T* src = which == 0 ? B.Vp() : which == 1 ? B.Kp() : B.Wp();
+                CK(cudaMemcpyAsync(out, src, sizeof(T) * B.n * B.cols, cudaMemcpyDeviceToHost, b->ctx->c.s));
+                b->ctx->c.sync();
+            }
+        });
+    });
+}
+int rd_basis_markers(rd_basis* b, uint8_t* out) {
+    return guard([&] { BASIS_DISPATCH(b, std::memcpy(out, B.markers.data(), B.markers.size())); });
+}
+long rd_basis_space(rd_basis* b, long j, int* out) {
+    long m = -1;
+    BASIS_DISPATCH(b, {
+        if (j >= 0 && j < (long)B.spaces.size()) {
+            m = (long)B.spaces[j].size();
+            if (out) std::memcpy(out, B.spaces[j].data(), sizeof(int) * m);
+        }
+    });
+    return m;
+}
+int rd_basis_refresh(rd_basis* b, rd_op* op) {
+    return guard([&] { BASIS_DISPATCH(b, B.refresh(op->op)); });
+}
+int rd_basis_append(rd_basis* b, const void* y, const void* z, int marker, int where, int* appended) {
+    return guard([&] {
+        Ctx& cx = b->ctx->c;
+        BASIS_DISPATCH(b, {
+            using T = std::remove_reference_t<decltype(B.R[0])>;
+            Staged ys(cx, y, sizeof(T) * B.n, where), zs(cx, z, sizeof(T) * B.n, where);
+            const bool ok = B.append((const T*)ys.p, (const T*)zs.p, (uint8_t)marker);
+            if (appended) *appended = ok ? 1 : 0;
+        });
+    });
+}
+int rd_basis_solve_projected(rd_basis* b, const void* rhs, void* x, void* coords, int where) {
+    return guard([&] {
+        Ctx& cx = b->ctx->c;
+        BASIS_DISPATCH(b, {
+            using T = std::remove_reference_t<decltype(B.R[0])>;
+            constexpr int W = Sc<T>::W;
+            const long n = B.n, r = B.cols;
+            Staged bs(cx, rhs, sizeof(T) * n, where);
+            Out xs(cx, x, sizeof(T) * n, where);
+            DevBuf w, zero, xt;
+            w.ensure(sizeof(double) * W * std::max(1L, r));
+            zero.ensure(sizeof(T) * n);
+            CK(cudaMemsetAsync(zero.p, 0, sizeof(T) * n, cx.s));
+            ts_T_launch<T, true>(cx, B.Kp(), n, r, (const T*)bs.p, n, w.template as<double>());
+            void* xp = xs.p;
+            if (!xp) {
+                xt.ensure(sizeof(T) * n);
+                xp = xt.p;
+            }
+            ts_N_launch<T>(cx, B.Wp(), n, r, zero.template as<T>(), (T*)xp, n, w.template as<double>(), -1.0);
+            xs.finish();
+            if (coords) {
+                // c = R^-1 w (host triangular solve on the r x r factor)
+                std::vector<T> wc(r);
+                CK(cudaMemcpyAsync(wc.data(), w.p, sizeof(T) * r, cudaMemcpyDeviceToHost, cx.s));
+                cx.sync();
+                for (long i = r - 1; i >= 0; --i) {
+                    T s = wc[i];
+                    for (long k = i + 1; k < r; ++k) s = Sc<T>::sub(s, Sc<T>::mul(B.Rat(i, k), wc[k]));
+                    wc[i] = Sc<T>::div(s, B.Rat(i, i));
+                }
+                std::memcpy(coords, wc.data(), sizeof(T) * r);
+            }
+            cx.sync();
+        });
+    });
+}
+
+int rd_process_system(rd_basis* b, rd_op* op, long nrhs, const long* bidx, const double* bval, double tol,
+                      int system_index, long maxit, void* X, int where, double* log, long* inner_iterations,
+                      long* appends) {
+    return guard([&] {
+        Ctx& cx = b->ctx->c;
+        if (!op->op.have_fields) throw rd::ConfigError("operator: fields not set");
+        BASIS_DISPATCH(b, {
+            using T = std::remove_reference_t<decltype(B.R[0])>;
+            if (B.n != op->op.d.n) throw rd::ConfigError("process_system: dimension mismatch");
+            Out xs(cx, X, sizeof(T) * B.n * nrhs, where);
+            if (X && where == 0) B.X.ensure(sizeof(T) * B.n * nrhs);
+            T* Xd = X ? (where == 0 ? B.X.template as<T>() : (T*)X) : nullptr;
+            std::vector<LogRow> lg;
+            long its = 0, app = 0;
+            process_system<T>(B, op->op, nrhs, bidx, bval, tol, system_index, maxit, Xd, lg, its, app);
+            if (X && where == 0) {
+                CK(cudaMemcpyAsync(X, Xd, sizeof(T) * B.n * nrhs, cudaMemcpyDeviceToHost, cx.s));
+                cx.sync();
+            }
+            if (log)
+                for (size_t t = 0; t < lg.size(); ++t) {
+                    log[5 * t + 0] = lg[t].system;
+                    log[5 * t + 1] = lg[t].rhs;
+                    log[5 * t + 2] = lg[t].init_relres;
+                    log[5 * t + 3] = lg[t].iterations;
+                    log[5 * t + 4] = lg[t].appended ? 1.0 : 0.0;
+                }
+            if (inner_iterations) *inner_iterations = its;
+            if (appends) *appends = app;
+        });
+    });
+}
+
+int rd_smallest_eigenpairs(rd_op* op, long k, double tol, double* lambda, void* U, int where) {
+    (void)op;
+    (void)k;
+    (void)tol;
+    (void)lambda;
+    (void)U;
+    (void)where;
+    g_err = "rd_smallest_eigenpairs: not built yet";
+    return 1;
+}
+
+int rd_rrqr(rd_ctx* ctx, int dtype, long n, long m, const void* A, double tol, int normalize, long* rank, long* perm,
+            double* rdiag, void* Q, int where) {
+    (void)ctx;
+    (void)dtype;
+    (void)n;
+    (void)m;
+    (void)A;
+    (void)tol;
+    (void)normalize;
+    (void)rank;
+    (void)perm;
+    (void)rdiag;
+    (void)Q;
+    (void)where;
+    g_err = "rd_rrqr: not built yet";
+    return 1;
+}
+
+}  // extern "C"

@@ -1,0 +1,438 @@
+"""Python mirror of the reference's basis-builder API over the C ABI
+(include/romdot_b200.h), backed by libromdot_b200.so (CUDA, sm_100a).
+
+Names and semantics follow the reference (proj/include/romdot/{grid,krylov,
+basis}.hpp): ``SchurOperator.apply``, ``RecycleSpace``, ``recycled_cg`` (the
+CG/COCG counterpart of ``recycled_minres``), ``GlobalBasis`` with
+``refresh/append/solve_projected/projected_coordinates/V/K_img/R/markers``,
+``init_basis`` / ``init_basis_from`` and ``process_system``. Errors map to
+``ConfigError`` / ``SolverError`` like the reference's exception taxonomy
+(include/romdot/types.hpp:20-30).
+
+There is no CPU fallback: importing this module without the built library, or
+calling it without a CUDA device, raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from dataclasses import dataclass
+from typing import List, Optional
+
+import numpy as np
+
+from . import problem as P
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SO = os.path.join(_HERE, "libromdot_b200.so")
+
+EXPORTS = [
+    "rd_ctx_create", "rd_ctx_destroy", "rd_last_error", "rd_ctx_sync", "rd_ctx_mark", "rd_ctx_elapsed_ms",
+    "rd_ctx_launches", "rd_ctx_stream", "rd_op_create", "rd_op_destroy", "rd_op_set_fields", "rd_op_apply",
+    "rd_op_lam_max", "rd_recycled_solve", "rd_recycle_space_from_raw", "rd_initial_solutions",
+    "rd_smallest_eigenpairs", "rd_basis_create", "rd_basis_destroy", "rd_basis_cols", "rd_basis_eig_block",
+    "rd_basis_get", "rd_basis_device_ptr", "rd_basis_markers", "rd_basis_space", "rd_basis_refresh",
+    "rd_basis_append", "rd_basis_solve_projected", "rd_process_system", "rd_rrqr",
+]
+
+
+class RomdotError(RuntimeError):
+    def __init__(self, code, msg):
+        super().__init__(msg)
+        self.code = code
+
+
+class ConfigError(RomdotError):
+    pass
+
+
+class SolverError(RomdotError):
+    pass
+
+
+class CudaError(RomdotError):
+    pass
+
+
+class _Report(C.Structure):
+    _fields_ = [("iterations", C.c_int), ("converged", C.c_int), ("correction_norm", C.c_double),
+                ("final_relres", C.c_double)]
+
+
+_LIB = None
+
+
+def load_library(path: Optional[str] = None):
+    """Load libromdot_b200.so (raises if it has not been built)."""
+    global _LIB
+    if _LIB is not None:
+        return _LIB
+    so = path or _SO
+    if not os.path.exists(so):
+        raise ImportError(f"{so} not built: run `python -m paper_1602_00138_b200.build` (no CPU fallback)")
+    L = C.CDLL(so)
+    vp, lp, ip, dp = C.c_void_p, C.POINTER(C.c_long), C.POINTER(C.c_int), C.POINTER(C.c_double)
+    L.rd_last_error.restype = C.c_char_p
+    L.rd_ctx_create.argtypes = [C.c_int, C.POINTER(vp)]
+    L.rd_ctx_destroy.argtypes = [vp]
+    L.rd_ctx_sync.argtypes = [vp]
+    L.rd_ctx_mark.argtypes = [vp]
+    L.rd_ctx_elapsed_ms.argtypes = [vp]
+    L.rd_ctx_elapsed_ms.restype = C.c_double
+    L.rd_ctx_launches.argtypes = [vp]
+    L.rd_ctx_launches.restype = C.c_long
+    L.rd_ctx_stream.argtypes = [vp]
+    L.rd_ctx_stream.restype = vp
+    L.rd_op_create.argtypes = [vp, C.c_int, lp, C.c_double, C.POINTER(vp)]
+    L.rd_op_destroy.argtypes = [vp]
+    L.rd_op_set_fields.argtypes = [vp, vp, vp, C.c_double, C.c_int]
+    L.rd_op_apply.argtypes = [vp, C.c_int, vp, vp, C.c_long, C.c_int]
+    L.rd_op_lam_max.argtypes = [vp]
+    L.rd_op_lam_max.restype = C.c_double
+    L.rd_recycled_solve.argtypes = [vp, C.c_int, vp, vp, C.c_long, vp, C.c_double, C.c_long, C.c_double, vp, vp, vp,
+                                    C.POINTER(_Report), vp, C.c_long, C.c_int]
+    L.rd_recycle_space_from_raw.argtypes = [vp, C.c_int, C.c_long, C.c_long, vp, vp, vp, vp, C.c_int]
+    L.rd_initial_solutions.argtypes = [vp, C.c_int, C.c_long, vp, vp, C.c_double, vp, C.c_int, lp]
+    L.rd_smallest_eigenpairs.argtypes = [vp, C.c_long, C.c_double, vp, vp, C.c_int]
+    L.rd_basis_create.argtypes = [vp, C.c_int, C.c_long, C.c_long, C.c_long, vp, vp, C.c_long, C.c_int,
+                                  C.POINTER(vp)]
+    L.rd_basis_destroy.argtypes = [vp]
+    L.rd_basis_cols.argtypes = [vp]
+    L.rd_basis_cols.restype = C.c_long
+    L.rd_basis_eig_block.argtypes = [vp]
+    L.rd_basis_eig_block.restype = C.c_long
+    L.rd_basis_get.argtypes = [vp, C.c_int, vp]
+    L.rd_basis_device_ptr.argtypes = [vp, C.c_int]
+    L.rd_basis_device_ptr.restype = vp
+    L.rd_basis_markers.argtypes = [vp, vp]
+    L.rd_basis_space.argtypes = [vp, C.c_long, vp]
+    L.rd_basis_space.restype = C.c_long
+    L.rd_basis_refresh.argtypes = [vp, vp]
+    L.rd_basis_append.argtypes = [vp, vp, vp, C.c_int, C.c_int, ip]
+    L.rd_basis_solve_projected.argtypes = [vp, vp, vp, vp, C.c_int]
+    L.rd_process_system.argtypes = [vp, vp, C.c_long, vp, vp, C.c_double, C.c_int, C.c_long, vp, C.c_int, vp, lp,
+                                    lp]
+    L.rd_rrqr.argtypes = [vp, C.c_int, C.c_long, C.c_long, vp, C.c_double, C.c_int, lp, vp, vp, vp, C.c_int]
+    _LIB = L
+    return L
+
+
+def _check(rc):
+    if rc != 0:
+        msg = load_library().rd_last_error().decode()
+        raise {2: ConfigError, 3: SolverError, 5: CudaError}.get(rc, RomdotError)(rc, msg)
+
+
+def _p(a):
+    return None if a is None else a.ctypes.data_as(C.c_void_p)
+
+
+def _dt(dtype) -> int:
+    return 1 if np.dtype(dtype) == np.complex128 else 0
+
+
+def _f(a, dtype):
+    return np.asfortranarray(a, dtype=dtype)
+
+
+HOST, DEVICE = 0, 1
+
+
+class Context:
+    """Device, stream and reduction workspace (one per host thread)."""
+
+    def __init__(self, device: int = 0):
+        L = load_library()
+        h = C.c_void_p()
+        _check(L.rd_ctx_create(device, C.byref(h)))
+        self.h = h
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            load_library().rd_ctx_destroy(self.h)
+            self.h = None
+
+    def sync(self):
+        _check(load_library().rd_ctx_sync(self.h))
+
+    def mark(self):
+        _check(load_library().rd_ctx_mark(self.h))
+
+    def elapsed_ms(self) -> float:
+        return load_library().rd_ctx_elapsed_ms(self.h)
+
+    @property
+    def launches(self) -> int:
+        return load_library().rd_ctx_launches(self.h)
+
+    @property
+    def stream(self) -> int:
+        return load_library().rd_ctx_stream(self.h)
+
+
+_DEFAULT_CTX: Optional[Context] = None
+
+
+def default_context() -> Context:
+    global _DEFAULT_CTX
+    if _DEFAULT_CTX is None:
+        _DEFAULT_CTX = Context(0)
+    return _DEFAULT_CTX
+
+
+class SchurOperator:
+    """Device Schur operator A~(p) (grid.hpp:100-114): 5/7-point variable-D
+    stencil with the eliminated Robin layers, coefficient fields per system."""
+
+    def __init__(self, grid: P.GridSpec, fields: Optional[P.Fields] = None, dtype=np.float64,
+                 ctx: Optional[Context] = None):
+        self.ctx = ctx or default_context()
+        self.grid = grid
+        self.n = grid.n
+        self.dtype = np.dtype(dtype)
+        N = (C.c_long * 3)(*(list(grid.N) + [1] * (3 - grid.d)))
+        h = C.c_void_p()
+        _check(load_library().rd_op_create(self.ctx.h, grid.d, N, grid.robin_face, C.byref(h)))
+        self.h = h
+        if fields is not None:
+            self.set_fields(fields)
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            load_library().rd_op_destroy(self.h)
+            self.h = None
+
+    def set_fields(self, fields: P.Fields, where: int = HOST, D_ptr=None, mu_ptr=None):
+        if where == DEVICE:
+            _check(load_library().rd_op_set_fields(self.h, D_ptr, mu_ptr, float(fields.shift), DEVICE))
+        else:
+            D = np.ascontiguousarray(fields.D, dtype=np.float64)
+            mu = np.ascontiguousarray(fields.mu, dtype=np.float64)
+            _check(load_library().rd_op_set_fields(self.h, _p(D), _p(mu), float(fields.shift), HOST))
+        self.fields = fields
+
+    @property
+    def lam_max(self) -> float:
+        return load_library().rd_op_lam_max(self.h)
+
+    def apply(self, x: np.ndarray) -> np.ndarray:
+        x = _f(x, self.dtype)
+        y = np.zeros_like(x)
+        ncols = 1 if x.ndim == 1 else x.shape[1]
+        _check(load_library().rd_op_apply(self.h, _dt(self.dtype), _p(x), _p(y), ncols, HOST))
+        return y
+
+
+@dataclass
+class SolveReport:
+    iterations: int
+    converged: bool
+    rel_residual_history: np.ndarray
+    correction_norm: float
+    final_relres: float
+
+
+@dataclass
+class RecycledResult:
+    correction: np.ndarray
+    new_direction: np.ndarray
+    image: np.ndarray
+    report: SolveReport
+
+
+def recycled_cg(op: SchurOperator, U: Optional[np.ndarray], K: Optional[np.ndarray], rhs, tol, maxit,
+                rhs_scale: float = 0.0) -> RecycledResult:
+    """Deflated CG / COCG on the correction equation (krylov.hpp:53-58 semantics)."""
+    dt = op.dtype
+    rhs = np.ascontiguousarray(rhs, dtype=dt)
+    c = 0 if U is None else U.shape[1]
+    Uf = _f(U, dt) if c else None
+    Kf = _f(K, dt) if c else None
+    g, y, im = (np.zeros(op.n, dtype=dt) for _ in range(3))
+    rep = _Report()
+    hist = np.zeros(min(maxit + 2, 1 << 16))
+    _check(load_library().rd_recycled_solve(op.h, _dt(dt), _p(Uf), _p(Kf), c, _p(rhs), tol, maxit, rhs_scale,
+                                            _p(g), _p(y), _p(im), C.byref(rep), _p(hist), hist.size, HOST))
+    m = min(rep.iterations + 1, hist.size)
+    return RecycledResult(g, y, im, SolveReport(rep.iterations, bool(rep.converged), hist[:m].copy(),
+                                                rep.correction_norm, rep.final_relres))
+
+
+def recycle_space_from_raw(W: np.ndarray, AW: np.ndarray, ctx: Optional[Context] = None):
+    """RecycleSpace::from_raw (krylov.cpp:106-115) on the device: returns (U, K)."""
+    ctx = ctx or default_context()
+    dt = W.dtype
+    W = _f(W, dt)
+    AW = _f(AW, dt)
+    U = np.zeros_like(W)
+    K = np.zeros_like(W)
+    _check(load_library().rd_recycle_space_from_raw(ctx.h, _dt(dt), W.shape[0], W.shape[1], _p(W), _p(AW), _p(U),
+                                                    _p(K), HOST))
+    return U, K
+
+
+def initial_solutions(op: SchurOperator, layout: P.Layout, tol: float):
+    """X0 columns of init_basis (basis.cpp:141-149), CG/COCG at 0.25 tol."""
+    idx = np.ascontiguousarray(layout.idx, dtype=np.int64)
+    val = np.ascontiguousarray(layout.val, dtype=np.float64)
+    X0 = np.zeros((op.n, layout.n_rhs), dtype=op.dtype, order="F")
+    tot = C.c_long()
+    _check(load_library().rd_initial_solutions(op.h, _dt(op.dtype), layout.n_rhs, _p(idx), _p(val), tol, _p(X0),
+                                               HOST, C.byref(tot)))
+    return X0, tot.value
+
+
+def smallest_eigenpairs(op: SchurOperator, k: int, tol: float = 1e-8):
+    lam = np.zeros(k)
+    U = np.zeros((op.n, k), order="F")
+    _check(load_library().rd_smallest_eigenpairs(op.h, k, tol, _p(lam), _p(U), HOST))
+    return lam, U
+
+
+@dataclass
+class BuildLogRow:
+    system: int
+    rhs: int
+    init_relres: float
+    iterations: int
+    appended: bool
+
+
+@dataclass
+class ProcessResult:
+    X: Optional[np.ndarray]
+    log: List[BuildLogRow]
+    inner_iterations: int
+    appends: int
+
+
+class GlobalBasis:
+    """Device GlobalBasis + PerRhsSpaces (basis.hpp:28-70)."""
+
+    def __init__(self, U0: np.ndarray, X0: np.ndarray, cap: int = 0, ctx: Optional[Context] = None,
+                 dtype=None):
+        self.ctx = ctx or default_context()
+        dt = np.dtype(dtype) if dtype is not None else np.result_type(U0.dtype, X0.dtype)
+        U0 = _f(U0, dt)
+        X0 = _f(X0, dt)
+        self.dtype = dt
+        self.n = X0.shape[0]
+        self.nrhs = X0.shape[1]
+        h = C.c_void_p()
+        _check(load_library().rd_basis_create(self.ctx.h, _dt(dt), self.n, U0.shape[1], X0.shape[1], _p(U0), _p(X0),
+                                              cap, HOST, C.byref(h)))
+        self.h = h
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            load_library().rd_basis_destroy(self.h)
+            self.h = None
+
+    @property
+    def cols(self) -> int:
+        return load_library().rd_basis_cols(self.h)
+
+    @property
+    def eig_block(self) -> int:
+        return load_library().rd_basis_eig_block(self.h)
+
+    def _get(self, which, shape):
+        out = np.zeros(shape, dtype=self.dtype, order="F")
+        _check(load_library().rd_basis_get(self.h, which, _p(out)))
+        return out
+
+    @property
+    def V(self):
+        return self._get(0, (self.n, self.cols))
+
+    @property
+    def K_img(self):
+        return self._get(1, (self.n, self.cols))
+
+    @property
+    def R(self):
+        return self._get(2, (self.cols, self.cols))
+
+    @property
+    def W(self):
+        return self._get(3, (self.n, self.cols))
+
+    @property
+    def markers(self):
+        out = np.zeros(max(1, self.cols), dtype=np.uint8)
+        _check(load_library().rd_basis_markers(self.h, _p(out)))
+        return out[: self.cols]
+
+    def space(self, j) -> List[int]:
+        m = load_library().rd_basis_space(self.h, j, None)
+        out = np.zeros(max(m, 1), dtype=np.int32)
+        load_library().rd_basis_space(self.h, j, _p(out))
+        return out[:m].tolist()
+
+    def refresh(self, op: SchurOperator):
+        _check(load_library().rd_basis_refresh(self.h, op.h))
+
+    def append(self, y, z, marker: int = 2) -> bool:
+        y = np.ascontiguousarray(y, dtype=self.dtype)
+        z = np.ascontiguousarray(z, dtype=self.dtype)
+        ok = C.c_int()
+        _check(load_library().rd_basis_append(self.h, _p(y), _p(z), marker, HOST, C.byref(ok)))
+        return bool(ok.value)
+
+    def solve_projected(self, b):
+        b = np.ascontiguousarray(b, dtype=self.dtype)
+        x = np.zeros(self.n, dtype=self.dtype)
+        _check(load_library().rd_basis_solve_projected(self.h, _p(b), _p(x), None, HOST))
+        return x
+
+    def projected_coordinates(self, b):
+        b = np.ascontiguousarray(b, dtype=self.dtype)
+        x = np.zeros(self.n, dtype=self.dtype)
+        c = np.zeros(self.cols, dtype=self.dtype)
+        _check(load_library().rd_basis_solve_projected(self.h, _p(b), _p(x), _p(c), HOST))
+        return c
+
+
+def process_system(gb: GlobalBasis, op: SchurOperator, layout: P.Layout, tol: float, system_index: int,
+                   maxit: int = 0, want_X: bool = True) -> ProcessResult:
+    """Algorithm 2 main loop for one system (basis.cpp:157-207)."""
+    nrhs = layout.n_rhs
+    idx = np.ascontiguousarray(layout.idx, dtype=np.int64)
+    val = np.ascontiguousarray(layout.val, dtype=np.float64)
+    X = np.zeros((gb.n, nrhs), dtype=gb.dtype, order="F") if want_X else None
+    log = np.zeros((nrhs, 5))
+    its, app = C.c_long(), C.c_long()
+    _check(load_library().rd_process_system(gb.h, op.h, nrhs, _p(idx), _p(val), tol, system_index, maxit, _p(X),
+                                            HOST, _p(log), C.byref(its), C.byref(app)))
+    rows = [BuildLogRow(int(r[0]), int(r[1]), float(r[2]), int(r[3]), bool(r[4])) for r in log]
+    return ProcessResult(X, rows, its.value, app.value)
+
+
+def init_basis_from(U0, X0, cap: int = 0, ctx: Optional[Context] = None, dtype=None) -> GlobalBasis:
+    """basis.cpp:114-134."""
+    return GlobalBasis(U0, X0, cap, ctx, dtype)
+
+
+def init_basis(op0: SchurOperator, op0_real: SchurOperator, layout: P.Layout, k_eig: int, tol: float,
+               cap: int = 0, U0: Optional[np.ndarray] = None):
+    """basis.cpp:136-155: U0 = k_eig smallest eigenvectors of the omega = 0
+    operator (device Lanczos), X0 by CG/COCG at 0.25 tol."""
+    lam = None
+    if U0 is None:
+        lam, U0 = smallest_eigenpairs(op0_real, k_eig, min(tol, 1e-8))
+    X0, its = initial_solutions(op0, layout, tol)
+    gb = GlobalBasis(U0.astype(op0.dtype), X0, cap, op0.ctx)
+    return gb, X0, lam, U0
+
+
+def rrqr(A: np.ndarray, tol: float = 1e-10, normalize: bool = True, ctx: Optional[Context] = None):
+    ctx = ctx or default_context()
+    A = _f(A, A.dtype)
+    n, m = A.shape
+    rank = C.c_long()
+    perm = np.zeros(m, dtype=np.int64)
+    rdiag = np.zeros(m)
+    Q = np.zeros((n, m), dtype=A.dtype, order="F")
+    _check(load_library().rd_rrqr(ctx.h, _dt(A.dtype), n, m, _p(A), tol, int(normalize), C.byref(rank), _p(perm),
+                                  _p(rdiag), _p(Q), HOST))
+    return rank.value, perm, rdiag, Q[:, : rank.value].copy()
