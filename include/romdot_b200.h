@@ -47,6 +47,11 @@ int rd_ctx_mark(rd_ctx* ctx);
 double rd_ctx_elapsed_ms(rd_ctx* ctx);
 /* Number of this library's kernel launches issued on the context so far. */
 long rd_ctx_launches(rd_ctx* ctx);
+/* Sampled per-kernel-class device timing of the inner iteration (CUDA events on
+ * the ctx stream, first iteration of each launch batch). enable resets the counters.
+ * cls: 0 cg_stencil_dots, 1 ts_T, 2 ts_NT, 3 cg_update. bytes = algorithmic bytes. */
+void rd_ctx_profile(rd_ctx* ctx, int enable);
+int rd_ctx_prof_get(rd_ctx* ctx, int cls, double* ms, double* bytes, long* samples);
 /* Raw stream handle (cudaStream_t) for interop. */
 void* rd_ctx_stream(rd_ctx* ctx);
 

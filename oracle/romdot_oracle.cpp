@@ -65,20 +65,67 @@ inline double abs2(cd x) { return x.real() * x.real() + x.imag() * x.imag(); }
 inline double sqrt_s(double x) { return std::sqrt(x); }
 inline cd sqrt_s(cd x) { return std::sqrt(x); }
 
-template <class T> T dotT(long n, const T* x, const T* y) {  // bilinear x^T y
+// Reductions use fixed 8192-element chunks summed in chunk order, so results
+// are identical for any OpenMP thread count (bitwise-deterministic oracle).
+constexpr long kChunk = 8192;
+
+template <class T, class F> T chunked_sum(long n, F term) {
+    const long nc = (n + kChunk - 1) / kChunk;
+    if (nc <= 1) {
+        T s = T(0);
+        for (long i = 0; i < n; ++i) s += term(i);
+        return s;
+    }
+    std::vector<T> part(nc, T(0));
+#pragma omp parallel for schedule(static) if (nc >= 4)
+    for (long c = 0; c < nc; ++c) {
+        T s = T(0);
+        const long e = std::min(n, (c + 1) * kChunk);
+        for (long i = c * kChunk; i < e; ++i) s += term(i);
+        part[c] = s;
+    }
     T s = T(0);
-    for (long i = 0; i < n; ++i) s += x[i] * y[i];
+    for (long c = 0; c < nc; ++c) s += part[c];
     return s;
+}
+template <class T> T dotT_seq(long n, const T* x, const T* y) {  // same chunk order, one thread
+    const long nc = (n + kChunk - 1) / kChunk;
+    T tot = T(0);
+    if (nc <= 1) {
+        for (long i = 0; i < n; ++i) tot += x[i] * y[i];
+        return tot;
+    }
+    for (long c = 0; c < nc; ++c) {
+        T s = T(0);
+        const long e = std::min(n, (c + 1) * kChunk);
+        for (long i = c * kChunk; i < e; ++i) s += x[i] * y[i];
+        tot += s;
+    }
+    return tot;
+}
+template <class T> T dotH_seq(long n, const T* x, const T* y) {
+    const long nc = (n + kChunk - 1) / kChunk;
+    T tot = T(0);
+    if (nc <= 1) {
+        for (long i = 0; i < n; ++i) tot += cj(x[i]) * y[i];
+        return tot;
+    }
+    for (long c = 0; c < nc; ++c) {
+        T s = T(0);
+        const long e = std::min(n, (c + 1) * kChunk);
+        for (long i = c * kChunk; i < e; ++i) s += cj(x[i]) * y[i];
+        tot += s;
+    }
+    return tot;
+}
+template <class T> T dotT(long n, const T* x, const T* y) {  // bilinear x^T y
+    return chunked_sum<T>(n, [&](long i) { return x[i] * y[i]; });
 }
 template <class T> T dotH(long n, const T* x, const T* y) {  // Hermitian x^H y
-    T s = T(0);
-    for (long i = 0; i < n; ++i) s += cj(x[i]) * y[i];
-    return s;
+    return chunked_sum<T>(n, [&](long i) { return cj(x[i]) * y[i]; });
 }
 template <class T> double nrm2(long n, const T* x) {
-    double s = 0.0;
-    for (long i = 0; i < n; ++i) s += abs2(x[i]);
-    return std::sqrt(s);
+    return std::sqrt(chunked_sum<double>(n, [&](long i) { return abs2(x[i]); }));
 }
 
 // ----------------------------------------------------- column-major matrix ---
@@ -131,7 +178,9 @@ struct GridOp {
     template <class T> void apply_one(const T* x, T* y) const {
         const long s1 = N[0], s2 = N[0] * N[1];
         const long n0 = N[0], n1 = N[1], n2 = N[2];
-        for (long k = 0; k < (d == 3 ? n2 : 1); ++k)
+        const long nk = (d == 3 ? n2 : 1);
+#pragma omp parallel for collapse(2) schedule(static) if (n >= 65536)
+        for (long k = 0; k < nk; ++k)
             for (long j = 0; j < n1; ++j)
                 for (long i = 0; i < n0; ++i) {
                     const long p = i + j * s1 + k * s2;
@@ -253,13 +302,24 @@ struct BandChol {
 // ---------------------------------------------------------- dense kernels ---
 // y -= K c ; c = K^op w  with op = T (bilinear) or H (Hermitian)
 template <class T> void gemv_op(const Mat<T>& K, long cols, const T* w, T* c, bool herm) {
-    for (long j = 0; j < cols; ++j) c[j] = herm ? dotH(K.r, K.col(j), w) : dotT(K.r, K.col(j), w);
+    if (cols >= 4) {
+#pragma omp parallel for schedule(dynamic, 1)
+        for (long j = 0; j < cols; ++j) c[j] = herm ? dotH_seq(K.r, K.col(j), w) : dotT_seq(K.r, K.col(j), w);
+    } else {
+        for (long j = 0; j < cols; ++j) c[j] = herm ? dotH(K.r, K.col(j), w) : dotT(K.r, K.col(j), w);
+    }
 }
 template <class T> void sub_Kc(const Mat<T>& K, long cols, const T* c, T* y) {
-    for (long j = 0; j < cols; ++j) {
-        const T cjv = c[j];
-        const T* kc = K.col(j);
-        for (long i = 0; i < K.r; ++i) y[i] -= kc[i] * cjv;
+    const long n = K.r;
+    const long nb = (n + kChunk - 1) / kChunk;
+#pragma omp parallel for schedule(static) if (nb >= 4)
+    for (long b = 0; b < nb; ++b) {
+        const long i0 = b * kChunk, i1 = std::min(n, i0 + kChunk);
+        for (long j = 0; j < cols; ++j) {
+            const T cjv = c[j];
+            const T* kc = K.col(j);
+            for (long i = i0; i < i1; ++i) y[i] -= kc[i] * cjv;
+        }
     }
 }
 
@@ -285,6 +345,7 @@ template <class T> void thin_qr(const Mat<T>& M, Mat<T>& Q, Mat<T>& R) {
         }
         // apply H_j^H = I - conj(tau) v v^H to trailing columns
         if (tau[j] != T(0)) {
+#pragma omp parallel for schedule(dynamic, 1) if (n * (m - j) >= 65536)
             for (long k = j + 1; k < m; ++k) {
                 T s = A(j, k);
                 for (long i = j + 1; i < n; ++i) s += cj(A(i, j)) * A(i, k);
@@ -301,6 +362,7 @@ template <class T> void thin_qr(const Mat<T>& M, Mat<T>& Q, Mat<T>& R) {
     for (long i = 0; i < m && i < n; ++i) Q(i, i) = T(1);
     for (long j = std::min(m, n) - 1; j >= 0; --j) {
         if (tau[j] == T(0)) continue;
+#pragma omp parallel for schedule(dynamic, 1) if (n * (m - j) >= 65536)
         for (long k = j; k < m; ++k) {
             T s = Q(j, k);
             for (long i = j + 1; i < n; ++i) s += cj(A(i, j)) * Q(i, k);
@@ -684,6 +746,7 @@ RecycledResult<T> recycled_cg(const LinOp<T>& A, const RecycleSpace<T>& rs, cons
                 gemv_op(rs.K, c, w.data(), c2.data(), false);
                 sub_Kc(rs.K, c, c2.data(), w.data());
             }
+#pragma omp parallel for schedule(static) if (n >= 65536)
             for (long i = 0; i < n; ++i) {
                 p[i] = r[i] + beta * p[i];
                 s[i] = w[i] + beta * s[i];

@@ -114,8 +114,8 @@ struct GridRed {
 };
 
 __device__ inline bool grid_commit(const GridRed& g, const double* vals, int nv) {
-    const unsigned nb = gridDim.x * gridDim.y;
-    const unsigned b = blockIdx.x + gridDim.x * blockIdx.y;
+    const unsigned nb = gridDim.x * gridDim.y * gridDim.z;
+    const unsigned b = blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z);
     for (int v = threadIdx.x; v < nv; v += blockDim.x) g.partials[(size_t)b * nv + v] = vals[v];
     __threadfence();
     __syncthreads();
@@ -130,7 +130,7 @@ __device__ inline bool grid_commit(const GridRed& g, const double* vals, int nv)
 // fixed-order combine). Resets the counter.
 __device__ inline void grid_finish(const GridRed& g, int nv, double* out /* shared or global */) {
     __threadfence();
-    const unsigned nb = gridDim.x * gridDim.y;
+    const unsigned nb = gridDim.x * gridDim.y * gridDim.z;
     int tpc = 1;
     while (tpc * 2 * nv <= (int)blockDim.x && tpc < 32) tpc *= 2;
     const int groups = blockDim.x / tpc;

@@ -1,4 +1,300 @@
-// Dense tall-skinny block kernels (Gram, block GEMM, small on-device
-// factorisations) -- filled in with the CholQR2 refresh and RRQR.
+// Block kernels for the tall-skinny factorisations (sm_100a, fp64 FMA pipes):
+//
+//   gram_kernel     G = op(X)^T Y, X: n x a, Y: n x b  (op = T or H). 64x64
+//                   (real) / 32x32 (complex) output tiles, 4x4 / 2x2 register
+//                   tile per thread, row chunks staged in shared memory,
+//                   deterministic split over n (slices reduced in order).
+//   gemm_tall       Z = X M  or  Z = Y - X M, X: n x a, M: a x b small
+//                   (device), row tiles of X staged in shared memory.
+//   small dense     single-CTA Cholesky (Hermitian or bilinear), upper
+//                   triangular inverse and product for the r x r factors.
+//
+// FP64 on B200 runs at the same rate on the FMA pipe as through DMMA, so the
+// Gram products use DFMA register tiling (tcgen05 has no f64 kind).
 #pragma once
+
 #include "common.cuh"
+
+namespace rd {
+
+template <class T> struct GT;  // tile geometry per scalar type
+template <> struct GT<double> {
+    static constexpr int TA = 64, TB = 64, KC = 32, RA = 4, RB = 4;
+};
+template <> struct GT<cplx> {
+    static constexpr int TA = 32, TB = 32, KC = 32, RA = 2, RB = 2;
+};
+
+// G_partial[slice][i][j] (column-major a x b per slice) = sum_{rows in slice} op(X[r,i]) Y[r,j]
+template <class T, bool HERM>
+__global__ void __launch_bounds__(256) gram_kernel(const T* __restrict__ X, long ldx, int a, const T* __restrict__ Y,
+                                                   long ldy, int b, long n, long rows_per_slice, T* __restrict__ part,
+                                                   bool sym_upper) {
+    constexpr int TA = GT<T>::TA, TB = GT<T>::TB, KC = GT<T>::KC, RA = GT<T>::RA, RB = GT<T>::RB;
+    const int ta = blockIdx.x, tb = blockIdx.y, sl = blockIdx.z;
+    if (sym_upper && ta > tb) return;
+    __shared__ T Xs[KC][TA + 1];
+    __shared__ T Ys[KC][TB + 1];
+    const int tx = threadIdx.x % (TB / RB), ty = threadIdx.x / (TB / RB);  // 16 x 16 threads
+    T acc[RA][RB];
+#pragma unroll
+    for (int i = 0; i < RA; ++i)
+#pragma unroll
+        for (int j = 0; j < RB; ++j) acc[i][j] = Sc<T>::zero();
+    const long r0 = (long)sl * rows_per_slice;
+    const long r1 = min(n, r0 + rows_per_slice);
+    const int col_a0 = ta * TA, col_b0 = tb * TB;
+    for (long rc = r0; rc < r1; rc += KC) {
+        // load KC rows x TA cols of X and TB cols of Y (lane = row within chunk)
+        const int lr = threadIdx.x % KC, lc = threadIdx.x / KC;  // 32 rows x 8 col groups
+        const long row = rc + lr;
+#pragma unroll
+        for (int c = lc; c < TA; c += 256 / KC) {
+            const int col = col_a0 + c;
+            Xs[lr][c] = (row < r1 && col < a) ? X[(size_t)col * ldx + row] : Sc<T>::zero();
+        }
+#pragma unroll
+        for (int c = lc; c < TB; c += 256 / KC) {
+            const int col = col_b0 + c;
+            Ys[lr][c] = (row < r1 && col < b) ? Y[(size_t)col * ldy + row] : Sc<T>::zero();
+        }
+        __syncthreads();
+#pragma unroll 8
+        for (int k = 0; k < KC; ++k) {
+            T xa[RA], yb[RB];
+#pragma unroll
+            for (int i = 0; i < RA; ++i) xa[i] = Xs[k][ty * RA + i];
+#pragma unroll
+            for (int j = 0; j < RB; ++j) yb[j] = Ys[k][tx * RB + j];
+#pragma unroll
+            for (int i = 0; i < RA; ++i)
+#pragma unroll
+                for (int j = 0; j < RB; ++j) acc[i][j] = opfma<T, HERM>(xa[i], yb[j], acc[i][j]);
+        }
+        __syncthreads();
+    }
+    T* P = part + (size_t)sl * a * b;
+#pragma unroll
+    for (int i = 0; i < RA; ++i)
+#pragma unroll
+        for (int j = 0; j < RB; ++j) {
+            const int gi = col_a0 + ty * RA + i, gj = col_b0 + tx * RB + j;
+            if (gi < a && gj < b) P[(size_t)gj * a + gi] = acc[i][j];
+        }
+}
+
+// G = sum over slices in order; if sym, mirror the upper triangle (op(G)^T = G for
+// the Hermitian case uses the conjugate).
+template <class T, bool HERM>
+__global__ void gram_reduce(const T* __restrict__ part, int slices, int a, int b, T* __restrict__ G, bool sym) {
+    const long tot = (long)a * b;
+    for (long e = blockIdx.x * (long)blockDim.x + threadIdx.x; e < tot; e += (long)gridDim.x * blockDim.x) {
+        const int i = (int)(e % a), j = (int)(e / a);
+        if (sym && (i / GT<T>::TA) > (j / GT<T>::TB)) {
+            // lower tile: mirror from the upper element (j, i)
+            T s = Sc<T>::zero();
+            for (int q = 0; q < slices; ++q) s = Sc<T>::add(s, part[(size_t)q * tot + (size_t)i * a + j]);
+            if constexpr (HERM) {
+                if constexpr (Sc<T>::W == 2) s = make_double2(((cplx&)s).x, -((cplx&)s).y);
+            }
+            G[e] = s;
+        } else {
+            T s = Sc<T>::zero();
+            for (int q = 0; q < slices; ++q) s = Sc<T>::add(s, part[(size_t)q * tot + e]);
+            G[e] = s;
+        }
+    }
+}
+
+// Z[n x b] = (sub ? Y : 0) -/+ X[n x a] M[a x b]; M column-major (ldm = a).
+// Block: 64 rows x TBc output columns; M chunk and X chunk in shared memory.
+template <class T, bool SUB>
+__global__ void __launch_bounds__(256) gemm_tall(const T* __restrict__ X, long ldx, int a, const T* __restrict__ M,
+                                                 int b, const T* __restrict__ Y, long ldy, T* __restrict__ Z, long ldz,
+                                                 long n, bool upper_tri) {
+    constexpr int TR = 64;                        // rows per block
+    constexpr int TC = Sc<T>::W == 1 ? 64 : 32;   // output cols per block
+    constexpr int KC = 16;
+    constexpr int RR = 4, RC = TC / 16;           // per-thread 4 rows x RC cols
+    __shared__ T Xs[KC][TR + 1];
+    __shared__ T Ms[KC][TC];
+    const long row0 = (long)blockIdx.y * TR;
+    const int col0 = blockIdx.x * TC;
+    const int tr = threadIdx.x % 16, tc = threadIdx.x / 16;  // 16 x 16
+    T acc[RR][RC];
+#pragma unroll
+    for (int i = 0; i < RR; ++i)
+#pragma unroll
+        for (int j = 0; j < RC; ++j) acc[i][j] = Sc<T>::zero();
+    const int kend = upper_tri ? min(a, col0 + TC) : a;  // M upper triangular: rows k > col are zero
+    for (int k0 = 0; k0 < kend; k0 += KC) {
+        // X chunk: TR rows x KC cols
+        for (int e = threadIdx.x; e < TR * KC; e += 256) {
+            const int r = e % TR, k = e / TR;
+            const long row = row0 + r;
+            Xs[k][r] = (row < n && k0 + k < a) ? X[(size_t)(k0 + k) * ldx + row] : Sc<T>::zero();
+        }
+        for (int e = threadIdx.x; e < KC * TC; e += 256) {
+            const int k = e % KC, c = e / KC;
+            Ms[k][c] = (k0 + k < a && col0 + c < b) ? M[(size_t)(col0 + c) * a + k0 + k] : Sc<T>::zero();
+        }
+        __syncthreads();
+#pragma unroll
+        for (int k = 0; k < KC; ++k) {
+            T xr[RR], mc[RC];
+#pragma unroll
+            for (int i = 0; i < RR; ++i) xr[i] = Xs[k][tr + 16 * i];
+#pragma unroll
+            for (int j = 0; j < RC; ++j) mc[j] = Ms[k][tc * RC + j];
+#pragma unroll
+            for (int i = 0; i < RR; ++i)
+#pragma unroll
+                for (int j = 0; j < RC; ++j) acc[i][j] = Sc<T>::fma(xr[i], mc[j], acc[i][j]);
+        }
+        __syncthreads();
+    }
+#pragma unroll
+    for (int i = 0; i < RR; ++i) {
+        const long row = row0 + tr + 16 * i;
+        if (row >= n) continue;
+#pragma unroll
+        for (int j = 0; j < RC; ++j) {
+            const int col = col0 + tc * RC + j;
+            if (col >= b) continue;
+            T v = acc[i][j];
+            if (SUB) v = Sc<T>::sub(Y[(size_t)col * ldy + row], v);
+            Z[(size_t)col * ldz + row] = v;
+        }
+    }
+}
+
+// ------------------------------------------------------------ small dense ---
+// In-place upper Cholesky of the r x r matrix G (column-major, ld r):
+// HERM: G = S^H S ; bilinear: G = S^T S (complex symmetric). Lower part zeroed.
+// info[0] = first non-positive / zero pivot index + 1 (0 = success);
+// info[1] = min |S_jj|, info[2] = max |S_jj| (doubles).
+template <class T> __device__ __forceinline__ T csqrt_(T v);
+template <> __device__ __forceinline__ double csqrt_<double>(double v) { return sqrt(v); }
+template <> __device__ __forceinline__ cplx csqrt_<cplx>(cplx v) {
+    const double m = sqrt(v.x * v.x + v.y * v.y);
+    double sr = sqrt(0.5 * (m + v.x));
+    double si = sqrt(fmax(0.0, 0.5 * (m - v.x)));
+    if (v.y < 0) si = -si;
+    return make_double2(sr, si);
+}
+template <class T> __device__ __forceinline__ T conj_(T v);
+template <> __device__ __forceinline__ double conj_<double>(double v) { return v; }
+template <> __device__ __forceinline__ cplx conj_<cplx>(cplx v) { return make_double2(v.x, -v.y); }
+
+template <class T, bool HERM>
+__global__ void __launch_bounds__(1024) chol_upper(T* G, int r, double* info) {
+    __shared__ T s_piv;
+    __shared__ int s_bad;
+    if (threadIdx.x == 0) {
+        s_bad = 0;
+        info[1] = 1e300;
+        info[2] = 0.0;
+    }
+    __syncthreads();
+    for (int j = 0; j < r; ++j) {
+        if (threadIdx.x == 0) {
+            T d = G[(size_t)j * r + j];
+            bool bad;
+            if (HERM || Sc<T>::W == 1) {
+                const double dr = Sc<T>::real(d);
+                bad = !(dr > 0.0);
+                d = Sc<T>::from(bad ? 1.0 : sqrt(dr));
+            } else {
+                d = csqrt_<T>(d);
+                bad = !(Sc<T>::abs2(d) > 0.0);
+                if (bad) d = Sc<T>::from(1.0);
+            }
+            if (bad && !s_bad) {
+                s_bad = j + 1;
+                info[0] = j + 1;
+            }
+            const double ad = sqrt(Sc<T>::abs2(d));
+            info[1] = fmin(info[1], ad);
+            info[2] = fmax(info[2], ad);
+            G[(size_t)j * r + j] = d;
+            s_piv = d;
+        }
+        __syncthreads();
+        const T piv = s_piv;
+        // row j of S: S[j][k] = G[j][k] / piv (k > j)
+        for (int k = j + 1 + threadIdx.x; k < r; k += blockDim.x)
+            G[(size_t)k * r + j] = Sc<T>::div(G[(size_t)k * r + j], piv);
+        __syncthreads();
+        // trailing update of the upper triangle: G[k][l] -= op(S[j][k]) S[j][l], j < k <= l
+        const int m = r - j - 1;
+        const long tot = (long)m * (m + 1) / 2;
+        for (long e = threadIdx.x; e < tot; e += blockDim.x) {
+            // map e -> (k, l) with k <= l over the trailing m x m upper triangle (column-wise)
+            int l = (int)((sqrt(8.0 * (double)e + 1.0) - 1.0) * 0.5);
+            while ((long)l * (l + 1) / 2 > e) --l;
+            while ((long)(l + 1) * (l + 2) / 2 <= e) ++l;
+            const int k = (int)(e - (long)l * (l + 1) / 2);
+            const int kk = j + 1 + k, ll = j + 1 + l;
+            const T sk = G[(size_t)kk * r + j], sl = G[(size_t)ll * r + j];
+            G[(size_t)ll * r + kk] = Sc<T>::sub(G[(size_t)ll * r + kk], HERM ? Sc<T>::cmul(sk, sl) : Sc<T>::mul(sk, sl));
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x == 0 && !s_bad) info[0] = 0;
+    for (long e = threadIdx.x; e < (long)r * r; e += blockDim.x) {
+        const int i = (int)(e % r), jj = (int)(e / r);
+        if (i > jj) G[e] = Sc<T>::zero();
+    }
+}
+
+// Sinv = S^-1 for upper-triangular S (r x r, ld r); column by column.
+template <class T>
+__global__ void __launch_bounds__(1024) tri_inv_upper(const T* S, T* Sinv, int r) {
+    for (long e = threadIdx.x; e < (long)r * r; e += blockDim.x) Sinv[e] = Sc<T>::zero();
+    __syncthreads();
+    for (int j = 0; j < r; ++j) {
+        const T djj = Sc<T>::div(Sc<T>::from(1.0), S[(size_t)j * r + j]);
+        // Sinv[i][j] = -(sum_{k=i}^{j-1} Sinv[i][k] S[k][j]) / S[j][j], i < j
+        for (int i = threadIdx.x; i < j; i += blockDim.x) {
+            T s = Sc<T>::zero();
+            for (int k = i; k < j; ++k) s = Sc<T>::fma(Sinv[(size_t)k * r + i], S[(size_t)j * r + k], s);
+            Sinv[(size_t)j * r + i] = Sc<T>::mul(Sc<T>::sub(Sc<T>::zero(), s), djj);
+        }
+        if (threadIdx.x == 0) Sinv[(size_t)j * r + j] = djj;
+        __syncthreads();
+    }
+}
+
+// C = A B for upper-triangular A, B (r x r; lda = ldb = ldc = ld), C upper.
+template <class T>
+__global__ void tri_mul_upper(const T* A, const T* B, T* C, int r, int ld) {
+    const long tot = (long)r * r;
+    for (long e = blockIdx.x * (long)blockDim.x + threadIdx.x; e < tot; e += (long)gridDim.x * blockDim.x) {
+        const int i = (int)(e % r), j = (int)(e / r);
+        T s = Sc<T>::zero();
+        if (i <= j)
+            for (int k = i; k <= j; ++k) s = Sc<T>::fma(A[(size_t)k * ld + i], B[(size_t)j * ld + k], s);
+        C[(size_t)j * ld + i] = s;
+    }
+}
+
+// Hermitian column norms^2 of X (n x c): out[j] = sum_i |X_ij|^2 (block partials -> last block)
+template <class T>
+__global__ void __launch_bounds__(256) col_norms(const T* __restrict__ X, long ldx, int c, long n, GridRed red,
+                                                 double* out) {
+    __shared__ double s_red[32];
+    extern __shared__ double s_vals[];
+    for (int j = 0; j < c; ++j) {
+        double h = 0.0;
+        const T* xc = X + (size_t)j * ldx;
+        for (long i = blockIdx.x * (long)blockDim.x + threadIdx.x; i < n; i += (long)gridDim.x * blockDim.x)
+            h += Sc<T>::abs2(xc[i]);
+        const double s = block_sum(h, s_red);
+        if (threadIdx.x == 0) s_vals[j] = s;
+    }
+    __syncthreads();
+    if (!grid_commit(red, s_vals, c)) return;
+    grid_finish(red, c, out);
+}
+
+}  // namespace rd

@@ -21,14 +21,20 @@
 namespace rd {
 
 // ----------------------------------------------------------- operator ---
+// Coefficients are assembled once per system (op_prepare) into four node
+// fields: F[0] diag (sum of face coefficients + h^2 mu_a), F[1..3] the face
+// coefficient toward the +x / +y / +z neighbour (harmonic mean of the two node
+// D values; 0 where the neighbour is outside the grid). The apply is then
+// division-free:  y_p = (diag_p + i shift) x_p - sum_faces F_face x_q.
 struct OpDev {
     int d;
     int N0, N1, N2;
     long n;
     double robin_face;  // Dbg / (1 + rho)
     double shift;       // h^2 omega/nu (imaginary diagonal)
-    const double* D;
+    const double* D;    // node fields (input)
     const double* mu;
+    const double* F;    // assembled [4][n]: diag, fx, fy, fz
 };
 
 __device__ __forceinline__ double hmean(double a, double b) { return 2.0 * (a * b) / (a + b); }
@@ -44,85 +50,95 @@ template <> __device__ __forceinline__ cplx axpy_real<cplx>(double a, cplx x, cp
     return make_double2(acc.x + a * x.x, acc.y + a * x.y);
 }
 
-// Row p of A x. Face order (axis 0 -, +, axis 1 -, +, axis 2 -, +) matches the
-// oracle (the CPU checker under oracle/, GridOp::apply_one).
-template <class T>
-__device__ __forceinline__ T stencil_row(const OpDev& op, const T* __restrict__ x, long p, int i, int j, int k) {
-    const double* __restrict__ D = op.D;
-    const double Dp = __ldg(D + p);
-    double diag = 0.0;
-    T acc = Sc<T>::zero();
-    // axis 0 (lateral, Dirichlet ghosts)
-    if (i > 0) {
-        const double f = hmean(Dp, __ldg(D + p - 1));
-        diag += f;
-        acc = axpy_real(f, x[p - 1], acc);
-    } else {
-        diag += Dp;
-    }
-    if (i < op.N0 - 1) {
-        const double f = hmean(Dp, __ldg(D + p + 1));
-        diag += f;
-        acc = axpy_real(f, x[p + 1], acc);
-    } else {
-        diag += Dp;
-    }
-    // axis 1
-    const long s1 = op.N0;
+// Assemble the per-system coefficient fields. Face order of the diagonal sum
+// (axis 0 -, +, axis 1 -, +, axis 2 -, +) matches the CPU checker.
+__global__ void __launch_bounds__(256) op_prepare(OpDev op, double* __restrict__ F) {
+    const int i = blockIdx.x * 32 + (threadIdx.x & 31);
+    const int j = blockIdx.y * 8 + (threadIdx.x >> 5);
+    const int k = blockIdx.z;
+    if (i >= op.N0 || j >= op.N1) return;
+    const long s1 = op.N0, s2 = (long)op.N0 * op.N1;
+    const long p = i + s1 * j + s2 * k;
+    const double* D = op.D;
+    const double Dp = D[p];
     const bool robin1 = (op.d == 2);
-    if (j > 0) {
-        const double f = hmean(Dp, __ldg(D + p - s1));
-        diag += f;
-        acc = axpy_real(f, x[p - s1], acc);
+    double diag = 0.0, fx = 0.0, fy = 0.0, fz = 0.0;
+    diag += (i > 0) ? hmean(Dp, D[p - 1]) : Dp;
+    if (i < op.N0 - 1) {
+        fx = hmean(Dp, D[p + 1]);
+        diag += fx;
     } else {
-        diag += robin1 ? op.robin_face : Dp;
+        diag += Dp;
     }
+    diag += (j > 0) ? hmean(Dp, D[p - s1]) : (robin1 ? op.robin_face : Dp);
     if (j < op.N1 - 1) {
-        const double f = hmean(Dp, __ldg(D + p + s1));
-        diag += f;
-        acc = axpy_real(f, x[p + s1], acc);
+        fy = hmean(Dp, D[p + s1]);
+        diag += fy;
     } else {
         diag += robin1 ? op.robin_face : Dp;
     }
     if (op.d == 3) {
-        const long s2 = (long)op.N0 * op.N1;
-        if (k > 0) {
-            const double f = hmean(Dp, __ldg(D + p - s2));
-            diag += f;
-            acc = axpy_real(f, x[p - s2], acc);
-        } else {
-            diag += op.robin_face;
-        }
+        diag += (k > 0) ? hmean(Dp, D[p - s2]) : op.robin_face;
         if (k < op.N2 - 1) {
-            const double f = hmean(Dp, __ldg(D + p + s2));
-            diag += f;
-            acc = axpy_real(f, x[p + s2], acc);
+            fz = hmean(Dp, D[p + s2]);
+            diag += fz;
         } else {
             diag += op.robin_face;
         }
     }
-    return Sc<T>::sub(diag_apply<T>(diag + __ldg(op.mu + p), op.shift, x[p]), acc);
+    F[p] = diag + op.mu[p];
+    F[op.n + p] = fx;
+    F[2 * op.n + p] = fy;
+    F[3 * op.n + p] = fz;
+}
+
+// Row p of A x from the assembled fields (same face order as the checker).
+template <class T>
+__device__ __forceinline__ T stencil_row(const OpDev& op, const T* __restrict__ x, long p, int i, int j, int k) {
+    const double* __restrict__ F = op.F;
+    const long n = op.n;
+    const long s1 = op.N0, s2 = (long)op.N0 * op.N1;
+    T acc = Sc<T>::zero();
+    if (i > 0) acc = axpy_real(__ldg(F + n + p - 1), x[p - 1], acc);
+    if (i < op.N0 - 1) acc = axpy_real(__ldg(F + n + p), x[p + 1], acc);
+    if (j > 0) acc = axpy_real(__ldg(F + 2 * n + p - s1), x[p - s1], acc);
+    if (j < op.N1 - 1) acc = axpy_real(__ldg(F + 2 * n + p), x[p + s1], acc);
+    if (op.d == 3) {
+        if (k > 0) acc = axpy_real(__ldg(F + 3 * n + p - s2), x[p - s2], acc);
+        if (k < op.N2 - 1) acc = axpy_real(__ldg(F + 3 * n + p), x[p + s2], acc);
+    }
+    return Sc<T>::sub(diag_apply<T>(__ldg(F + p), op.shift, x[p]), acc);
+}
+
+// 3D launch: block 32 x 8 threads covers an (i, j) tile, blockIdx.z = k.
+__device__ __forceinline__ bool node_of_block(const OpDev& op, int& i, int& j, int& k, long& p) {
+    i = blockIdx.x * 32 + (threadIdx.x & 31);
+    j = blockIdx.y * 8 + (threadIdx.x >> 5);
+    k = blockIdx.z;
+    p = i + (long)op.N0 * (j + (long)op.N1 * k);
+    return i < op.N0 && j < op.N1;
 }
 
 __device__ __forceinline__ void node_coords(const OpDev& op, long p, int& i, int& j, int& k) {
-    i = (int)(p % op.N0);
-    const long q = p / op.N0;
-    j = (int)(q % op.N1);
-    k = (int)(q / op.N1);
+    const int pi = (int)p;
+    i = pi % op.N0;
+    const int q = pi / op.N0;
+    j = q % op.N1;
+    k = q / op.N1;
 }
 
-// y[:, c] = A x[:, xcol ? xcol[c] : c]  (blockIdx.y = column)
+// y[:, c] = A x[:, xcol ? xcol[c] : c] for c < ncols; grid.z = N2 * ncols.
 template <class T>
 __global__ void __launch_bounds__(256) stencil_kernel(OpDev op, const T* __restrict__ x, long ldx,
                                                       const int* __restrict__ xcol, T* __restrict__ y, long ldy) {
-    const int c = blockIdx.y;
+    const int c = blockIdx.z / op.N2;
+    const int i = blockIdx.x * 32 + (threadIdx.x & 31);
+    const int j = blockIdx.y * 8 + (threadIdx.x >> 5);
+    const int k = blockIdx.z - c * op.N2;
+    if (i >= op.N0 || j >= op.N1) return;
+    const long p = i + (long)op.N0 * (j + (long)op.N1 * k);
     const T* xc = x + (size_t)(xcol ? xcol[c] : c) * ldx;
-    T* yc = y + (size_t)c * ldy;
-    for (long p = blockIdx.x * (long)blockDim.x + threadIdx.x; p < op.n; p += (long)gridDim.x * blockDim.x) {
-        int i, j, k;
-        node_coords(op, p, i, j, k);
-        yc[p] = stencil_row<T>(op, xc, p, i, j, k);
-    }
+    y[(size_t)c * ldy + p] = stencil_row<T>(op, xc, p, i, j, k);
 }
 
 // ------------------------------------------------------------ CG state ---
@@ -151,9 +167,9 @@ __global__ void __launch_bounds__(256) cg_stencil_dots(OpDev op, const T* __rest
     constexpr int W = Sc<T>::W;
     T g = Sc<T>::zero(), dl = Sc<T>::zero();
     double h = 0.0;
-    for (long p = blockIdx.x * (long)blockDim.x + threadIdx.x; p < op.n; p += (long)gridDim.x * blockDim.x) {
-        int i, j, k;
-        node_coords(op, p, i, j, k);
+    int i, j, k;
+    long p;
+    if (node_of_block(op, i, j, k, p)) {
         const T wp = stencil_row<T>(op, r, p, i, j, k);
         w[p] = wp;
         const T rp = r[p];
@@ -275,30 +291,46 @@ __device__ __forceinline__ void ts_finish_cols(T (&acc)[CPW], int c, int col0, G
     grid_finish(red, nv, out + (size_t)col0 * W);
 }
 
+// Rows per lane per step: enough independent loads in flight per lane
+// (CPW columns x U rows) to cover HBM latency.
+template <class T, int CPW> struct TSU {
+    static constexpr int LOADS = Sc<T>::W == 1 ? 16 : 8;
+    static constexpr int U = CPW >= LOADS ? 1 : (LOADS / CPW > 8 ? 8 : LOADS / CPW);
+};
+
 // out[col0 + j] = sum_i op(K[i, col0 + j]) x[i], j < c (c <= 8*CPW)
 template <class T, bool HERM, int CPW>
 __global__ void __launch_bounds__(TS_THREADS) ts_T(const T* __restrict__ K, long ldk, int c, int col0,
                                                    const T* __restrict__ x, long n, GridRed red, double* out,
                                                    const CGState* st) {
     if (st && st->done) return;
+    constexpr int U = TSU<T, CPW>::U;
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const int j0 = wid * CPW;
     T acc[CPW];
 #pragma unroll
     for (int jj = 0; jj < CPW; ++jj) acc[jj] = Sc<T>::zero();
-    const long ntiles = (n + 31) >> 5;
-    const T* Kc = K + (size_t)col0 * ldk;
-    for (long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-        const long row = (tile << 5) + lane;
-        if (row < n) {
-            const T xv = x[row];
-            T kv[CPW];
+    const long nsteps = (n + 32 * U - 1) / (32 * U);
+    const T* Kc = K + (size_t)(col0 + j0) * ldk;
+    int ncol = c - j0;
+    if (ncol > CPW) ncol = CPW;
+    for (long stp = blockIdx.x; stp < nsteps; stp += gridDim.x) {
+        const long base = stp * 32 * U + lane;
+        T xv[U];
+        T kv[U][CPW];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const long row = base + 32 * u;
+            const bool ok = row < n;
+            xv[u] = ok ? x[row] : Sc<T>::zero();
 #pragma unroll
             for (int jj = 0; jj < CPW; ++jj)
-                kv[jj] = (j0 + jj < c) ? Kc[(size_t)(j0 + jj) * ldk + row] : Sc<T>::zero();
-#pragma unroll
-            for (int jj = 0; jj < CPW; ++jj) acc[jj] = opfma<T, HERM>(kv[jj], xv, acc[jj]);
+                kv[u][jj] = (ok && jj < ncol) ? Kc[(size_t)jj * ldk + row] : Sc<T>::zero();
         }
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+#pragma unroll
+            for (int jj = 0; jj < CPW; ++jj) acc[jj] = opfma<T, HERM>(kv[u][jj], xv[u], acc[jj]);
     }
     ts_finish_cols<T, HERM, CPW>(acc, c, col0, red, out, nullptr);
 }
@@ -311,36 +343,52 @@ __global__ void __launch_bounds__(TS_THREADS) ts_NT(const T* __restrict__ K, lon
                                                     const CGState* st) {
     if (st && st->done) return;
     constexpr int W = Sc<T>::W;
+    constexpr int U = TSU<T, CPW>::U;
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const int j0 = wid * CPW;
-    __shared__ T s_part[TS_WARPS][32];
+    __shared__ T s_part[TS_WARPS][32 * U];
+    int ncol = c - j0;
+    if (ncol > CPW) ncol = CPW;
     T cw[CPW];
 #pragma unroll
-    for (int jj = 0; jj < CPW; ++jj) cw[jj] = (j0 + jj < c) ? Sc<T>::get(cin + (size_t)(j0 + jj) * W) : Sc<T>::zero();
+    for (int jj = 0; jj < CPW; ++jj) cw[jj] = (jj < ncol) ? Sc<T>::get(cin + (size_t)(j0 + jj) * W) : Sc<T>::zero();
     T acc[CPW];
 #pragma unroll
     for (int jj = 0; jj < CPW; ++jj) acc[jj] = Sc<T>::zero();
-    const long ntiles = (n + 31) >> 5;
-    for (long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-        const long row = (tile << 5) + lane;
-        const bool ok = row < n;
-        T xv = ok ? x[row] : Sc<T>::zero();  // read before the barrier: xo may alias x
-        T kv[CPW];
-        T part = Sc<T>::zero();
+    const long nsteps = (n + 32 * U - 1) / (32 * U);
+    const T* Kc = K + (size_t)j0 * ldk;
+    for (long stp = blockIdx.x; stp < nsteps; stp += gridDim.x) {
+        const long base = stp * 32 * U + lane;
+        T xv[U];
+        T kv[U][CPW];
 #pragma unroll
-        for (int jj = 0; jj < CPW; ++jj) {
-            kv[jj] = (ok && j0 + jj < c) ? K[(size_t)(j0 + jj) * ldk + row] : Sc<T>::zero();
-            part = Sc<T>::fma(kv[jj], cw[jj], part);
+        for (int u = 0; u < U; ++u) {
+            const long row = base + 32 * u;
+            const bool ok = row < n;
+            xv[u] = ok ? x[row] : Sc<T>::zero();  // read before the barrier: xo may alias x
+#pragma unroll
+            for (int jj = 0; jj < CPW; ++jj)
+                kv[u][jj] = (ok && jj < ncol) ? Kc[(size_t)jj * ldk + row] : Sc<T>::zero();
         }
-        s_part[wid][lane] = part;
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            T part = Sc<T>::zero();
+#pragma unroll
+            for (int jj = 0; jj < CPW; ++jj) part = Sc<T>::fma(kv[u][jj], cw[jj], part);
+            s_part[wid][32 * u + lane] = part;
+        }
         __syncthreads();
-        T sum = s_part[0][lane];
 #pragma unroll
-        for (int w2 = 1; w2 < TS_WARPS; ++w2) sum = Sc<T>::add(sum, s_part[w2][lane]);
-        xv = Sc<T>::sub(xv, sum);
-        if (wid == 0 && ok) xo[row] = xv;
+        for (int u = 0; u < U; ++u) {
+            T sum = s_part[0][32 * u + lane];
 #pragma unroll
-        for (int jj = 0; jj < CPW; ++jj) acc[jj] = opfma<T, HERM>(kv[jj], xv, acc[jj]);
+            for (int w2 = 1; w2 < TS_WARPS; ++w2) sum = Sc<T>::add(sum, s_part[w2][32 * u + lane]);
+            const T xn = Sc<T>::sub(xv[u], sum);
+            const long row = base + 32 * u;
+            if (wid == 0 && row < n) xo[row] = xn;
+#pragma unroll
+            for (int jj = 0; jj < CPW; ++jj) acc[jj] = opfma<T, HERM>(kv[u][jj], xn, acc[jj]);
+        }
         __syncthreads();
     }
     ts_finish_cols<T, HERM, CPW>(acc, c, 0, red, out, nullptr);
@@ -489,6 +537,67 @@ __global__ void row_gather(const T* __restrict__ K, long ldk, int c, long idx, d
 // out = a - b (device double arrays), or out = a + b
 __global__ void dvec_addsub(int m, const double* a, const double* b, double sgn, double* out) {
     for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < m; t += gridDim.x * blockDim.x) out[t] = a[t] + sgn * b[t];
+}
+
+// Seeded N(0,1) vector: splitmix64(seed, i) -> two uniforms -> Box-Muller.
+__device__ __forceinline__ uint64_t splitmix64(uint64_t z) {
+    z += 0x9e3779b97f4a7c15ull;
+    z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
+    z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
+    return z ^ (z >> 31);
+}
+__global__ void vec_randn(double* x, long n, uint64_t seed) {
+    for (long i = blockIdx.x * (long)blockDim.x + threadIdx.x; i < n; i += (long)gridDim.x * blockDim.x) {
+        const uint64_t a = splitmix64(seed ^ (2 * (uint64_t)i)), b = splitmix64(seed ^ (2 * (uint64_t)i + 1));
+        const double u1 = ((a >> 11) + 1.0) * 0x1.0p-53, u2 = ((b >> 11) + 1.0) * 0x1.0p-53;
+        x[i] = sqrt(-2.0 * log(u1)) * cospi(2.0 * u2);
+    }
+}
+
+// Gershgorin bound max_p (|diag| + |shift| + sum |offdiag|) (krylov.cpp:190-195)
+__global__ void __launch_bounds__(256) op_gershgorin(OpDev op, GridRed red, double* out) {
+    double m = 0.0;
+    for (long p = blockIdx.x * (long)blockDim.x + threadIdx.x; p < op.n; p += (long)gridDim.x * blockDim.x) {
+        int i, j, k;
+        node_coords(op, p, i, j, k);
+        // A applied to e_p gives column p = row p (symmetric); recompute the row sums directly
+        const double Dp = op.D[p];
+        double diag = op.mu[p], off = 0.0;
+        const int idx[3] = {i, j, k};
+        const int len[3] = {op.N0, op.N1, op.N2};
+        const long st[3] = {1, op.N0, (long)op.N0 * op.N1};
+        for (int ax = 0; ax < op.d; ++ax)
+            for (int dir = -1; dir <= 1; dir += 2) {
+                const int q = idx[ax] + dir;
+                if (q >= 0 && q < len[ax]) {
+                    const double f = hmean(Dp, op.D[p + dir * st[ax]]);
+                    diag += f;
+                    off += f;
+                } else {
+                    diag += (ax == op.d - 1) ? op.robin_face : Dp;
+                }
+            }
+        m = fmax(m, fabs(diag) + fabs(op.shift) + off);
+    }
+    __shared__ double s_m[32];
+    __shared__ double s_v[1];
+    for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if ((threadIdx.x & 31) == 0) s_m[threadIdx.x >> 5] = m;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double b = 0.0;
+        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) b = fmax(b, s_m[w]);
+        s_v[0] = b;
+    }
+    __syncthreads();
+    if (!grid_commit(red, s_v, 1)) return;
+    __threadfence();
+    if (threadIdx.x == 0) {
+        double b = 0.0;
+        for (unsigned q = 0; q < gridDim.x * gridDim.y; ++q) b = fmax(b, __ldcg(red.partials + q));
+        out[0] = b;
+        *red.counter = 0u;
+    }
 }
 
 }  // namespace rd

@@ -77,12 +77,61 @@ struct Ctx {
     long launches = 0;
     int hist_cap = 1 << 16;
 
+    // Sampled per-kernel-class device timing (CUDA events on this stream):
+    // the first inner iteration of every launch batch is bracketed.
+    struct ProfClass {
+        double ms = 0.0, bytes = 0.0;
+        long samples = 0;
+    };
+    struct Pending {
+        int cls;
+        double bytes;
+        long iter;
+        cudaEvent_t a, b;
+    };
+    bool prof = false;
+    ProfClass pc[8];
+    std::vector<cudaEvent_t> evpool;
+    size_t evnext = 0;
+    std::vector<Pending> pend;
+    cudaEvent_t next_event() {
+        if (evnext == evpool.size()) {
+            cudaEvent_t e;
+            CK(cudaEventCreate(&e));
+            evpool.push_back(e);
+        }
+        return evpool[evnext++];
+    }
+    cudaEvent_t prof_start() {
+        cudaEvent_t a = next_event();
+        CK(cudaEventRecord(a, s));
+        return a;
+    }
+    void prof_stop(cudaEvent_t a, int cls, double bytes, long iter) {
+        cudaEvent_t b = next_event();
+        CK(cudaEventRecord(b, s));
+        pend.push_back(Pending{cls, bytes, iter, a, b});
+    }
+    // after a sync: keep samples of iterations that really executed
+    void prof_flush(long executed) {
+        for (auto& q : pend) {
+            if (q.iter >= executed) continue;
+            float ms = 0.f;
+            CK(cudaEventElapsedTime(&ms, q.a, q.b));
+            pc[q.cls].ms += ms;
+            pc[q.cls].bytes += q.bytes;
+            pc[q.cls].samples += 1;
+        }
+        pend.clear();
+        evnext = 0;
+    }
+
     void init(int dev) {
         device = dev;
         CK(cudaSetDevice(dev));
         CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
         CK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
-        partials.ensure(sizeof(double) * 4096 * 64);
+        partials.ensure(sizeof(double) * 1024 * 1024);
         counter.ensure(sizeof(unsigned) * 16);
         CK(cudaMemset(counter.p, 0, counter.bytes));
         scal.ensure(sizeof(double) * 64 * 1024);
@@ -94,6 +143,7 @@ struct Ctx {
     }
     ~Ctx() {
         if (s) cudaStreamSynchronize(s);
+        for (auto& e : evpool) cudaEventDestroy(e);
         if (st_host) cudaFreeHost(st_host);
         for (auto& e : ev)
             if (e) cudaEventDestroy(e);
@@ -119,28 +169,32 @@ struct Ctx {
 struct DevOp {
     Ctx* ctx = nullptr;
     OpDev d{};
-    DevBuf D, mu;
+    DevBuf D, mu, F;
     bool have_fields = false;
     double lam_max = 0.0;
     long n() const { return d.n; }
 };
 
 // ------------------------------------------------------ launch helpers ---
+inline dim3 stencil_grid(const OpDev& op, long zmult) {
+    return dim3((unsigned)((op.N0 + 31) / 32), (unsigned)((op.N1 + 7) / 8), (unsigned)(op.N2 * zmult));
+}
+
 template <class T> void launch_stencil(Ctx& c, const OpDev& op, const T* x, long ldx, const int* xcol, T* y,
                                        long ldy, long ncols) {
     if (ncols <= 0) return;
-    for (long c0 = 0; c0 < ncols; c0 += 65535) {
-        const int nc = (int)std::min(65535L, ncols - c0);
-        dim3 grid(c.grid_for(op.n, 256, 8), nc);
-        stencil_kernel<T><<<grid, 256, 0, c.s>>>(op, xcol ? x : x + (size_t)c0 * ldx, ldx, xcol ? xcol + c0 : nullptr,
-                                                 y + (size_t)c0 * ldy, ldy);
+    const long maxc = std::max(1L, 65535L / op.N2);
+    for (long c0 = 0; c0 < ncols; c0 += maxc) {
+        const long nc = std::min(maxc, ncols - c0);
+        stencil_kernel<T><<<stencil_grid(op, nc), 256, 0, c.s>>>(op, xcol ? x : x + (size_t)c0 * ldx, ldx,
+                                                                  xcol ? xcol + c0 : nullptr, y + (size_t)c0 * ldy, ldy);
         c.check_launch();
     }
 }
 
 template <class T, bool HERM, int CPW>
 void ts_T_inst(Ctx& c, const T* K, long ldk, int cc, int col0, const T* x, long n, double* out, const CGState* st) {
-    const long ntiles = (n + 31) / 32;
+    const long ntiles = (n + 32 * TSU<T, CPW>::U - 1) / (32 * TSU<T, CPW>::U);
     const int grid = (int)std::max(1L, std::min<long>(ntiles, (long)c.sms * 2));
     ts_T<T, HERM, CPW><<<grid, TS_THREADS, 0, c.s>>>(K, ldk, cc, col0, x, n, c.red(), out, st);
     c.check_launch();
@@ -168,7 +222,7 @@ void ts_T_launch(Ctx& c, const T* K, long ldk, long ncol, const T* x, long n, do
 template <class T, bool HERM, int CPW>
 void ts_NT_inst(Ctx& c, const T* K, long ldk, int cc, const T* x, T* xo, long n, const double* cin, double* out,
                 const CGState* st) {
-    const long ntiles = (n + 31) / 32;
+    const long ntiles = (n + 32 * TSU<T, CPW>::U - 1) / (32 * TSU<T, CPW>::U);
     const int grid = (int)std::max(1L, std::min<long>(ntiles, (long)c.sms * 2));
     ts_NT<T, HERM, CPW><<<grid, TS_THREADS, 0, c.s>>>(K, ldk, cc, x, xo, n, cin, c.red(), out, st);
     c.check_launch();
@@ -248,6 +302,93 @@ void cgs2(Ctx& c, const T* Q, long ldq, long t, const T* z, T* q, long n, double
     launch_addsub(c, (int)(t * W), tmp1, tmp2, 1.0, coef);
 }
 
+
+// ------------------------------------------------------- block helpers ---
+// G (a x b, device, ld a) = op(X)^T Y over n rows. sym: X == Y, upper tiles only.
+template <class T, bool HERM>
+void gram(Ctx& c, const T* X, long ldx, long a, const T* Y, long ldy, long b, long n, T* G, bool sym, DevBuf& work) {
+    if (a == 0 || b == 0) return;
+    const long ta = (a + GT<T>::TA - 1) / GT<T>::TA, tb = (b + GT<T>::TB - 1) / GT<T>::TB;
+    const long tiles = sym ? ta * (ta + 1) / 2 : ta * tb;
+    long slices = std::max(1L, std::min<long>((4L * c.sms + tiles - 1) / tiles, (n + 4095) / 4096));
+    slices = std::min(slices, 1024L);
+    long rps = (n + slices - 1) / slices;
+    rps = (rps + GT<T>::KC - 1) / GT<T>::KC * GT<T>::KC;
+    slices = (n + rps - 1) / rps;
+    work.ensure(sizeof(T) * slices * a * b);
+    dim3 grid((unsigned)ta, (unsigned)tb, (unsigned)slices);
+    gram_kernel<T, HERM><<<grid, 256, 0, c.s>>>(X, ldx, (int)a, Y, ldy, (int)b, n, rps, work.template as<T>(), sym);
+    c.check_launch();
+    gram_reduce<T, HERM><<<c.grid_for(a * b, 256, 4), 256, 0, c.s>>>(work.template as<T>(), (int)slices, (int)a,
+                                                                      (int)b, G, sym);
+    c.check_launch();
+}
+
+// Z = X M (SUB=false) or Z = Y - X M (SUB=true); M is a x b on the device (ld a).
+template <class T, bool SUB>
+void gemm(Ctx& c, const T* X, long ldx, long a, const T* M, long b, const T* Y, long ldy, T* Z, long ldz, long n,
+          bool upper) {
+    if (b == 0 || n == 0) return;
+    if (a == 0) {
+        if (SUB && Z != Y)
+            for (long j = 0; j < b; ++j)
+                CK(cudaMemcpyAsync(Z + j * ldz, Y + j * ldy, sizeof(T) * n, cudaMemcpyDeviceToDevice, c.s));
+        return;
+    }
+    constexpr int TC = Sc<T>::W == 1 ? 64 : 32;
+    const long rt = (n + 63) / 64;
+    for (long r0 = 0; r0 < rt; r0 += 65535) {
+        const long nr = std::min(65535L, rt - r0);
+        const long off = r0 * 64;
+        dim3 grid((unsigned)((b + TC - 1) / TC), (unsigned)nr);
+        gemm_tall<T, SUB><<<grid, 256, 0, c.s>>>(X + off, ldx, (int)a, M, (int)b, SUB ? Y + off : nullptr, ldy,
+                                                  Z + off, ldz, std::min(n - off, nr * 64), upper);
+        c.check_launch();
+    }
+}
+
+// In-place upper Cholesky (HERM: S^H S, else S^T S) + inverse; returns the
+// pivot diagnostics and the 1-norm condition estimate of S.
+struct CholInfo {
+    int bad = 0;
+    double kappa1 = 0.0;
+};
+template <class T, bool HERM> CholInfo chol_inv(Ctx& c, T* G, T* Sinv, long r, bool want_kappa) {
+    CholInfo ci;
+    if (r == 0) return ci;
+    double* info = c.sc(7) + 32;
+    chol_upper<T, HERM><<<1, 1024, 0, c.s>>>(G, (int)r, info);
+    c.check_launch();
+    tri_inv_upper<T><<<1, 1024, 0, c.s>>>(G, Sinv, (int)r);
+    c.check_launch();
+    double hi[3];
+    CK(cudaMemcpyAsync(hi, info, sizeof(hi), cudaMemcpyDeviceToHost, c.s));
+    std::vector<T> S, Si;
+    if (want_kappa) {
+        S.resize(r * r);
+        Si.resize(r * r);
+        CK(cudaMemcpyAsync(S.data(), G, sizeof(T) * r * r, cudaMemcpyDeviceToHost, c.s));
+        CK(cudaMemcpyAsync(Si.data(), Sinv, sizeof(T) * r * r, cudaMemcpyDeviceToHost, c.s));
+    }
+    c.sync();
+    ci.bad = (int)hi[0];
+    if (want_kappa) {
+        double n1 = 0.0, n2 = 0.0;
+        for (long j = 0; j < r; ++j) {
+            double a = 0.0, b = 0.0;
+            for (long i = 0; i <= j; ++i) {
+                a += std::sqrt(Sc<T>::abs2(S[i + j * r]));
+                b += std::sqrt(Sc<T>::abs2(Si[i + j * r]));
+            }
+            n1 = std::max(n1, a);
+            n2 = std::max(n2, b);
+        }
+        ci.kappa1 = n1 * n2;
+        if (!std::isfinite(ci.kappa1)) ci.bad = ci.bad ? ci.bad : 1;
+    }
+    return ci;
+}
+
 // ---------------------------------------------------------- CG driver ---
 struct SolveOut {
     int iterations = 0;
@@ -317,20 +458,33 @@ SolveOut recycled_cg(Ctx& c, DevOp& op, const T* U, const T* K, long ncol, const
     CK(cudaMemcpyAsync(st, &c.st_host[0], sizeof(CGState), cudaMemcpyHostToDevice, c.s));
     CK(cudaStreamSynchronize(c.s));  // st_host slot reused below
 
-    const int grid_st = c.grid_for(n, 256, 2);
+    const dim3 grid_st = stencil_grid(op.d, 1);
     const size_t smem_c = sizeof(double) * W * std::max(1L, ncol);
     const int batch = n < 200000 ? 16 : 8;
+    long batches = 0;
+    const double es = sizeof(T);
     auto launch_batch = [&]() {
         for (int b = 0; b < batch; ++b) {
+            const bool samp = c.prof && b == 0;
+            const long iter = batches * batch;
+            cudaEvent_t e0 = samp ? c.prof_start() : nullptr;
             cg_stencil_dots<T><<<grid_st, 256, 0, c.s>>>(op.d, r, w, st, c.hist.template as<double>(), c.red());
             c.check_launch();
+            if (samp) c.prof_stop(e0, 0, n * (2 * es + 16.0), iter);
             if (ncol > 0) {
+                cudaEvent_t e1 = samp ? c.prof_start() : nullptr;
                 ts_T_launch<T, false>(c, K, n, ncol, w, n, c1, st);
+                if (samp) c.prof_stop(e1, 1, n * es * (ncol + 1.0), iter);
+                cudaEvent_t e2 = samp ? c.prof_start() : nullptr;
                 ts_NT_launch<T, false>(c, K, n, ncol, w, w, n, c1, c2, st);
+                if (samp) c.prof_stop(e2, 2, n * es * (ncol + 2.0), iter);
             }
+            cudaEvent_t e3 = samp ? c.prof_start() : nullptr;
             cg_update<T><<<c.grid_for(n, 256, 8), 256, smem_c, c.s>>>(K, n, (int)ncol, w, n, c2, r, p, s, y, st);
             c.check_launch();
+            if (samp) c.prof_stop(e3, 3, n * es * (ncol + 9.0), iter);
         }
+        ++batches;
     };
     // two batches in flight; poll the done flag of the older one
     int slot = 0;
@@ -353,6 +507,7 @@ SolveOut recycled_cg(Ctx& c, DevOp& op, const T* U, const T* K, long ncol, const
     CK(cudaMemcpyAsync(&c.st_host[0], st, sizeof(CGState), cudaMemcpyDeviceToHost, c.s));
     c.sync();
     const CGState fin = c.st_host[0];
+    if (c.prof) c.prof_flush(fin.it);
     SolveOut out;
     out.iterations = fin.it;
     out.converged = fin.converged != 0;
@@ -400,6 +555,191 @@ void from_raw(Ctx& c, long n, long ncol, const T* Wbase, const int* wcol_host, c
     (void)W;
 }
 
+
+// ------------------------------------------------------------ eigen seed ---
+// Small symmetric eigenproblem of the Lanczos tridiagonal (host, m <= a few
+// hundred; the reference uses SelfAdjointEigenSolver on T, krylov.cpp:214-221).
+static void jacobi_eig(long m, std::vector<double>& T, std::vector<double>& Z) {
+    Z.assign((size_t)m * m, 0.0);
+    for (long i = 0; i < m; ++i) Z[i + i * m] = 1.0;
+    auto at = [&](long i, long j) -> double& { return T[i + j * m]; };
+    for (int sweep = 0; sweep < 100; ++sweep) {
+        double off = 0.0, tot = 0.0;
+        for (long p = 0; p < m; ++p)
+            for (long q = 0; q < m; ++q) {
+                tot += at(p, q) * at(p, q);
+                if (p != q) off += at(p, q) * at(p, q);
+            }
+        if (off <= 1e-30 * tot || off < 1e-300) break;
+        for (long p = 0; p < m; ++p)
+            for (long q = p + 1; q < m; ++q) {
+                const double apq = at(p, q);
+                if (std::fabs(apq) < 1e-300) continue;
+                const double th = (at(q, q) - at(p, p)) / (2.0 * apq);
+                const double t = (th >= 0 ? 1.0 : -1.0) / (std::fabs(th) + std::sqrt(th * th + 1.0));
+                const double cs = 1.0 / std::sqrt(t * t + 1.0), sn = t * cs;
+                for (long r = 0; r < m; ++r) {
+                    const double a = at(r, p), b = at(r, q);
+                    at(r, p) = cs * a - sn * b;
+                    at(r, q) = sn * a + cs * b;
+                }
+                for (long r = 0; r < m; ++r) {
+                    const double a = at(p, r), b = at(q, r);
+                    at(p, r) = cs * a - sn * b;
+                    at(q, r) = sn * a + cs * b;
+                }
+                for (long r = 0; r < m; ++r) {
+                    const double a = Z[r + p * m], b = Z[r + q * m];
+                    Z[r + p * m] = cs * a - sn * b;
+                    Z[r + q * m] = sn * a + cs * b;
+                }
+            }
+    }
+}
+
+// smallest_eigenpairs (krylov.cpp:181-280) on the device: shift-invert
+// Lanczos on A^-1 with full two-pass reorthogonalisation; A^-1 v by plain CG
+// to 1e-12 (no sparse factorisation on the GPU). Ritz check every max(k,10)
+// steps against tol * lambda_max (Gershgorin).
+static void smallest_eigenpairs_dev(Ctx& c, DevOp& op, long k, double tol, std::vector<double>& lam, double* Uout,
+                                    double inner_tol = 1e-12) {
+    const long n = op.n();
+    if (k < 1 || k > n) throw ConfigError("eigensolver: k out of range");
+    if (!(op.lam_max > 0.0)) {
+        op_gershgorin<<<c.grid_for(n, 256, 2), 256, 0, c.s>>>(op.d, c.red(), c.sc(3));
+        c.check_launch();
+        CK(cudaMemcpyAsync(&op.lam_max, c.sc(3), sizeof(double), cudaMemcpyDeviceToHost, c.s));
+        c.sync();
+    }
+    const double lam_max = op.lam_max;
+    long mcap = std::min(n, std::max(2 * k + 30, 60L));
+    DevBuf Vb, wbuf, ybuf, ibuf, ubuf, aubuf;
+    Vb.ensure(sizeof(double) * n * mcap);
+    wbuf.ensure(sizeof(double) * n);
+    ybuf.ensure(sizeof(double) * n);
+    ibuf.ensure(sizeof(double) * n);
+    ubuf.ensure(sizeof(double) * n * k);
+    aubuf.ensure(sizeof(double) * n);
+    Workspace<double> ws;
+    double* w = wbuf.template as<double>();
+    double* nrm = c.sc(3);
+    double* coef = c.sc(4);
+    auto V = [&](long j) { return Vb.template as<double>() + (size_t)j * n; };
+    auto grow = [&](long want) {
+        if (want <= mcap) return;
+        const long nc = std::min(n, std::max(want, 2 * mcap));
+        DevBuf nb;
+        nb.ensure(sizeof(double) * n * nc);
+        CK(cudaMemcpyAsync(nb.p, Vb.p, sizeof(double) * n * mcap, cudaMemcpyDeviceToDevice, c.s));
+        c.sync();
+        std::swap(Vb.p, nb.p);
+        std::swap(Vb.bytes, nb.bytes);
+        mcap = nc;
+    };
+    auto host1 = [&](const double* d) {
+        double h;
+        CK(cudaMemcpyAsync(&h, d, sizeof(double), cudaMemcpyDeviceToHost, c.s));
+        c.sync();
+        return h;
+    };
+    uint64_t seed = 12345;
+    auto random_unit = [&](double* v) {
+        vec_randn<<<c.grid_for(n, 256, 8), 256, 0, c.s>>>(v, n, seed++);
+        c.check_launch();
+    };
+    random_unit(V(0));
+    launch_norms<double>(c, V(0), n, nrm);
+    launch_scale<double>(c, V(0), V(0), n, nrm, 0);
+    std::vector<double> alphas, betas;
+    long m = 0;
+    auto ritz = [&]() -> bool {
+        if (m < k) return false;
+        std::vector<double> T((size_t)m * m, 0.0), Z;
+        for (long i = 0; i < m; ++i) {
+            T[i + i * m] = alphas[i];
+            if (i + 1 < m) T[i + (i + 1) * m] = T[(i + 1) + i * m] = betas[i];
+        }
+        jacobi_eig(m, T, Z);
+        std::vector<long> ord(m);
+        for (long i = 0; i < m; ++i) ord[i] = i;
+        std::sort(ord.begin(), ord.end(), [&](long a, long b) { return T[a + a * m] > T[b + b * m]; });
+        std::vector<double> lm(k);
+        double* U = ubuf.template as<double>();
+        for (long i = 0; i < k; ++i) {
+            // u_i = V_m z_i, normalised
+            std::vector<double> z(m);
+            for (long t = 0; t < m; ++t) z[t] = -Z[t + ord[i] * m];
+            CK(cudaMemcpyAsync(coef, z.data(), sizeof(double) * m, cudaMemcpyHostToDevice, c.s));
+            CK(cudaMemsetAsync(ybuf.p, 0, sizeof(double) * n, c.s));
+            double* ui = U + (size_t)i * n;
+            ts_N_launch<double>(c, V(0), n, m, ybuf.template as<double>(), ui, n, coef);
+            launch_norms<double>(c, ui, n, nrm);
+            launch_scale<double>(c, ui, ui, n, nrm, 0);
+        }
+        for (long i = 0; i < k; ++i) {
+            double* ui = U + (size_t)i * n;
+            double* au = aubuf.template as<double>();
+            launch_stencil<double>(c, op.d, ui, n, nullptr, au, n, 1);
+            ts_T_launch<double, false>(c, ui, n, 1, au, n, nrm + 16);
+            const double li = host1(nrm + 16);
+            lm[i] = li;
+            // au - li * ui
+            vec_axpby<double><<<c.grid_for(n, 256, 8), 256, 0, c.s>>>(n, make_double2(-li, 0.0), ui,
+                                                                       make_double2(1.0, 0.0), au);
+            c.check_launch();
+            launch_norms<double>(c, au, n, nrm);
+            if (std::sqrt(host1(nrm)) > tol * lam_max) return false;
+        }
+        lam = lm;
+        CK(cudaMemcpyAsync(Uout, U, sizeof(double) * n * k, cudaMemcpyDeviceToDevice, c.s));
+        c.sync();
+        return true;
+    };
+    const long check_every = std::max(k, 10L);
+    while (m < n) {
+        grow(m + 1);
+        recycled_cg<double>(c, op, nullptr, nullptr, 0, V(m), inner_tol, 2 * n, 0.0, w, ybuf.template as<double>(),
+                            ibuf.template as<double>(), ws, false);
+        ts_T_launch<double, false>(c, V(m), n, 1, w, n, nrm + 16);
+        const double alpha = host1(nrm + 16);
+        vec_axpby<double><<<c.grid_for(n, 256, 8), 256, 0, c.s>>>(n, make_double2(-alpha, 0.0), V(m),
+                                                                   make_double2(1.0, 0.0), w);
+        c.check_launch();
+        if (m > 0) {
+            vec_axpby<double><<<c.grid_for(n, 256, 8), 256, 0, c.s>>>(n, make_double2(-betas[m - 1], 0.0), V(m - 1),
+                                                                       make_double2(1.0, 0.0), w);
+            c.check_launch();
+        }
+        // full reorthogonalisation, two passes (CGS2 against V[:, 0..m])
+        cgs2<double, false>(c, V(0), n, m + 1, w, w, n, coef, c.sc(5), c.sc(6));
+        alphas.push_back(alpha);
+        ++m;
+        launch_norms<double>(c, w, n, nrm);
+        double beta = std::sqrt(host1(nrm));
+        if (beta <= 1e-13 * std::fabs(alpha)) {
+            if (m >= n) {
+                betas.push_back(0.0);
+                break;
+            }
+            random_unit(w);
+            cgs2<double, false>(c, V(0), n, m, w, w, n, coef, c.sc(5), c.sc(6));
+            launch_norms<double>(c, w, n, nrm);
+            launch_scale<double>(c, w, w, n, nrm, 0);
+            beta = 0.0;
+        } else {
+            launch_scale<double>(c, w, w, n, nrm, 0);
+        }
+        if (m < n) {
+            betas.push_back(beta);
+            grow(m + 1);
+            CK(cudaMemcpyAsync(V(m), w, sizeof(double) * n, cudaMemcpyDeviceToDevice, c.s));
+        }
+        if ((m % check_every == 0 || m == n) && ritz()) return;
+    }
+    if (ritz()) return;
+    throw SolverError("eigensolver: Lanczos did not converge");
+}
+
 // ---------------------------------------------------------- global basis ---
 constexpr uint8_t kColEigenvector = 0, kColInitialSolution = 1, kColCorrection = 2;
 constexpr double kInnerSafety = 0.25;  // basis.cpp:27
@@ -419,6 +759,10 @@ template <class T> struct DevBasis : BasisBase {
     bool factored = false;
     Workspace<T> ws;
     DevBuf tmpv, tmpv2, AW, Ur, Kr, idx, X, bvec;
+    DevBuf Ktmp, Gd, Sinvd, Rd, Rd2, gwork;   // block refresh workspace
+    long eig_ready_for = -1;                 // system tag whose eig-block factor sits in Ur/Kr
+    long cmax_space = 0;
+    long stats_block_refresh = 0, stats_seq_refresh = 0, stats_second_pass = 0;
 
     T* Vp() const { return V.template as<T>(); }
     T* Wp() const { return Wm.template as<T>(); }
@@ -427,7 +771,7 @@ template <class T> struct DevBasis : BasisBase {
     void reserve(long want) {
         if (want <= capcols) return;
         long nc = std::max(want, std::max(16L, capcols * 3 / 2));
-        if (cap > 0) nc = std::min(nc, std::max(want, cap));
+        if (cap > 0) nc = std::max(want, cap);  // capped bases are allocated once
         auto grow = [&](DevBuf& b) {
             DevBuf nb;
             nb.ensure(sizeof(T) * n * nc);
@@ -512,8 +856,20 @@ template <class T> struct DevBasis : BasisBase {
     }
 
     // GlobalBasis::refresh (basis.cpp:37-76): K_img R = A_i V with drop rule
-    // |R_ii| <= 1e-12 ||A_i v_i|| for i >= ku. Sequential CGS2 factorisation.
+    // |R_ii| <= 1e-12 ||A_i v_i|| for i >= ku.
+    // First call: sequential CGS2 factorisation of every column. Later calls
+    // reuse W = V R^-1 of the previous system: Y = A_i W is close to
+    // orthonormal (A_i A_{i-1}^-1 ~ I), so one Gram + Cholesky (CholQR) gives
+    // K_img = Y S^-1, W <- W S^-1, R <- S R; a second pass only if kappa(S)
+    // is large. Any pivot failure or deficient column falls back to the
+    // sequential path (which drops columns like the reference).
     void refresh(DevOp& op) {
+        eig_ready_for = -1;
+        if (factored && cols > 0 && refresh_block(op)) {
+            ++stats_block_refresh;
+            return;
+        }
+        ++stats_seq_refresh;
         long j = 0;
         while (j < cols) {
             if (factor_column(op, j, j >= ku)) {
@@ -523,6 +879,135 @@ template <class T> struct DevBasis : BasisBase {
             }
         }
         factored = true;
+    }
+
+    bool refresh_block(DevOp& op) {
+        Ctx& c = *ctx;
+        const long r = cols;
+        Ktmp.ensure(sizeof(T) * n * capcols);
+        Gd.ensure(sizeof(T) * r * r);
+        Sinvd.ensure(sizeof(T) * r * r);
+        Rd.ensure(sizeof(T) * r * r);
+        Rd2.ensure(sizeof(T) * r * r);
+        launch_stencil<T>(c, op.d, Wp(), n, nullptr, Ktmp.template as<T>(), n, r);  // Y = A_i W
+        // upload R (ld r)
+        std::vector<T> Rh((size_t)r * r, Sc<T>::zero());
+        for (long j = 0; j < r; ++j)
+            for (long i = 0; i <= j; ++i) Rh[i + j * r] = Rat(i, j);
+        CK(cudaMemcpyAsync(Rd.p, Rh.data(), sizeof(T) * r * r, cudaMemcpyHostToDevice, c.s));
+        for (int pass = 0; pass < 2; ++pass) {
+            // pass 0 factors Y (in Ktmp); pass 1 re-orthogonalises K_img
+            const T* src = pass == 0 ? Ktmp.template as<T>() : Kp();
+            gram<T, true>(c, src, n, r, src, n, r, n, Gd.template as<T>(), true, gwork);
+            CholInfo ci = chol_inv<T, true>(c, Gd.template as<T>(), Sinvd.template as<T>(), r, true);
+            if (ci.bad) return false;
+            if (pass == 0) {
+                gemm<T, false>(c, src, n, r, Sinvd.template as<T>(), r, nullptr, 0, Kp(), n, n, true);
+            } else {
+                gemm<T, false>(c, src, n, r, Sinvd.template as<T>(), r, nullptr, 0, Ktmp.template as<T>(), n, n, true);
+                std::swap(K.p, Ktmp.p);
+                std::swap(K.bytes, Ktmp.bytes);
+            }
+            gemm<T, false>(c, Wp(), n, r, Sinvd.template as<T>(), r, nullptr, 0, Ktmp.template as<T>(), n, n, true);
+            std::swap(Wm.p, Ktmp.p);
+            std::swap(Wm.bytes, Ktmp.bytes);
+            tri_mul_upper<T><<<c.grid_for(r * r, 256, 4), 256, 0, c.s>>>(Gd.template as<T>(), Rd.template as<T>(),
+                                                                           Rd2.template as<T>(), (int)r, (int)r);
+            c.check_launch();
+            std::swap(Rd.p, Rd2.p);
+            std::swap(Rd.bytes, Rd2.bytes);
+            if (ci.kappa1 <= 20.0) break;
+            ++stats_second_pass;
+        }
+        CK(cudaMemcpyAsync(Rh.data(), Rd.p, sizeof(T) * r * r, cudaMemcpyDeviceToHost, c.s));
+        c.sync();
+        // deficiency check (basis.cpp:57-61): |R_ii| <= 1e-12 ||R(:, i)|| = 1e-12 ||A_i v_i||
+        for (long i = ku; i < r; ++i) {
+            double cn = 0.0;
+            for (long k = 0; k <= i; ++k) cn += Sc<T>::abs2(Rh[k + i * r]);
+            if (std::sqrt(Sc<T>::abs2(Rh[i + i * r])) <= 1e-12 * std::sqrt(cn)) {
+                factored = false;  // sequential path re-factors and drops
+                return false;
+            }
+        }
+        for (long j = 0; j < r; ++j)
+            for (long i = 0; i <= j; ++i) Rat(i, j) = Rh[i + j * r];
+        return true;
+    }
+
+    // ---- per-RHS recycle spaces (RecycleSpace::from_raw, krylov.cpp:106-115) ----
+    // U_j = V[:, idx_j] with idx_j = [0..ku) + trailing columns. The eigen block
+    // [0..ku) is shared by every RHS of a system, so its factor A_i U0 = Q0 S0
+    // (bilinear for complex) and P0 = U0 S0^-1 are computed once per system
+    // into the leading columns of Kr / Ur; per RHS only the trailing columns
+    // are projected against Q0 (block CGS2) and orthonormalised (CGS2).
+    // Same span and projector as the reference's full per-RHS QR.
+    void factor_eig_block(DevOp& op, long cspace) {
+        Ctx& c = *ctx;
+        Ur.ensure(sizeof(T) * n * std::max(1L, cspace));
+        Kr.ensure(sizeof(T) * n * std::max(1L, cspace));
+        AW.ensure(sizeof(T) * n * std::max(1L, std::max(ku, cspace)));
+        tmpv2.ensure(sizeof(T) * n);
+        if (ku == 0) return;
+        T* Kb = Kr.template as<T>();
+        T* Ub = Ur.template as<T>();
+        T* S = AW.template as<T>();
+        Gd.ensure(sizeof(T) * ku * ku);
+        Sinvd.ensure(sizeof(T) * ku * ku);
+        launch_stencil<T>(c, op.d, Vp(), n, nullptr, Kb, n, ku);  // A_i U0
+        CK(cudaMemcpyAsync(Ub, Vp(), sizeof(T) * n * ku, cudaMemcpyDeviceToDevice, c.s));
+        for (int pass = 0; pass < 3; ++pass) {
+            gram<T, false>(c, Kb, n, ku, Kb, n, ku, n, Gd.template as<T>(), true, gwork);
+            CholInfo ci = chol_inv<T, false>(c, Gd.template as<T>(), Sinvd.template as<T>(), ku, true);
+            if (ci.bad) throw SolverError("recycle space: eigen block image is numerically singular");
+            gemm<T, false>(c, Kb, n, ku, Sinvd.template as<T>(), ku, nullptr, 0, S, n, n, true);
+            CK(cudaMemcpyAsync(Kb, S, sizeof(T) * n * ku, cudaMemcpyDeviceToDevice, c.s));
+            gemm<T, false>(c, Ub, n, ku, Sinvd.template as<T>(), ku, nullptr, 0, S, n, n, true);
+            CK(cudaMemcpyAsync(Ub, S, sizeof(T) * n * ku, cudaMemcpyDeviceToDevice, c.s));
+            if (ci.kappa1 <= 20.0) break;
+        }
+    }
+
+    void factor_rhs_space(DevOp& op, const std::vector<int>& cidx) {
+        Ctx& c = *ctx;
+        constexpr int W = Sc<T>::W;
+        const long cj = (long)cidx.size();
+        const long m = cj - ku;
+        T* Kb = Kr.template as<T>();
+        T* Ub = Ur.template as<T>();
+        if (m <= 0) return;
+        T* Kt = Kb + (size_t)ku * n;
+        T* Ut = Ub + (size_t)ku * n;
+        idx.ensure(sizeof(int) * m);
+        CK(cudaMemcpyAsync(idx.p, cidx.data() + ku, sizeof(int) * m, cudaMemcpyHostToDevice, c.s));
+        launch_stencil<T>(c, op.d, Vp(), n, idx.template as<int>(), Kt, n, m);
+        for (long t = 0; t < m; ++t)
+            CK(cudaMemcpyAsync(Ut + (size_t)t * n, Vp() + (size_t)cidx[ku + t] * n, sizeof(T) * n,
+                               cudaMemcpyDeviceToDevice, c.s));
+        if (ku > 0) {
+            T* C1 = (T*)c.sc(4);
+            T* C2 = (T*)c.sc(5);
+            if (ku * m * W > 8192) throw ConfigError("recycle space: trailing block too wide");
+            gram<T, false>(c, Kb, n, ku, Kt, n, m, n, C1, false, gwork);
+            gemm<T, true>(c, Kb, n, ku, C1, m, Kt, n, Kt, n, n, false);
+            gram<T, false>(c, Kb, n, ku, Kt, n, m, n, C2, false, gwork);
+            gemm<T, true>(c, Kb, n, ku, C2, m, Kt, n, Kt, n, n, false);
+            launch_addsub(c, (int)(ku * m * W), (double*)C1, (double*)C2, 1.0, (double*)C1);
+            gemm<T, true>(c, Ub, n, ku, C1, m, Ut, n, Ut, n, n, false);
+        }
+        double* coef = c.sc(6);
+        double* nrm = c.sc(7);
+        for (long t = 0; t < m; ++t) {
+            T* kt = Kt + (size_t)t * n;
+            T* ut = Ut + (size_t)t * n;
+            if (t > 0) {
+                cgs2<T, false>(c, Kt, n, t, kt, kt, n, coef, c.sc(4), c.sc(5));
+                ts_N_launch<T>(c, Ut, n, t, ut, ut, n, coef);
+            }
+            launch_norms<T>(c, kt, n, nrm);
+            launch_scale<T>(c, kt, kt, n, nrm, 1);
+            launch_scale<T>(c, ut, ut, n, nrm, 1);
+        }
     }
 
     bool append(const T* y, const T* z, uint8_t marker) {
@@ -568,6 +1053,9 @@ void process_system(DevBasis<T>& gb, DevOp& op, long nrhs, const long* bidx, con
     const long n = gb.n;
     if (maxit <= 0) maxit = 2 * n;
     gb.refresh(op);
+    long cspace = 1;
+    for (const auto& sp : gb.spaces) cspace = std::max(cspace, (long)sp.size() + 1);
+    gb.factor_eig_block(op, cspace);
     log.clear();
     inner_its = 0;
     appends = 0;
@@ -605,13 +1093,7 @@ void process_system(DevBasis<T>& gb, DevOp& op, long nrhs, const long* bidx, con
         } else {
             auto& idx = gb.spaces[j];
             const long cj = (long)idx.size();
-            gb.idx.ensure(sizeof(int) * std::max(1L, cj));
-            CK(cudaMemcpyAsync(gb.idx.p, idx.data(), sizeof(int) * cj, cudaMemcpyHostToDevice, c.s));
-            gb.AW.ensure(sizeof(T) * n * cj);
-            gb.Ur.ensure(sizeof(T) * n * cj);
-            gb.Kr.ensure(sizeof(T) * n * cj);
-            launch_stencil<T>(c, op.d, gb.Vp(), n, gb.idx.template as<int>(), gb.AW.template as<T>(), n, cj);
-            from_raw<T>(c, n, cj, gb.Vp(), idx.data(), gb.AW.template as<T>(), gb.Ur.template as<T>(), gb.Kr.template as<T>());
+            gb.factor_rhs_space(op, idx);
             SolveOut so = recycled_cg<T>(c, op, gb.Ur.template as<T>(), gb.Kr.template as<T>(), cj, rj, kInnerSafety * tol, maxit,
                                          bnorm, gbuf.template as<T>(), ybuf.template as<T>(), imbuf.template as<T>(), gb.ws, false);
             if (!so.converged)
@@ -781,6 +1263,18 @@ double rd_ctx_elapsed_ms(rd_ctx* ctx) {
     return ms;
 }
 long rd_ctx_launches(rd_ctx* ctx) { return ctx->c.launches; }
+void rd_ctx_profile(rd_ctx* ctx, int enable) {
+    ctx->c.prof = enable != 0;
+    for (auto& q : ctx->c.pc) q = Ctx::ProfClass();
+}
+int rd_ctx_prof_get(rd_ctx* ctx, int cls, double* ms, double* bytes, long* samples) {
+    if (cls < 0 || cls >= 8) return 2;
+    const auto& q = ctx->c.pc[cls];
+    if (ms) *ms = q.ms;
+    if (bytes) *bytes = q.bytes;
+    if (samples) *samples = q.samples;
+    return 0;
+}
 void* rd_ctx_stream(rd_ctx* ctx) { return (void*)ctx->c.s; }
 
 int rd_op_create(rd_ctx* ctx, int d, const long* N, double robin_face, rd_op** out) {
@@ -816,6 +1310,10 @@ int rd_op_set_fields(rd_op* o, const double* D, const double* mu, double shift, 
         o->op.d.D = o->op.D.template as<double>();
         o->op.d.mu = o->op.mu.template as<double>();
         o->op.d.shift = shift;
+        o->op.F.ensure(sizeof(double) * 4 * n);
+        o->op.d.F = o->op.F.template as<double>();
+        op_prepare<<<stencil_grid(o->op.d, 1), 256, 0, c.s>>>(o->op.d, o->op.F.template as<double>());
+        c.check_launch();
         o->op.have_fields = true;
         if (where == 0) {
             std::vector<double> Dh(D, D + n), mh(mu, mu + n);
@@ -1140,14 +1638,32 @@ int rd_process_system(rd_basis* b, rd_op* op, long nrhs, const long* bidx, const
 }
 
 int rd_smallest_eigenpairs(rd_op* op, long k, double tol, double* lambda, void* U, int where) {
-    (void)op;
-    (void)k;
-    (void)tol;
-    (void)lambda;
-    (void)U;
-    (void)where;
-    g_err = "rd_smallest_eigenpairs: not built yet";
-    return 1;
+    return guard([&] {
+        Ctx& cx = op->ctx->c;
+        if (!op->op.have_fields) throw rd::ConfigError("operator: fields not set");
+        const long n = op->op.d.n;
+        Out Us(cx, U, sizeof(double) * n * k, where);
+        DevBuf tmp;
+        void* up = Us.p;
+        if (!up) {
+            tmp.ensure(sizeof(double) * n * k);
+            up = tmp.p;
+        }
+        std::vector<double> lam;
+        // the seed is defined on the omega = 0 (real SPD) operator
+        const double sh = op->op.d.shift;
+        op->op.d.shift = 0.0;
+        try {
+            smallest_eigenpairs_dev(cx, op->op, k, tol, lam, (double*)up);
+        } catch (...) {
+            op->op.d.shift = sh;
+            throw;
+        }
+        op->op.d.shift = sh;
+        Us.finish();
+        if (lambda)
+            for (long i = 0; i < k; ++i) lambda[i] = lam[i];
+    });
 }
 
 int rd_rrqr(rd_ctx* ctx, int dtype, long n, long m, const void* A, double tol, int normalize, long* rank, long* perm,

@@ -28,7 +28,7 @@ _SO = os.path.join(_HERE, "libromdot_b200.so")
 
 EXPORTS = [
     "rd_ctx_create", "rd_ctx_destroy", "rd_last_error", "rd_ctx_sync", "rd_ctx_mark", "rd_ctx_elapsed_ms",
-    "rd_ctx_launches", "rd_ctx_stream", "rd_op_create", "rd_op_destroy", "rd_op_set_fields", "rd_op_apply",
+    "rd_ctx_launches", "rd_ctx_stream", "rd_ctx_profile", "rd_ctx_prof_get", "rd_op_create", "rd_op_destroy", "rd_op_set_fields", "rd_op_apply",
     "rd_op_lam_max", "rd_recycled_solve", "rd_recycle_space_from_raw", "rd_initial_solutions",
     "rd_smallest_eigenpairs", "rd_basis_create", "rd_basis_destroy", "rd_basis_cols", "rd_basis_eig_block",
     "rd_basis_get", "rd_basis_device_ptr", "rd_basis_markers", "rd_basis_space", "rd_basis_refresh",
@@ -83,6 +83,9 @@ def load_library(path: Optional[str] = None):
     L.rd_ctx_launches.restype = C.c_long
     L.rd_ctx_stream.argtypes = [vp]
     L.rd_ctx_stream.restype = vp
+    L.rd_ctx_profile.argtypes = [vp, C.c_int]
+    L.rd_ctx_profile.restype = None
+    L.rd_ctx_prof_get.argtypes = [vp, C.c_int, dp, dp, lp]
     L.rd_op_create.argtypes = [vp, C.c_int, lp, C.c_double, C.POINTER(vp)]
     L.rd_op_destroy.argtypes = [vp]
     L.rd_op_set_fields.argtypes = [vp, vp, vp, C.c_double, C.c_int]
@@ -164,6 +167,20 @@ class Context:
     @property
     def launches(self) -> int:
         return load_library().rd_ctx_launches(self.h)
+
+    def profile(self, enable: bool = True):
+        load_library().rd_ctx_profile(self.h, int(enable))
+
+    PROF_CLASSES = ("cg_stencil_dots", "ts_T", "ts_NT", "cg_update")
+
+    def prof(self):
+        """{class: (ms_total, algorithmic_bytes_total, samples)} of the sampled launches."""
+        out = {}
+        for i, name in enumerate(self.PROF_CLASSES):
+            ms, by, ns = C.c_double(), C.c_double(), C.c_long()
+            load_library().rd_ctx_prof_get(self.h, i, C.byref(ms), C.byref(by), C.byref(ns))
+            out[name] = (ms.value, by.value, ns.value)
+        return out
 
     @property
     def stream(self) -> int:

@@ -190,3 +190,22 @@ def test_build_is_bitwise_deterministic(rd):
         return gb.V
 
     assert build().tobytes() == build().tobytes()
+
+
+@pytest.mark.parametrize("cfg", ["T2", "T3"])
+def test_device_eigen_seed_matches_oracle(rd, cfg):
+    """smallest_eigenpairs (krylov.cpp:181-280): eigenvalues vs the oracle
+    (exact shift-invert) to 1e-8 relative; residuals <= tol * lambda_max."""
+    c = P.CONFIGS[cfg]
+    g = c.grid
+    f0 = c.fields(0)
+    lam_o, U_o = orc.smallest_eigenpairs(orc.Operator.grid(g, f0), c.k, 1e-8)
+    op = rd.SchurOperator(g, f0)
+    lam, U = rd.smallest_eigenpairs(op, c.k, 1e-8)
+    assert np.allclose(lam, lam_o, rtol=1e-8)
+    A = orc.Operator.grid(g, f0)
+    lm = A.lam_max
+    for i in range(c.k):
+        r = A.apply(U[:, i]) - lam[i] * U[:, i]
+        assert np.linalg.norm(r) <= 1e-8 * lm
+    assert np.linalg.norm(U.T @ U - np.eye(c.k)) <= 1e-7
