@@ -127,18 +127,42 @@ __device__ __forceinline__ void node_coords(const OpDev& op, long p, int& i, int
     k = q / op.N1;
 }
 
-// y[:, c] = A x[:, xcol ? xcol[c] : c] for c < ncols; grid.z = N2 * ncols.
+// y[:, c] = A x[:, xcol ? xcol[c] : c] for c < ncols. One thread per node
+// (32 x 8 (i, j) tile per block, blockIdx.z = k); the node's seven
+// coefficients are loaded once and applied to every column.
 template <class T>
 __global__ void __launch_bounds__(256) stencil_kernel(OpDev op, const T* __restrict__ x, long ldx,
-                                                      const int* __restrict__ xcol, T* __restrict__ y, long ldy) {
-    const int c = blockIdx.z / op.N2;
+                                                      const int* __restrict__ xcol, T* __restrict__ y, long ldy,
+                                                      int ncols) {
     const int i = blockIdx.x * 32 + (threadIdx.x & 31);
     const int j = blockIdx.y * 8 + (threadIdx.x >> 5);
-    const int k = blockIdx.z - c * op.N2;
+    const int k = blockIdx.z;
     if (i >= op.N0 || j >= op.N1) return;
-    const long p = i + (long)op.N0 * (j + (long)op.N1 * k);
-    const T* xc = x + (size_t)(xcol ? xcol[c] : c) * ldx;
-    y[(size_t)c * ldy + p] = stencil_row<T>(op, xc, p, i, j, k);
+    const long n = op.n;
+    const long s1 = op.N0, s2 = (long)op.N0 * op.N1;
+    const long p = i + s1 * j + s2 * k;
+    const double* __restrict__ F = op.F;
+    const double dg = __ldg(F + p);
+    const double fxm = i > 0 ? __ldg(F + n + p - 1) : 0.0, fxp = i < op.N0 - 1 ? __ldg(F + n + p) : 0.0;
+    const double fym = j > 0 ? __ldg(F + 2 * n + p - s1) : 0.0, fyp = j < op.N1 - 1 ? __ldg(F + 2 * n + p) : 0.0;
+    double fzm = 0.0, fzp = 0.0;
+    if (op.d == 3) {
+        fzm = k > 0 ? __ldg(F + 3 * n + p - s2) : 0.0;
+        fzp = k < op.N2 - 1 ? __ldg(F + 3 * n + p) : 0.0;
+    }
+    for (int c = 0; c < ncols; ++c) {
+        const T* xc = x + (size_t)(xcol ? xcol[c] : c) * ldx;
+        T acc = Sc<T>::zero();
+        if (i > 0) acc = axpy_real(fxm, xc[p - 1], acc);
+        if (i < op.N0 - 1) acc = axpy_real(fxp, xc[p + 1], acc);
+        if (j > 0) acc = axpy_real(fym, xc[p - s1], acc);
+        if (j < op.N1 - 1) acc = axpy_real(fyp, xc[p + s1], acc);
+        if (op.d == 3) {
+            if (k > 0) acc = axpy_real(fzm, xc[p - s2], acc);
+            if (k < op.N2 - 1) acc = axpy_real(fzp, xc[p + s2], acc);
+        }
+        y[(size_t)c * ldy + p] = Sc<T>::sub(diag_apply<T>(dg, op.shift, xc[p]), acc);
+    }
 }
 
 // ------------------------------------------------------------ CG state ---
@@ -162,14 +186,17 @@ __device__ inline bool finite_(double v) { return isfinite(v); }
 // the scalar recurrence. One grid reduction per iteration.
 template <class T>
 __global__ void __launch_bounds__(256) cg_stencil_dots(OpDev op, const T* __restrict__ r, T* __restrict__ w,
-                                                       CGState* st, double* hist, GridRed red) {
+                                                       CGState* st, double* hist, GridRed red, int kz) {
     if (st->done) return;
     constexpr int W = Sc<T>::W;
     T g = Sc<T>::zero(), dl = Sc<T>::zero();
     double h = 0.0;
-    int i, j, k;
-    long p;
-    if (node_of_block(op, i, j, k, p)) {
+    // block = (32 x 8) x-y tile marching over kz planes (blockIdx.z chunk)
+    const int i = blockIdx.x * 32 + (threadIdx.x & 31);
+    const int j = blockIdx.y * 8 + (threadIdx.x >> 5);
+    const int k0 = blockIdx.z * kz, k1 = min(op.N2, k0 + kz);
+    for (int k = k0; k < k1 && i < op.N0 && j < op.N1; ++k) {
+        const long p = i + (long)op.N0 * (j + (long)op.N1 * k);
         const T wp = stencil_row<T>(op, r, p, i, j, k);
         w[p] = wp;
         const T rp = r[p];
@@ -264,6 +291,48 @@ __global__ void __launch_bounds__(256) cg_stencil_dots(OpDev op, const T* __rest
 constexpr int TS_THREADS = 256;
 constexpr int TS_WARPS = 8;
 
+// Batched streaming loads: volatile PTX loads keep their program order, and the
+// empty volatile "fence" that names every loaded register makes the consumer
+// FMAs wait until all loads of the batch have been issued (ILP, not one load
+// in flight per thread).
+template <class T> __device__ __forceinline__ T ldg_nc(const T* p);
+template <> __device__ __forceinline__ double ldg_nc<double>(const double* p) {
+    double v;
+    asm volatile("ld.global.nc.f64 %0, [%1];" : "=d"(v) : "l"(p));
+    return v;
+}
+template <> __device__ __forceinline__ cplx ldg_nc<cplx>(const cplx* p) {
+    cplx v;
+    asm volatile("ld.global.nc.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "l"(p));
+    return v;
+}
+template <class T> __device__ __forceinline__ void reg_fence(T& v);
+template <> __device__ __forceinline__ void reg_fence<double>(double& v) { asm volatile("" : "+d"(v)); }
+template <> __device__ __forceinline__ void reg_fence<cplx>(cplx& v) { asm volatile("" : "+d"(v.x), "+d"(v.y)); }
+
+// Basis addressing. Column-major: (i, j) -> j*ld + i. Row-blocked ("RB"):
+// 32-row blocks, each holding all C columns contiguously,
+// (i, j) -> (i/32)*32*C + j*32 + i%32, so every 32-row tile of the basis the
+// inner-iteration kernels touch is one contiguous chunk of 32*C elements.
+template <bool RB> __device__ __forceinline__ size_t kaddr(long row, int j, long ld) {
+    if (RB) return (size_t)(row >> 5) * (32 * (size_t)ld) + (size_t)j * 32 + (size_t)(row & 31);
+    return (size_t)j * ld + (size_t)row;
+}
+
+// Repack an n x c column-major basis into the row-blocked layout (zero pad).
+template <class T>
+__global__ void repack_rb(const T* __restrict__ K, long ldk, int c, long n, T* __restrict__ out, long nrows_out) {
+    const long nb = (nrows_out + 31) >> 5;
+    const long tot = nb * 32 * (long)c;
+    for (long e = blockIdx.x * (long)blockDim.x + threadIdx.x; e < tot; e += (long)gridDim.x * blockDim.x) {
+        const long rb = e / (32L * c);
+        const long rem = e - rb * 32L * c;
+        const int j = (int)(rem >> 5);
+        const long row = rb * 32 + (rem & 31);
+        out[e] = row < n ? K[(size_t)j * ldk + row] : Sc<T>::zero();
+    }
+}
+
 template <class T, bool HERM, int CPW>
 __device__ __forceinline__ void ts_finish_cols(T (&acc)[CPW], int c, int col0, GridRed red, double* out,
                                                const double* flagdone) {
@@ -299,7 +368,10 @@ template <class T, int CPW> struct TSU {
 };
 
 // out[col0 + j] = sum_i op(K[i, col0 + j]) x[i], j < c (c <= 8*CPW)
-template <class T, bool HERM, int CPW>
+// Loads use clamped (always valid) indices so every lane issues all CPW x U
+// loads back to back; out-of-range rows are masked through x = 0 and
+// out-of-range columns are never committed.
+template <class T, bool HERM, int CPW, bool RB>
 __global__ void __launch_bounds__(TS_THREADS) ts_T(const T* __restrict__ K, long ldk, int c, int col0,
                                                    const T* __restrict__ x, long n, GridRed red, double* out,
                                                    const CGState* st) {
@@ -310,10 +382,11 @@ __global__ void __launch_bounds__(TS_THREADS) ts_T(const T* __restrict__ K, long
     T acc[CPW];
 #pragma unroll
     for (int jj = 0; jj < CPW; ++jj) acc[jj] = Sc<T>::zero();
-    const long nsteps = (n + 32 * U - 1) / (32 * U);
-    const T* Kc = K + (size_t)(col0 + j0) * ldk;
     int ncol = c - j0;
     if (ncol > CPW) ncol = CPW;
+    if (ncol < 1) ncol = 1;
+    const int jbase = (j0 < c ? j0 : 0) + col0;
+    const long nsteps = (n + 32 * U - 1) / (32 * U);
     for (long stp = blockIdx.x; stp < nsteps; stp += gridDim.x) {
         const long base = stp * 32 * U + lane;
         T xv[U];
@@ -321,22 +394,29 @@ __global__ void __launch_bounds__(TS_THREADS) ts_T(const T* __restrict__ K, long
 #pragma unroll
         for (int u = 0; u < U; ++u) {
             const long row = base + 32 * u;
-            const bool ok = row < n;
-            xv[u] = ok ? x[row] : Sc<T>::zero();
+            const long rr = row < n ? row : n - 1;
 #pragma unroll
-            for (int jj = 0; jj < CPW; ++jj)
-                kv[u][jj] = (ok && jj < ncol) ? Kc[(size_t)jj * ldk + row] : Sc<T>::zero();
+            for (int jj = 0; jj < CPW; ++jj) kv[u][jj] = ldg_nc(K + kaddr<RB>(rr, jbase + (jj < ncol ? jj : ncol - 1), ldk));
+            xv[u] = ldg_nc(x + rr);
         }
 #pragma unroll
-        for (int u = 0; u < U; ++u)
+        for (int u = 0; u < U; ++u) {
+#pragma unroll
+            for (int jj = 0; jj < CPW; ++jj) reg_fence(kv[u][jj]);
+            reg_fence(xv[u]);
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            if (base + 32 * u >= n) xv[u] = Sc<T>::zero();
 #pragma unroll
             for (int jj = 0; jj < CPW; ++jj) acc[jj] = opfma<T, HERM>(kv[u][jj], xv[u], acc[jj]);
+        }
     }
     ts_finish_cols<T, HERM, CPW>(acc, c, col0, red, out, nullptr);
 }
 
 // Fused CGS pass: xo = x - K c1 (c1 = cin, device), out = op(K)^T xo.
-template <class T, bool HERM, int CPW>
+template <class T, bool HERM, int CPW, bool RB>
 __global__ void __launch_bounds__(TS_THREADS) ts_NT(const T* __restrict__ K, long ldk, int c,
                                                     const T* __restrict__ x, T* __restrict__ xo, long n,
                                                     const double* __restrict__ cin, GridRed red, double* out,
@@ -347,16 +427,18 @@ __global__ void __launch_bounds__(TS_THREADS) ts_NT(const T* __restrict__ K, lon
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const int j0 = wid * CPW;
     __shared__ T s_part[TS_WARPS][32 * U];
+    __shared__ T s_cw[TS_WARPS * CPW];
+    for (int t = threadIdx.x; t < TS_WARPS * CPW; t += blockDim.x)
+        s_cw[t] = t < c ? Sc<T>::get(cin + (size_t)t * W) : Sc<T>::zero();
+    __syncthreads();
     int ncol = c - j0;
     if (ncol > CPW) ncol = CPW;
-    T cw[CPW];
-#pragma unroll
-    for (int jj = 0; jj < CPW; ++jj) cw[jj] = (jj < ncol) ? Sc<T>::get(cin + (size_t)(j0 + jj) * W) : Sc<T>::zero();
+    if (ncol < 1) ncol = 1;
+    const int jbase = j0 < c ? j0 : 0;
     T acc[CPW];
 #pragma unroll
     for (int jj = 0; jj < CPW; ++jj) acc[jj] = Sc<T>::zero();
     const long nsteps = (n + 32 * U - 1) / (32 * U);
-    const T* Kc = K + (size_t)j0 * ldk;
     for (long stp = blockIdx.x; stp < nsteps; stp += gridDim.x) {
         const long base = stp * 32 * U + lane;
         T xv[U];
@@ -364,17 +446,20 @@ __global__ void __launch_bounds__(TS_THREADS) ts_NT(const T* __restrict__ K, lon
 #pragma unroll
         for (int u = 0; u < U; ++u) {
             const long row = base + 32 * u;
-            const bool ok = row < n;
-            xv[u] = ok ? x[row] : Sc<T>::zero();  // read before the barrier: xo may alias x
+            const long rr = row < n ? row : n - 1;
 #pragma unroll
-            for (int jj = 0; jj < CPW; ++jj)
-                kv[u][jj] = (ok && jj < ncol) ? Kc[(size_t)jj * ldk + row] : Sc<T>::zero();
+            for (int jj = 0; jj < CPW; ++jj) kv[u][jj] = ldg_nc(K + kaddr<RB>(rr, jbase + (jj < ncol ? jj : ncol - 1), ldk));
+            xv[u] = x[rr];  // read before the barrier: xo may alias x
         }
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+#pragma unroll
+            for (int jj = 0; jj < CPW; ++jj) reg_fence(kv[u][jj]);
 #pragma unroll
         for (int u = 0; u < U; ++u) {
             T part = Sc<T>::zero();
 #pragma unroll
-            for (int jj = 0; jj < CPW; ++jj) part = Sc<T>::fma(kv[u][jj], cw[jj], part);
+            for (int jj = 0; jj < CPW; ++jj) part = Sc<T>::fma(kv[u][jj], s_cw[j0 + jj], part);
             s_part[wid][32 * u + lane] = part;
         }
         __syncthreads();
@@ -383,8 +468,9 @@ __global__ void __launch_bounds__(TS_THREADS) ts_NT(const T* __restrict__ K, lon
             T sum = s_part[0][32 * u + lane];
 #pragma unroll
             for (int w2 = 1; w2 < TS_WARPS; ++w2) sum = Sc<T>::add(sum, s_part[w2][32 * u + lane]);
-            const T xn = Sc<T>::sub(xv[u], sum);
             const long row = base + 32 * u;
+            T xn = Sc<T>::sub(xv[u], sum);
+            if (row >= n) xn = Sc<T>::zero();
             if (wid == 0 && row < n) xo[row] = xn;
 #pragma unroll
             for (int jj = 0; jj < CPW; ++jj) acc[jj] = opfma<T, HERM>(kv[u][jj], xn, acc[jj]);
@@ -421,7 +507,7 @@ __global__ void __launch_bounds__(256) ts_N(const T* __restrict__ K, long ldk, i
 }
 
 // K4: q = w - K c2 ; p = r + beta p ; s = q + beta s ; y += alpha p ; r -= alpha s
-template <class T>
+template <class T, bool RB>
 __global__ void __launch_bounds__(256) cg_update(const T* __restrict__ K, long ldk, int c, const T* __restrict__ w,
                                                  long n, const double* __restrict__ c2, T* __restrict__ r,
                                                  T* __restrict__ p, T* __restrict__ s, T* __restrict__ y,
@@ -435,15 +521,16 @@ __global__ void __launch_bounds__(256) cg_update(const T* __restrict__ K, long l
     for (long row = blockIdx.x * (long)blockDim.x + threadIdx.x; row < n; row += (long)gridDim.x * blockDim.x) {
         T acc = Sc<T>::zero();
         int j = 0;
-        for (; j + 4 <= c; j += 4) {
-            const T k0 = K[(size_t)j * ldk + row], k1 = K[(size_t)(j + 1) * ldk + row];
-            const T k2 = K[(size_t)(j + 2) * ldk + row], k3 = K[(size_t)(j + 3) * ldk + row];
-            acc = Sc<T>::fma(k0, Sc<T>::get(s_c + j * W), acc);
-            acc = Sc<T>::fma(k1, Sc<T>::get(s_c + (j + 1) * W), acc);
-            acc = Sc<T>::fma(k2, Sc<T>::get(s_c + (j + 2) * W), acc);
-            acc = Sc<T>::fma(k3, Sc<T>::get(s_c + (j + 3) * W), acc);
+        for (; j + 8 <= c; j += 8) {
+            T kk[8];
+#pragma unroll
+            for (int q = 0; q < 8; ++q) kk[q] = ldg_nc(K + kaddr<RB>(row, j + q, ldk));
+#pragma unroll
+            for (int q = 0; q < 8; ++q) reg_fence(kk[q]);
+#pragma unroll
+            for (int q = 0; q < 8; ++q) acc = Sc<T>::fma(kk[q], Sc<T>::get(s_c + (j + q) * W), acc);
         }
-        for (; j < c; ++j) acc = Sc<T>::fma(K[(size_t)j * ldk + row], Sc<T>::get(s_c + j * W), acc);
+        for (; j < c; ++j) acc = Sc<T>::fma(K[kaddr<RB>(row, j, ldk)], Sc<T>::get(s_c + j * W), acc);
         const T q = Sc<T>::sub(w[row], acc);
         const T pn = Sc<T>::fma(beta, p[row], r[row]);
         const T sn = Sc<T>::fma(beta, s[row], q);

@@ -17,6 +17,7 @@
 #include "../../include/romdot_b200.h"
 #include "dense.cuh"
 #include "kernels.cuh"
+#include "ts_tma.cuh"
 
 namespace rd {
 
@@ -183,48 +184,52 @@ inline dim3 stencil_grid(const OpDev& op, long zmult) {
 template <class T> void launch_stencil(Ctx& c, const OpDev& op, const T* x, long ldx, const int* xcol, T* y,
                                        long ldy, long ncols) {
     if (ncols <= 0) return;
-    const long maxc = std::max(1L, 65535L / op.N2);
-    for (long c0 = 0; c0 < ncols; c0 += maxc) {
-        const long nc = std::min(maxc, ncols - c0);
-        stencil_kernel<T><<<stencil_grid(op, nc), 256, 0, c.s>>>(op, xcol ? x : x + (size_t)c0 * ldx, ldx,
-                                                                  xcol ? xcol + c0 : nullptr, y + (size_t)c0 * ldy, ldy);
+    for (long c0 = 0; c0 < ncols; c0 += 16) {
+        const long nc = std::min(16L, ncols - c0);
+        stencil_kernel<T><<<stencil_grid(op, 1), 256, 0, c.s>>>(op, xcol ? x : x + (size_t)c0 * ldx, ldx,
+                                                                 xcol ? xcol + c0 : nullptr, y + (size_t)c0 * ldy,
+                                                                 ldy, (int)nc);
         c.check_launch();
     }
 }
 
-template <class T, bool HERM, int CPW>
+template <class T, bool HERM, int CPW, bool RB = false>
 void ts_T_inst(Ctx& c, const T* K, long ldk, int cc, int col0, const T* x, long n, double* out, const CGState* st) {
     const long ntiles = (n + 32 * TSU<T, CPW>::U - 1) / (32 * TSU<T, CPW>::U);
-    const int grid = (int)std::max(1L, std::min<long>(ntiles, (long)c.sms * 2));
-    ts_T<T, HERM, CPW><<<grid, TS_THREADS, 0, c.s>>>(K, ldk, cc, col0, x, n, c.red(), out, st);
+    const int grid = (int)std::max(1L, std::min<long>(ntiles, (long)c.sms * 4));
+    ts_T<T, HERM, CPW, RB><<<grid, TS_THREADS, 0, c.s>>>(K, ldk, cc, col0, x, n, c.red(), out, st);
     c.check_launch();
 }
 
-// out[j] = sum_i op(K_ij) x_i, j < ncol  (chunks of 128 columns)
-template <class T, bool HERM>
+// out[j] = sum_i op(K_ij) x_i, j < ncol  (chunks of 128 columns). RB: row-blocked K (ldk = C).
+template <class T, bool HERM, bool RB = false>
 void ts_T_launch(Ctx& c, const T* K, long ldk, long ncol, const T* x, long n, double* out, const CGState* st = nullptr) {
     for (long col0 = 0; col0 < ncol; col0 += 128) {
         const int cc = (int)std::min(128L, ncol - col0);
         const int cpw = (cc + 7) / 8;
         if (cpw <= 1)
-            ts_T_inst<T, HERM, 1>(c, K, ldk, cc, (int)col0, x, n, out, st);
+            ts_T_inst<T, HERM, 1, RB>(c, K, ldk, cc, (int)col0, x, n, out, st);
         else if (cpw <= 2)
-            ts_T_inst<T, HERM, 2>(c, K, ldk, cc, (int)col0, x, n, out, st);
+            ts_T_inst<T, HERM, 2, RB>(c, K, ldk, cc, (int)col0, x, n, out, st);
         else if (cpw <= 4)
-            ts_T_inst<T, HERM, 4>(c, K, ldk, cc, (int)col0, x, n, out, st);
+            ts_T_inst<T, HERM, 4, RB>(c, K, ldk, cc, (int)col0, x, n, out, st);
+        else if (cpw <= 6)
+            ts_T_inst<T, HERM, 6, RB>(c, K, ldk, cc, (int)col0, x, n, out, st);
         else if (cpw <= 8)
-            ts_T_inst<T, HERM, 8>(c, K, ldk, cc, (int)col0, x, n, out, st);
+            ts_T_inst<T, HERM, 8, RB>(c, K, ldk, cc, (int)col0, x, n, out, st);
+        else if (cpw <= 12)
+            ts_T_inst<T, HERM, 12, RB>(c, K, ldk, cc, (int)col0, x, n, out, st);
         else
-            ts_T_inst<T, HERM, 16>(c, K, ldk, cc, (int)col0, x, n, out, st);
+            ts_T_inst<T, HERM, 16, RB>(c, K, ldk, cc, (int)col0, x, n, out, st);
     }
 }
 
-template <class T, bool HERM, int CPW>
+template <class T, bool HERM, int CPW, bool RB = false>
 void ts_NT_inst(Ctx& c, const T* K, long ldk, int cc, const T* x, T* xo, long n, const double* cin, double* out,
                 const CGState* st) {
     const long ntiles = (n + 32 * TSU<T, CPW>::U - 1) / (32 * TSU<T, CPW>::U);
     const int grid = (int)std::max(1L, std::min<long>(ntiles, (long)c.sms * 2));
-    ts_NT<T, HERM, CPW><<<grid, TS_THREADS, 0, c.s>>>(K, ldk, cc, x, xo, n, cin, c.red(), out, st);
+    ts_NT<T, HERM, CPW, RB><<<grid, TS_THREADS, 0, c.s>>>(K, ldk, cc, x, xo, n, cin, c.red(), out, st);
     c.check_launch();
 }
 
@@ -247,10 +252,11 @@ void ts_N_launch(Ctx& c, const T* K, long ldk, long ncol, const T* x, T* xo, lon
 }
 
 // fused {xo = x - K c1 ; out = op(K)^T xo} for ncol <= 128, else N then T
-template <class T, bool HERM>
+template <class T, bool HERM, bool RB = false>
 void ts_NT_launch(Ctx& c, const T* K, long ldk, long ncol, const T* x, T* xo, long n, const double* cin,
                   double* out, const CGState* st = nullptr) {
     if (ncol > 128) {
+        if (RB) throw ConfigError("row-blocked basis limited to 128 columns");
         ts_N_launch<T>(c, K, ldk, ncol, x, xo, n, cin, 1.0, st);
         ts_T_launch<T, HERM>(c, K, ldk, ncol, xo, n, out, st);
         return;
@@ -258,15 +264,82 @@ void ts_NT_launch(Ctx& c, const T* K, long ldk, long ncol, const T* x, T* xo, lo
     const int cc = (int)ncol;
     const int cpw = (cc + 7) / 8;
     if (cpw <= 1)
-        ts_NT_inst<T, HERM, 1>(c, K, ldk, cc, x, xo, n, cin, out, st);
+        ts_NT_inst<T, HERM, 1, RB>(c, K, ldk, cc, x, xo, n, cin, out, st);
     else if (cpw <= 2)
-        ts_NT_inst<T, HERM, 2>(c, K, ldk, cc, x, xo, n, cin, out, st);
+        ts_NT_inst<T, HERM, 2, RB>(c, K, ldk, cc, x, xo, n, cin, out, st);
     else if (cpw <= 4)
-        ts_NT_inst<T, HERM, 4>(c, K, ldk, cc, x, xo, n, cin, out, st);
+        ts_NT_inst<T, HERM, 4, RB>(c, K, ldk, cc, x, xo, n, cin, out, st);
+    else if (cpw <= 6)
+        ts_NT_inst<T, HERM, 6, RB>(c, K, ldk, cc, x, xo, n, cin, out, st);
     else if (cpw <= 8)
-        ts_NT_inst<T, HERM, 8>(c, K, ldk, cc, x, xo, n, cin, out, st);
+        ts_NT_inst<T, HERM, 8, RB>(c, K, ldk, cc, x, xo, n, cin, out, st);
+    else if (cpw <= 12)
+        ts_NT_inst<T, HERM, 12, RB>(c, K, ldk, cc, x, xo, n, cin, out, st);
     else
-        ts_NT_inst<T, HERM, 16>(c, K, ldk, cc, x, xo, n, cin, out, st);
+        ts_NT_inst<T, HERM, 16, RB>(c, K, ldk, cc, x, xo, n, cin, out, st);
+}
+
+
+// ------------------------------------------------ TMA projection launcher ---
+constexpr long kRowPad = 256;  // row padding of RB bases and inner workspaces
+inline long padded_rows(long n) { return (n + kRowPad - 1) / kRowPad * kRowPad; }
+
+template <class T, int MODE, int CPW>
+void ts_tma_inst(Ctx& c, const T* Krb, int C, long n, const T* x, T* xo, const double* cin, double* out, T* r, T* p,
+                 T* s, T* y, CGState* st) {
+    const int es = sizeof(T);
+    const int NV = MODE == 2 ? 5 : 1;
+    int TR = 256;
+    while (TR > 32 && (long)TR * C * es > 48 * 1024) TR >>= 1;
+    TmaLayout L = tma_layout<T>(C, TR, 2, NV);
+    const uint32_t per_stage = ((L.tile_bytes + 127u) & ~127u) + NV * ((L.x_bytes + 127u) & ~127u);
+    const uint32_t fixed = L.total - 2 * per_stage;
+    int S = (int)std::min<long>(8, (196L * 1024 - fixed) / per_stage);
+    if (S < 2) S = 2;
+    L = tma_layout<T>(C, TR, S, NV);
+    static int configured = 0;
+    if (!configured) {
+        int optin = 0;
+        CK(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, c.device));
+        cudaFuncAttributes fa;
+        CK(cudaFuncGetAttributes(&fa, ts_tma<T, MODE, false, CPW>));
+        CK(cudaFuncSetAttribute(ts_tma<T, MODE, false, CPW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                optin - (int)fa.sharedSizeBytes));
+        configured = optin - (int)fa.sharedSizeBytes;
+    }
+    if ((int)L.total > configured) throw ConfigError("TMA projection: shared-memory ring too large");
+    const long ntile = padded_rows(n) / TR;
+    const int grid = (int)std::max(1L, std::min<long>(ntile, (long)c.sms));
+    ts_tma<T, MODE, false, CPW><<<grid, TMA_THREADS, L.total, c.s>>>(Krb, C, n, ntile, L, x, xo, cin, c.red(), out, r,
+                                                                     p, s, y, st);
+    c.check_launch();
+}
+
+template <class T, int MODE>
+void ts_tma_launch(Ctx& c, const T* Krb, int C, long n, const T* x, T* xo, const double* cin, double* out,
+                   T* r = nullptr, T* p = nullptr, T* s = nullptr, T* y = nullptr, CGState* st = nullptr) {
+    if (C > 128) throw ConfigError("TMA projection limited to 128 columns");
+    if (MODE == 2) {
+        ts_tma_inst<T, 2, 1>(c, Krb, C, n, x, xo, cin, out, r, p, s, y, st);
+        return;
+    }
+    const int cpw = (C + 7) / 8;
+    if (cpw <= 1)
+        ts_tma_inst<T, MODE, 1>(c, Krb, C, n, x, xo, cin, out, r, p, s, y, st);
+    else if (cpw <= 2)
+        ts_tma_inst<T, MODE, 2>(c, Krb, C, n, x, xo, cin, out, r, p, s, y, st);
+    else if (cpw <= 4)
+        ts_tma_inst<T, MODE, 4>(c, Krb, C, n, x, xo, cin, out, r, p, s, y, st);
+    else if (cpw <= 6)
+        ts_tma_inst<T, MODE, 6>(c, Krb, C, n, x, xo, cin, out, r, p, s, y, st);
+    else if (cpw <= 8)
+        ts_tma_inst<T, MODE, 8>(c, Krb, C, n, x, xo, cin, out, r, p, s, y, st);
+    else if (cpw <= 10)
+        ts_tma_inst<T, MODE, 10>(c, Krb, C, n, x, xo, cin, out, r, p, s, y, st);
+    else if (cpw <= 12)
+        ts_tma_inst<T, MODE, 12>(c, Krb, C, n, x, xo, cin, out, r, p, s, y, st);
+    else
+        ts_tma_inst<T, MODE, 16>(c, Krb, C, n, x, xo, cin, out, r, p, s, y, st);
 }
 
 // nrm[0] = ||x||^2, nrm[1..W] = x^T x
@@ -399,7 +472,7 @@ struct SolveOut {
 };
 
 template <class T> struct Workspace {
-    DevBuf r, w, p, s, y, tmp, vec;
+    DevBuf r, w, p, s, y, tmp, vec, krb;
     void ensure(long n) {
         const size_t b = sizeof(T) * n;
         r.ensure(b);
@@ -420,17 +493,20 @@ SolveOut recycled_cg(Ctx& c, DevOp& op, const T* U, const T* K, long ncol, const
                      double rhs_scale, T* g, T* y_out, T* image, Workspace<T>& ws, bool want_hist) {
     constexpr int W = Sc<T>::W;
     const long n = op.n();
-    ws.ensure(n);
+    const long npad = padded_rows(n);
+    ws.ensure(npad);
     T* r = ws.r.template as<T>();
     T* w = ws.w.template as<T>();
     T* p = ws.p.template as<T>();
     T* s = ws.s.template as<T>();
-    T* y = y_out;
+    T* y = ws.y.template as<T>();
     double* e = c.sc(0);
     double* c1 = c.sc(1);
     double* c2 = c.sc(2);
     double* nrm = c.sc(3);
     if (ncol > 1024) throw ConfigError("recycle space wider than 1024 columns");
+    CK(cudaMemsetAsync(r, 0, sizeof(T) * npad, c.s));
+    CK(cudaMemsetAsync(w, 0, sizeof(T) * npad, c.s));
     // r0 = P rhs (CGS2), e = K^T rhs
     if (ncol > 0) {
         cgs2<T, false>(c, K, n, ncol, rhs, r, n, e, c1, c2);
@@ -445,9 +521,9 @@ SolveOut recycled_cg(Ctx& c, DevOp& op, const T* U, const T* K, long ncol, const
         c.sync();
         scale = std::sqrt(h);
     }
-    CK(cudaMemsetAsync(y, 0, sizeof(T) * n, c.s));
-    CK(cudaMemsetAsync(p, 0, sizeof(T) * n, c.s));
-    CK(cudaMemsetAsync(s, 0, sizeof(T) * n, c.s));
+    CK(cudaMemsetAsync(y, 0, sizeof(T) * npad, c.s));
+    CK(cudaMemsetAsync(p, 0, sizeof(T) * npad, c.s));
+    CK(cudaMemsetAsync(s, 0, sizeof(T) * npad, c.s));
     CGState init{};
     init.scale = scale;
     init.tol = tol;
@@ -458,7 +534,20 @@ SolveOut recycled_cg(Ctx& c, DevOp& op, const T* U, const T* K, long ncol, const
     CK(cudaMemcpyAsync(st, &c.st_host[0], sizeof(CGState), cudaMemcpyHostToDevice, c.s));
     CK(cudaStreamSynchronize(c.s));  // st_host slot reused below
 
-    const dim3 grid_st = stencil_grid(op.d, 1);
+    // stencil+dots: (32 x 8) x-y tiles marching over kz planes, ~8 blocks per SM
+    dim3 grid_st = stencil_grid(op.d, 1);
+    int kz = 1;
+    while ((long)grid_st.x * grid_st.y * ((op.d.N2 + kz - 1) / kz) > 8L * c.sms && kz < op.d.N2) kz *= 2;
+    grid_st.z = (unsigned)((op.d.N2 + kz - 1) / kz);
+    // row-blocked copy of K for the inner-iteration kernels (contiguous 32-row tiles)
+    const T* Kit = K;
+    if (ncol > 0) {
+        ws.krb.ensure(sizeof(T) * npad * ncol);
+        repack_rb<T><<<c.grid_for(npad * ncol, 256, 8), 256, 0, c.s>>>(K, n, (int)ncol, n, ws.krb.template as<T>(),
+                                                                      npad);
+        c.check_launch();
+        Kit = ws.krb.template as<T>();
+    }
     const size_t smem_c = sizeof(double) * W * std::max(1L, ncol);
     const int batch = n < 200000 ? 16 : 8;
     long batches = 0;
@@ -468,21 +557,26 @@ SolveOut recycled_cg(Ctx& c, DevOp& op, const T* U, const T* K, long ncol, const
             const bool samp = c.prof && b == 0;
             const long iter = batches * batch;
             cudaEvent_t e0 = samp ? c.prof_start() : nullptr;
-            cg_stencil_dots<T><<<grid_st, 256, 0, c.s>>>(op.d, r, w, st, c.hist.template as<double>(), c.red());
+            cg_stencil_dots<T><<<grid_st, 256, 0, c.s>>>(op.d, r, w, st, c.hist.template as<double>(), c.red(), kz);
             c.check_launch();
             if (samp) c.prof_stop(e0, 0, n * (2 * es + 16.0), iter);
             if (ncol > 0) {
                 cudaEvent_t e1 = samp ? c.prof_start() : nullptr;
-                ts_T_launch<T, false>(c, K, n, ncol, w, n, c1, st);
+                ts_tma_launch<T, 0>(c, Kit, (int)ncol, n, w, nullptr, nullptr, c1, nullptr, nullptr, nullptr, nullptr,
+                                    st);
                 if (samp) c.prof_stop(e1, 1, n * es * (ncol + 1.0), iter);
                 cudaEvent_t e2 = samp ? c.prof_start() : nullptr;
-                ts_NT_launch<T, false>(c, K, n, ncol, w, w, n, c1, c2, st);
+                ts_tma_launch<T, 1>(c, Kit, (int)ncol, n, w, w, c1, c2, nullptr, nullptr, nullptr, nullptr, st);
                 if (samp) c.prof_stop(e2, 2, n * es * (ncol + 2.0), iter);
+                cudaEvent_t e3 = samp ? c.prof_start() : nullptr;
+                ts_tma_launch<T, 2>(c, Kit, (int)ncol, n, w, nullptr, c2, nullptr, r, p, s, y, st);
+                if (samp) c.prof_stop(e3, 3, n * es * (ncol + 9.0), iter);
+            } else {
+                cudaEvent_t e3 = samp ? c.prof_start() : nullptr;
+                cg_update<T, false><<<c.grid_for(n, 256, 8), 256, smem_c, c.s>>>(Kit, n, 0, w, n, c2, r, p, s, y, st);
+                c.check_launch();
+                if (samp) c.prof_stop(e3, 3, n * es * 9.0, iter);
             }
-            cudaEvent_t e3 = samp ? c.prof_start() : nullptr;
-            cg_update<T><<<c.grid_for(n, 256, 8), 256, smem_c, c.s>>>(K, n, (int)ncol, w, n, c2, r, p, s, y, st);
-            c.check_launch();
-            if (samp) c.prof_stop(e3, 3, n * es * (ncol + 9.0), iter);
         }
         ++batches;
     };
@@ -517,6 +611,8 @@ SolveOut recycled_cg(Ctx& c, DevOp& op, const T* U, const T* K, long ncol, const
         out.hist.resize(m);
         CK(cudaMemcpy(out.hist.data(), c.hist.p, sizeof(double) * m, cudaMemcpyDeviceToHost));
     }
+    CK(cudaMemcpyAsync(y_out, y, sizeof(T) * n, cudaMemcpyDeviceToDevice, c.s));
+    y = y_out;
     // image = A y ; g = y + U (e - K^T image)
     launch_stencil<T>(c, op.d, y, n, nullptr, image, n, 1);
     if (ncol > 0) {

@@ -1,0 +1,216 @@
+// TMA-pipelined recycle-space projection kernels for the inner iteration.
+//
+// The per-RHS recycle basis K (n x C) is kept in the row-blocked layout
+// (kaddr<true>), so a tile of TR consecutive rows x all C columns is ONE
+// contiguous chunk of TR*C elements. A persistent CTA per SM runs a producer
+// warp that streams tiles with 1D bulk TMA copies (cp.async.bulk + mbarrier
+// complete_tx) into an S-stage shared-memory ring (~160 KB in flight per SM,
+// what HBM3e needs at ~3 us loaded latency), and 8 consumer warps that compute
+// from shared memory:
+//
+//   MODE 0  c   = op(K)^T x                          (first CGS pass)
+//   MODE 1  x'  = x - K c1 ; c2 = op(K)^T x'         (fused second CGS pass)
+//   MODE 2  q   = w' - K c2 ; p = r + beta p ; s = q + beta s ;
+//           y  += alpha p ; r -= alpha s             (CG/COCG update)
+//
+// Rows >= n are zero padding of K and of the x workspace. Reductions are the
+// deterministic per-block partial + last-block sum of common.cuh.
+#pragma once
+
+#include "common.cuh"
+#include "kernels.cuh"
+
+namespace rd {
+
+constexpr int TMA_CONSUMERS = 256;  // 8 warps
+constexpr int TMA_THREADS = TMA_CONSUMERS + 32;
+
+__device__ __forceinline__ void consumer_sync() { asm volatile("bar.sync 1, 256;" ::: "memory"); }
+
+struct TmaLayout {
+    int TR, S, NV;
+    uint32_t tile_bytes, x_bytes;
+    uint32_t off_k, off_x, off_part, off_xs, off_cw, off_vals, off_bar, total;
+};
+
+template <class T> __host__ __device__ inline TmaLayout tma_layout(int C, int TR, int S, int NV) {
+    TmaLayout L;
+    L.TR = TR;
+    L.S = S;
+    L.NV = NV;
+    const uint32_t es = sizeof(T);
+    L.tile_bytes = (uint32_t)TR * C * es;
+    L.x_bytes = (uint32_t)TR * es;
+    auto al = [](uint32_t v) { return (v + 127u) & ~127u; };
+    uint32_t o = 0;
+    L.off_k = o;
+    o += al(L.tile_bytes) * S;
+    L.off_x = o;
+    o += al(L.x_bytes) * S * NV;
+    const int G = TMA_CONSUMERS / TR > 0 ? TMA_CONSUMERS / TR : 1;
+    L.off_part = o;
+    o += al((uint32_t)G * TR * es);
+    L.off_xs = o;
+    o += al((uint32_t)TR * es);
+    L.off_cw = o;
+    o += al((uint32_t)(C > 0 ? C : 1) * es);
+    L.off_vals = o;
+    o += al((uint32_t)(C > 0 ? C : 1) * 2 * sizeof(double));
+    L.off_bar = o;
+    o += 2 * S * 8;
+    L.total = o;
+    return L;
+}
+
+template <class T, int MODE, bool HERM, int CPW>
+__global__ void __launch_bounds__(TMA_THREADS, 1)
+    ts_tma(const T* __restrict__ Krb, int C, long n, long ntile, TmaLayout L, const T* __restrict__ x,
+           T* __restrict__ xo, const double* __restrict__ cin, GridRed red, double* out, T* __restrict__ r,
+           T* __restrict__ p, T* __restrict__ s, T* __restrict__ y, CGState* st) {
+    if (st && st->done) return;
+    constexpr int W = Sc<T>::W;
+    extern __shared__ __align__(128) unsigned char smem[];
+    const int TR = L.TR, S = L.S;
+    const uint32_t stride_k = (L.tile_bytes + 127u) & ~127u;
+    const uint32_t stride_x = (L.x_bytes + 127u) & ~127u;
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + L.off_bar);
+    uint64_t* empty = full + S;
+    T* part = reinterpret_cast<T*>(smem + L.off_part);
+    T* xs2 = reinterpret_cast<T*>(smem + L.off_xs);
+    T* cw = reinterpret_cast<T*>(smem + L.off_cw);
+    double* vals = reinterpret_cast<double*>(smem + L.off_vals);
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    if (tid == 0) {
+        for (int i = 0; i < S; ++i) {
+            mbar_init(&full[i], 1);
+            mbar_init(&empty[i], TMA_CONSUMERS / 32);
+        }
+        fence_mbar_init();
+    }
+    if (MODE != 0)
+        for (int t = tid; t < C; t += blockDim.x) cw[t] = Sc<T>::get(cin + (size_t)t * W);
+    __syncthreads();
+
+    if (wid == TMA_CONSUMERS / 32) {
+        // ---------------- producer warp: one elected lane streams tiles ----------------
+        if (lane == 0) {
+            long k = 0;
+            for (long t = blockIdx.x; t < ntile; t += gridDim.x, ++k) {
+                const int stage = (int)(k % S);
+                const uint32_t use = (uint32_t)(k / S);
+                mbar_wait(&empty[stage], (use & 1u) ^ 1u);
+                mbar_arrive_expect_tx(&full[stage], L.tile_bytes + L.NV * L.x_bytes);
+                tma_load_1d(smem + L.off_k + stage * stride_k, Krb + (size_t)t * TR * C, L.tile_bytes, &full[stage]);
+                unsigned char* xb = smem + L.off_x + (size_t)stage * L.NV * stride_x;
+                tma_load_1d(xb, x + (size_t)t * TR, L.x_bytes, &full[stage]);
+                if (MODE == 2) {
+                    tma_load_1d(xb + 1 * stride_x, r + (size_t)t * TR, L.x_bytes, &full[stage]);
+                    tma_load_1d(xb + 2 * stride_x, p + (size_t)t * TR, L.x_bytes, &full[stage]);
+                    tma_load_1d(xb + 3 * stride_x, s + (size_t)t * TR, L.x_bytes, &full[stage]);
+                    tma_load_1d(xb + 4 * stride_x, y + (size_t)t * TR, L.x_bytes, &full[stage]);
+                }
+            }
+        }
+    } else {
+        // ---------------- consumer warps ----------------
+        const int G = TMA_CONSUMERS / TR > 0 ? TMA_CONSUMERS / TR : 1;
+        const int j0 = wid * CPW;
+        int ncol = C - j0;
+        if (ncol > CPW) ncol = CPW;
+        T acc[CPW];
+#pragma unroll
+        for (int jj = 0; jj < CPW; ++jj) acc[jj] = Sc<T>::zero();
+        T alpha = Sc<T>::zero(), beta = Sc<T>::zero();
+        if (MODE == 2) {
+            alpha = ld2<T>(st->alpha);
+            beta = ld2<T>(st->beta);
+        }
+        long k = 0;
+        for (long t = blockIdx.x; t < ntile; t += gridDim.x, ++k) {
+            const int stage = (int)(k % S);
+            const uint32_t use = (uint32_t)(k / S);
+            mbar_wait(&full[stage], use & 1u);
+            const T* Ks = reinterpret_cast<const T*>(smem + L.off_k + stage * stride_k);
+            const unsigned char* xb = smem + L.off_x + (size_t)stage * L.NV * stride_x;
+            const T* Xs = reinterpret_cast<const T*>(xb);
+            const long row0 = t * TR;
+            const T* xsrc = Xs;
+            if (MODE != 0) {
+                // N part: row r = tid % TR, column group g = tid / TR
+                if (tid < G * TR) {
+                    const int rr = tid % TR, g = tid / TR;
+                    const T* kr = Ks + (size_t)(rr >> 5) * 32 * C + (rr & 31);
+                    T pa = Sc<T>::zero();
+                    for (int j = g; j < C; j += G) pa = Sc<T>::fma(kr[(size_t)j * 32], cw[j], pa);
+                    part[g * TR + rr] = pa;
+                }
+                consumer_sync();
+                if (tid < TR) {
+                    T sum = part[tid];
+                    for (int g = 1; g < G; ++g) sum = Sc<T>::add(sum, part[g * TR + tid]);
+                    const long row = row0 + tid;
+                    const T q = Sc<T>::sub(Xs[tid], sum);
+                    if (MODE == 1) {
+                        if (row < n) xo[row] = q;
+                        xs2[tid] = row < n ? q : Sc<T>::zero();
+                    } else if (row < n) {
+                        const T rv = reinterpret_cast<const T*>(xb + 1 * stride_x)[tid];
+                        const T pv = reinterpret_cast<const T*>(xb + 2 * stride_x)[tid];
+                        const T sv = reinterpret_cast<const T*>(xb + 3 * stride_x)[tid];
+                        const T yv = reinterpret_cast<const T*>(xb + 4 * stride_x)[tid];
+                        const T pn = Sc<T>::fma(beta, pv, rv);
+                        const T sn = Sc<T>::fma(beta, sv, q);
+                        p[row] = pn;
+                        s[row] = sn;
+                        y[row] = Sc<T>::fma(alpha, pn, yv);
+                        r[row] = Sc<T>::sub(rv, Sc<T>::mul(alpha, sn));
+                    }
+                }
+                if (MODE == 1) consumer_sync();
+                xsrc = xs2;
+            }
+            if (MODE != 2) {
+                // T part: warp w owns columns [j0, j0 + CPW), lanes over the TR rows
+                for (int rb = 0; rb < TR / 32; ++rb) {
+                    const T xv = xsrc[rb * 32 + lane];
+                    const T* kb = Ks + (size_t)rb * 32 * C + lane;
+#pragma unroll
+                    for (int jj = 0; jj < CPW; ++jj)
+                        if (jj < ncol) acc[jj] = opfma<T, HERM>(kb[(size_t)(j0 + jj) * 32], xv, acc[jj]);
+                }
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&empty[stage]);
+        }
+        if (MODE != 2) {
+#pragma unroll
+            for (int jj = 0; jj < CPW; ++jj) {
+                double a[W];
+                if constexpr (W == 1) {
+                    a[0] = (double&)acc[jj];
+                } else {
+                    a[0] = ((cplx&)acc[jj]).x;
+                    a[1] = ((cplx&)acc[jj]).y;
+                }
+#pragma unroll
+                for (int q = 0; q < W; ++q) {
+                    const double v = warp_sum(a[q]);
+                    if (lane == 0 && jj < ncol) vals[(j0 + jj) * W + q] = v;
+                }
+            }
+        }
+    }
+    if (MODE == 2) {
+        if (blockIdx.x == 0 && tid == 0) {
+            st->gamma_prev = st->gamma;
+            st->alpha_prev = st->alpha;
+            st->it = st->it + 1;
+        }
+        return;
+    }
+    __syncthreads();
+    if (!grid_commit(red, vals, C * W)) return;
+    grid_finish(red, C * W, out);
+}
+
+}  // namespace rd
