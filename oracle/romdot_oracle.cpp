@@ -703,6 +703,8 @@ inline RecycledResult<double> recycled_minres(const LinOp<double>& A, const Recy
 // the operator image (the two projections per step of krylov.cpp:161-166).
 // Convergence: ||rhs - A g|| / rhs_scale <= tol, as in krylov.cpp:159.
 // g = y + U (K^T rhs - K^T A y) solves A g = rhs over Range([U, Krylov]).
+constexpr int kCgStagnationWindow = 1000;
+
 template <class T>
 RecycledResult<T> recycled_cg(const LinOp<T>& A, const RecycleSpace<T>& rs, const T* rhs, double tol,
                               long maxit, double rhs_scale) {
@@ -766,10 +768,13 @@ RecycledResult<T> recycled_cg(const LinOp<T>& A, const RecycleSpace<T>& rs, cons
                 rep.converged = true;
                 break;
             }
+            // CG residual norms are not monotone (Galerkin, not minimal residual):
+            // the reference's 50-step MINRES window (krylov.cpp:79-84) would stop CG
+            // while its residual is still rising on ill-conditioned 3D grids.
             if (relres < best * (1.0 - 1e-12)) {
                 best = relres;
                 stagnant = 0;
-            } else if (++stagnant >= 50) {
+            } else if (++stagnant >= kCgStagnationWindow) {
                 break;
             }
         }

@@ -258,10 +258,11 @@ __global__ void __launch_bounds__(256) cg_stencil_dots(OpDev op, const T* __rest
             st->done = 1;
             return;
         }
+        // CG residuals are not monotone: 1000-step window (the reference's 50 is for MINRES)
         if (relres < st->best * (1.0 - 1e-12)) {
             st->best = relres;
             st->stagnant = 0;
-        } else if (++st->stagnant >= 50) {
+        } else if (++st->stagnant >= 1000) {
             st->done = 1;
             return;
         }

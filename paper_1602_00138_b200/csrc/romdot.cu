@@ -8,6 +8,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <stdexcept>
@@ -32,6 +33,25 @@ struct CudaError : std::runtime_error {
 };
 
 static thread_local std::string g_err;
+
+// ROMDOT_VERBOSE=1 prints solver progress to stderr (host-side, no device syncs added).
+static int verbose() {
+    static int v = -1;
+    if (v < 0) {
+        const char* e = std::getenv("ROMDOT_VERBOSE");
+        v = e ? std::atoi(e) : 0;
+    }
+    return v;
+}
+#define VLOG(lvl, ...)                           \
+    do {                                         \
+        if (verbose() >= (lvl)) {                \
+            std::fprintf(stderr, "[romdot] ");   \
+            std::fprintf(stderr, __VA_ARGS__);   \
+            std::fprintf(stderr, "\n");          \
+            std::fflush(stderr);                 \
+        }                                        \
+    } while (0)
 
 #define CK(x)                                                                                        \
     do {                                                                                             \
@@ -698,7 +718,7 @@ static void jacobi_eig(long m, std::vector<double>& T, std::vector<double>& Z) {
 // to 1e-12 (no sparse factorisation on the GPU). Ritz check every max(k,10)
 // steps against tol * lambda_max (Gershgorin).
 static void smallest_eigenpairs_dev(Ctx& c, DevOp& op, long k, double tol, std::vector<double>& lam, double* Uout,
-                                    double inner_tol = 1e-12) {
+                                    double inner_tol = 1e-10) {
     const long n = op.n();
     if (k < 1 || k > n) throw ConfigError("eigensolver: k out of range");
     if (!(op.lam_max > 0.0)) {
@@ -784,7 +804,11 @@ static void smallest_eigenpairs_dev(Ctx& c, DevOp& op, long k, double tol, std::
                                                                        make_double2(1.0, 0.0), au);
             c.check_launch();
             launch_norms<double>(c, au, n, nrm);
-            if (std::sqrt(host1(nrm)) > tol * lam_max) return false;
+            const double res = std::sqrt(host1(nrm));
+            if (res > tol * lam_max) {
+                VLOG(1, "lanczos: ritz pair %ld residual %.3e > %.3e (lambda %.6e)", i, res, tol * lam_max, li);
+                return false;
+            }
         }
         lam = lm;
         CK(cudaMemcpyAsync(Uout, U, sizeof(double) * n * k, cudaMemcpyDeviceToDevice, c.s));
@@ -794,8 +818,10 @@ static void smallest_eigenpairs_dev(Ctx& c, DevOp& op, long k, double tol, std::
     const long check_every = std::max(k, 10L);
     while (m < n) {
         grow(m + 1);
-        recycled_cg<double>(c, op, nullptr, nullptr, 0, V(m), inner_tol, 2 * n, 0.0, w, ybuf.template as<double>(),
-                            ibuf.template as<double>(), ws, false);
+        SolveOut so = recycled_cg<double>(c, op, nullptr, nullptr, 0, V(m), inner_tol, std::min(2 * n, 200000L), 0.0, w,
+                                          ybuf.template as<double>(), ibuf.template as<double>(), ws, false);
+        VLOG(2, "lanczos step %ld: inner CG %d its, relres %.3e, converged %d", m, so.iterations, so.final_relres,
+             (int)so.converged);
         ts_T_launch<double, false>(c, V(m), n, 1, w, n, nrm + 16);
         const double alpha = host1(nrm + 16);
         vec_axpby<double><<<c.grid_for(n, 256, 8), 256, 0, c.s>>>(n, make_double2(-alpha, 0.0), V(m),
@@ -830,7 +856,12 @@ static void smallest_eigenpairs_dev(Ctx& c, DevOp& op, long k, double tol, std::
             grow(m + 1);
             CK(cudaMemcpyAsync(V(m), w, sizeof(double) * n, cudaMemcpyDeviceToDevice, c.s));
         }
-        if ((m % check_every == 0 || m == n) && ritz()) return;
+        if (m % check_every == 0 || m == n) {
+            const bool ok = ritz();
+            VLOG(1, "lanczos: ritz check at m=%ld -> %s", m, ok ? "converged" : "not yet");
+            if (ok) return;
+        }
+        if (m >= 8 * k + 200) throw SolverError("eigensolver: Lanczos did not converge within 8k+200 steps");
     }
     if (ritz()) return;
     throw SolverError("eigensolver: Lanczos did not converge");
@@ -1149,6 +1180,8 @@ void process_system(DevBasis<T>& gb, DevOp& op, long nrhs, const long* bidx, con
     const long n = gb.n;
     if (maxit <= 0) maxit = 2 * n;
     gb.refresh(op);
+    VLOG(1, "system %d: refresh done (cols %ld, block %ld seq %ld second-pass %ld)", system_index, gb.cols,
+         gb.stats_block_refresh, gb.stats_seq_refresh, gb.stats_second_pass);
     long cspace = 1;
     for (const auto& sp : gb.spaces) cspace = std::max(cspace, (long)sp.size() + 1);
     gb.factor_eig_block(op, cspace);
@@ -1207,6 +1240,8 @@ void process_system(DevBasis<T>& gb, DevOp& op, long nrhs, const long* bidx, con
         T zero = Sc<T>::zero();
         CK(cudaMemcpyAsync(b + bi, &zero, sizeof(T), cudaMemcpyHostToDevice, c.s));
         c.sync();
+        VLOG(2, "system %d rhs %ld: init_relres %.3e its %d appended %d cols %ld", system_index, j, row.init_relres,
+             row.iterations, (int)row.appended, gb.cols);
         log.push_back(row);
     }
 }
@@ -1544,6 +1579,7 @@ int rd_initial_solutions(rd_op* o, int dtype, long nrhs, const long* bidx, const
                 if (!so.converged)
                     throw rd::SolverError("init_basis: CG failed on initial solution column " + std::to_string(j));
                 tot += so.iterations;
+                VLOG(2, "X0 column %ld: %d its", j, so.iterations);
             }
         };
         if (dtype == 0)
