@@ -287,6 +287,7 @@ def main():
     ctx.profile(True)
     solves = its_tot = zeros = 0
     barrier()
+    torch.cuda.nvtx.range_push("timed")
     with ClockSampler(local) as clk:
         ctx.mark()
         for i in range(args.warmup, args.warmup + args.steps):
@@ -297,6 +298,7 @@ def main():
             its_tot += its
         ctx.mark()
         barrier()
+    torch.cuda.nvtx.range_pop()
     t_val_ms = ctx.elapsed_ms()
     launches = ctx.launches - launches0
     prof = ctx.prof()

@@ -47,9 +47,8 @@ template <class T> __host__ __device__ inline TmaLayout tma_layout(int C, int TR
     o += al(L.tile_bytes) * S;
     L.off_x = o;
     o += al(L.x_bytes) * S * NV;
-    const int G = TMA_CONSUMERS / TR > 0 ? TMA_CONSUMERS / TR : 1;
     L.off_part = o;
-    o += al((uint32_t)G * TR * es);
+    o += al((uint32_t)2 * (TR / 32) * 8 * 32 * es);
     L.off_xs = o;
     o += al((uint32_t)TR * es);
     L.off_cw = o;
@@ -113,7 +112,6 @@ __global__ void __launch_bounds__(TMA_THREADS, 1)
         }
     } else {
         // ---------------- consumer warps ----------------
-        const int G = TMA_CONSUMERS / TR > 0 ? TMA_CONSUMERS / TR : 1;
         const int j0 = wid * CPW;
         int ncol = C - j0;
         if (ncol > CPW) ncol = CPW;
@@ -134,49 +132,65 @@ __global__ void __launch_bounds__(TMA_THREADS, 1)
             const unsigned char* xb = smem + L.off_x + (size_t)stage * L.NV * stride_x;
             const T* Xs = reinterpret_cast<const T*>(xb);
             const long row0 = t * TR;
-            const T* xsrc = Xs;
-            if (MODE != 0) {
-                // N part: row r = tid % TR, column group g = tid / TR
-                if (tid < G * TR) {
-                    const int rr = tid % TR, g = tid / TR;
-                    const T* kr = Ks + (size_t)(rr >> 5) * 32 * C + (rr & 31);
-                    T pa = Sc<T>::zero();
-                    for (int j = g; j < C; j += G) pa = Sc<T>::fma(kr[(size_t)j * 32], cw[j], pa);
-                    part[g * TR + rr] = pa;
-                }
-                consumer_sync();
-                if (tid < TR) {
-                    T sum = part[tid];
-                    for (int g = 1; g < G; ++g) sum = Sc<T>::add(sum, part[g * TR + tid]);
-                    const long row = row0 + tid;
-                    const T q = Sc<T>::sub(Xs[tid], sum);
-                    if (MODE == 1) {
-                        if (row < n) xo[row] = q;
-                        xs2[tid] = row < n ? q : Sc<T>::zero();
-                    } else if (row < n) {
-                        const T rv = reinterpret_cast<const T*>(xb + 1 * stride_x)[tid];
-                        const T pv = reinterpret_cast<const T*>(xb + 2 * stride_x)[tid];
-                        const T sv = reinterpret_cast<const T*>(xb + 3 * stride_x)[tid];
-                        const T yv = reinterpret_cast<const T*>(xb + 4 * stride_x)[tid];
-                        const T pn = Sc<T>::fma(beta, pv, rv);
-                        const T sn = Sc<T>::fma(beta, sv, q);
-                        p[row] = pn;
-                        s[row] = sn;
-                        y[row] = Sc<T>::fma(alpha, pn, yv);
-                        r[row] = Sc<T>::sub(rv, Sc<T>::mul(alpha, sn));
-                    }
-                }
-                if (MODE == 1) consumer_sync();
-                xsrc = xs2;
-            }
-            if (MODE != 2) {
+            const int RBN = TR >> 5;
+            if (MODE == 0) {
                 // T part: warp w owns columns [j0, j0 + CPW), lanes over the TR rows
-                for (int rb = 0; rb < TR / 32; ++rb) {
-                    const T xv = xsrc[rb * 32 + lane];
+                for (int rb = 0; rb < RBN; ++rb) {
+                    const T xv = Xs[rb * 32 + lane];
                     const T* kb = Ks + (size_t)rb * 32 * C + lane;
 #pragma unroll
                     for (int jj = 0; jj < CPW; ++jj)
                         if (jj < ncol) acc[jj] = opfma<T, HERM>(kb[(size_t)(j0 + jj) * 32], xv, acc[jj]);
+                }
+            } else {
+                // N part on the same (column-block x lane) mapping: every warp forms the
+                // partial row sums of its own columns; one barrier per tile (the partial
+                // buffer alternates with the tile parity).
+                T* pb = part + (size_t)(k & 1) * RBN * 8 * 32;
+                for (int rb = 0; rb < RBN; ++rb) {
+                    const T* kb = Ks + (size_t)rb * 32 * C + lane;
+                    T pa = Sc<T>::zero();
+#pragma unroll
+                    for (int jj = 0; jj < CPW; ++jj)
+                        if (jj < ncol) pa = Sc<T>::fma(kb[(size_t)(j0 + jj) * 32], cw[j0 + jj], pa);
+                    pb[(rb * 8 + wid) * 32 + lane] = pa;
+                }
+                consumer_sync();
+                if (MODE == 1) {
+                    for (int rb = 0; rb < RBN; ++rb) {
+                        T sum = pb[(rb * 8) * 32 + lane];
+#pragma unroll
+                        for (int w2 = 1; w2 < 8; ++w2) sum = Sc<T>::add(sum, pb[(rb * 8 + w2) * 32 + lane]);
+                        const long row = row0 + rb * 32 + lane;
+                        T q = Sc<T>::sub(Xs[rb * 32 + lane], sum);
+                        if (row >= n) q = Sc<T>::zero();
+                        if (wid == (rb & 7) && row < n) xo[row] = q;
+                        const T* kb = Ks + (size_t)rb * 32 * C + lane;
+#pragma unroll
+                        for (int jj = 0; jj < CPW; ++jj)
+                            if (jj < ncol) acc[jj] = opfma<T, HERM>(kb[(size_t)(j0 + jj) * 32], q, acc[jj]);
+                    }
+                } else {
+                    for (int rb = wid; rb < RBN; rb += 8) {
+                        T sum = pb[(rb * 8) * 32 + lane];
+#pragma unroll
+                        for (int w2 = 1; w2 < 8; ++w2) sum = Sc<T>::add(sum, pb[(rb * 8 + w2) * 32 + lane]);
+                        const int rr = rb * 32 + lane;
+                        const long row = row0 + rr;
+                        if (row < n) {
+                            const T q = Sc<T>::sub(Xs[rr], sum);
+                            const T rv = reinterpret_cast<const T*>(xb + 1 * stride_x)[rr];
+                            const T pv = reinterpret_cast<const T*>(xb + 2 * stride_x)[rr];
+                            const T sv = reinterpret_cast<const T*>(xb + 3 * stride_x)[rr];
+                            const T yv = reinterpret_cast<const T*>(xb + 4 * stride_x)[rr];
+                            const T pn = Sc<T>::fma(beta, pv, rv);
+                            const T sn = Sc<T>::fma(beta, sv, q);
+                            p[row] = pn;
+                            s[row] = sn;
+                            y[row] = Sc<T>::fma(alpha, pn, yv);
+                            r[row] = Sc<T>::sub(rv, Sc<T>::mul(alpha, sn));
+                        }
+                    }
                 }
             }
             __syncwarp();
