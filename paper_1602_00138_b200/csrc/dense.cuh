@@ -298,3 +298,111 @@ __global__ void __launch_bounds__(256) col_norms(const T* __restrict__ X, long l
 }
 
 }  // namespace rd
+
+namespace rd {
+
+// Greedy pivoted Cholesky of the Hermitian PSD Gram G (m x m, ld m), the
+// column-pivoted QR pivot rule (largest residual column norm first).
+// Stops when the largest remaining residual d_max <= stop_abs2 or when
+// d_max <= rel_band * d0 (d0 = largest diagonal of this call).
+// Outputs: piv[0..nsel), rdiag[0..nsel) = sqrt(d at pick), Rrow (mmax x m):
+// Rrow[k*m + i] = R(k, i) (pivot-order row k, original column i).
+// info[0] = nsel, info[1] = d_max remaining, info[2] = 1 if stopped by stop_abs2.
+template <class T>
+__global__ void __launch_bounds__(1024) pivoted_chol(const T* __restrict__ G, int m, double stop_abs2, double rel_band,
+                                                     int* piv, double* rdiag, T* Rrow, double* info) {
+    extern __shared__ double sh[];
+    double* d = sh;                           // m residual norms^2
+    int* picked = reinterpret_cast<int*>(d + m);  // m flags
+    __shared__ double s_best[32];
+    __shared__ int s_bi[32];
+    __shared__ int s_p;
+    __shared__ double s_dp, s_d0;
+    __shared__ int s_stop;
+    for (int i = threadIdx.x; i < m; i += blockDim.x) {
+        d[i] = Sc<T>::real(G[(size_t)i * m + i]);
+        picked[i] = 0;
+    }
+    __syncthreads();
+    int k = 0;
+    for (; k < m; ++k) {
+        // argmax over unpicked (deterministic: lowest index wins ties)
+        double best = -1.0;
+        int bi = m;
+        for (int i = threadIdx.x; i < m; i += blockDim.x)
+            if (!picked[i] && (d[i] > best || (d[i] == best && i < bi))) {
+                best = d[i];
+                bi = i;
+            }
+        for (int o = 16; o > 0; o >>= 1) {
+            const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+            const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+            if (ob > best || (ob == best && oi < bi)) {
+                best = ob;
+                bi = oi;
+            }
+        }
+        if ((threadIdx.x & 31) == 0) {
+            s_best[threadIdx.x >> 5] = best;
+            s_bi[threadIdx.x >> 5] = bi;
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            double b = -1.0;
+            int ii = m;
+            for (int w = 0; w < (int)(blockDim.x >> 5); ++w)
+                if (s_best[w] > b || (s_best[w] == b && s_bi[w] < ii)) {
+                    b = s_best[w];
+                    ii = s_bi[w];
+                }
+            if (k == 0) s_d0 = b;
+            s_stop = 0;
+            if (ii >= m || b <= stop_abs2) s_stop = 2;
+            else if (b <= rel_band * s_d0) s_stop = 1;
+            s_p = ii;
+            s_dp = b;
+            info[1] = b;
+            if (!s_stop) {
+                piv[k] = ii;
+                rdiag[k] = sqrt(b);
+                picked[ii] = 1;
+            }
+        }
+        __syncthreads();
+        if (s_stop) {
+            if (threadIdx.x == 0) info[2] = s_stop == 2 ? 1.0 : 0.0;
+            break;
+        }
+        const int p = s_p;
+        const double rkk = sqrt(s_dp);
+        // row k: R(k, i) = (G(p, i) - sum_{l<k} conj(R(l, p)) R(l, i)) / R(k, k)
+        for (int i = threadIdx.x; i < m; i += blockDim.x) {
+            T v = Sc<T>::zero();
+            if (i == p) {
+                v = Sc<T>::from(rkk);
+            } else if (!picked[i]) {
+                T sum = G[(size_t)i * m + p];  // G(p, i) column-major
+                for (int l = 0; l < k; ++l)
+                    sum = Sc<T>::sub(sum, Sc<T>::cmul(Rrow[(size_t)l * m + p], Rrow[(size_t)l * m + i]));
+                v = Sc<T>::scale(sum, 1.0 / rkk);
+                d[i] -= Sc<T>::abs2(v);
+            }
+            Rrow[(size_t)k * m + i] = v;
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) info[0] = k;
+}
+
+// Scale column j of X (n x c, ld) by 1/sqrt(nrm2[j]) (nrm2 = squared norms); zero columns untouched.
+template <class T>
+__global__ void scale_columns(T* X, long ld, int c, long n, const double* nrm2) {
+    const int j = blockIdx.y;
+    if (j >= c) return;
+    const double s = nrm2[j] > 0.0 ? 1.0 / sqrt(nrm2[j]) : 1.0;
+    T* xc = X + (size_t)j * ld;
+    for (long i = blockIdx.x * (long)blockDim.x + threadIdx.x; i < n; i += (long)gridDim.x * blockDim.x)
+        xc[i] = Sc<T>::scale(xc[i], s);
+}
+
+}  // namespace rd

@@ -1246,6 +1246,150 @@ void process_system(DevBasis<T>& gb, DevOp& op, long nrhs, const long* bidx, con
     }
 }
 
+
+// ------------------------------------------------------------------ RRQR ---
+// Rank-revealing compression of the candidate basis (BASELINE RRQR, the
+// reference's truncation rule at acceptance.cpp:378-383): column-pivoted QR
+// computed as recursive block-pivoted CholQR on the device.
+//   level: G = Z^H Z (device Gram) -> greedy pivoted Cholesky on the device
+//   (pivot = largest residual column norm, the QRCP rule) accepting pivots
+//   within 8 decades of the level's largest residual norm^2 -> Q_P =
+//   CholQR2(Z_P) -> Z_rest <- (I - Q_P Q_P^H)^2 Z_rest (explicit BCGS2) ->
+//   next level on the deflated columns. The explicit deflation keeps every
+//   level's Gram accurate relative to its own scale, so residual norms down
+//   to ~1e-14 of the first are resolved (the Gram alone stops near 1e-8).
+// rank = #{R_kk > tol * R_00}; Q (n x rank) spans the retained columns.
+template <class T>
+long rrqr_dev(Ctx& c, long n, long m, const T* A, double tol, bool normalize, std::vector<long>& perm,
+              std::vector<double>& rdiag_out, DevBuf& Qout) {
+    constexpr int W = Sc<T>::W;
+    const long ld = n;
+    DevBuf Z, Zb, G, Sp, Sinv, Rrow, pivd, rdg, infod, work, tmp, nrm;
+    Z.ensure(sizeof(T) * n * std::max(1L, m));
+    CK(cudaMemcpyAsync(Z.p, A, sizeof(T) * n * m, cudaMemcpyDeviceToDevice, c.s));
+    nrm.ensure(sizeof(double) * std::max(1L, m));
+    if (normalize && m > 0) {
+        for (long j0 = 0; j0 < m; j0 += 1024) {
+            const long cc = std::min(1024L, m - j0);
+            col_norms<T><<<c.grid_for(n, 256, 2), 256, sizeof(double) * cc, c.s>>>(Z.template as<T>() + j0 * ld, ld,
+                                                                                   (int)cc, n, c.red(),
+                                                                                   nrm.template as<double>() + j0);
+            c.check_launch();
+        }
+        scale_columns<T><<<dim3(c.grid_for(n, 256, 1), (unsigned)m), 256, 0, c.s>>>(Z.template as<T>(), ld, (int)m, n,
+                                                                                   nrm.template as<double>());
+        c.check_launch();
+    }
+    Qout.ensure(sizeof(T) * n * std::max(1L, m));
+    std::vector<long> remaining(m);
+    for (long j = 0; j < m; ++j) remaining[j] = j;
+    perm.clear();
+    rdiag_out.clear();
+    double r00 = -1.0;
+    long rank = 0;
+    bool done = false;
+    int level = 0;
+    while (!done && !remaining.empty()) {
+        const long mr = (long)remaining.size();
+        G.ensure(sizeof(T) * mr * mr);
+        gram<T, true>(c, Z.template as<T>(), ld, mr, Z.template as<T>(), ld, mr, n, G.template as<T>(), true, work);
+        Rrow.ensure(sizeof(T) * mr * mr);
+        pivd.ensure(sizeof(int) * mr);
+        rdg.ensure(sizeof(double) * mr);
+        infod.ensure(sizeof(double) * 4);
+        const double stop_abs2 = r00 > 0.0 ? (tol * r00) * (tol * r00) : 0.0;
+        const size_t shm = sizeof(double) * mr + sizeof(int) * mr;
+        if (shm > 200 * 1024) throw ConfigError("rrqr: candidate basis too wide");
+        CK(cudaFuncSetAttribute(pivoted_chol<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+        pivoted_chol<T><<<1, 1024, shm, c.s>>>(G.template as<T>(), (int)mr, stop_abs2, 1e-8, pivd.template as<int>(),
+                                               rdg.template as<double>(), Rrow.template as<T>(),
+                                               infod.template as<double>());
+        c.check_launch();
+        double info[3];
+        CK(cudaMemcpyAsync(info, infod.p, sizeof(info), cudaMemcpyDeviceToHost, c.s));
+        c.sync();
+        const long nsel = (long)info[0];
+        std::vector<int> piv(nsel);
+        std::vector<double> rdl(nsel);
+        if (nsel) {
+            CK(cudaMemcpy(piv.data(), pivd.p, sizeof(int) * nsel, cudaMemcpyDeviceToHost));
+            CK(cudaMemcpy(rdl.data(), rdg.p, sizeof(double) * nsel, cudaMemcpyDeviceToHost));
+        }
+        if (r00 < 0.0) r00 = nsel ? rdl[0] : 0.0;
+        // accept pivots above the rank threshold
+        long keep = 0;
+        while (keep < nsel && rdl[keep] > tol * r00) ++keep;
+        for (long k = 0; k < keep; ++k) {
+            perm.push_back(remaining[piv[k]]);
+            rdiag_out.push_back(rdl[k]);
+        }
+        if (keep < nsel || info[2] > 0.5 || nsel == 0) done = true;
+        if (keep > 0) {
+            // Z_P (gathered, pivot order) -> Q_P = Z_P S_PP^-1, then a CholQR pass
+            Zb.ensure(sizeof(T) * n * keep);
+            T* ZP = Zb.template as<T>();
+            for (long k = 0; k < keep; ++k)
+                CK(cudaMemcpyAsync(ZP + k * ld, Z.template as<T>() + (long)piv[k] * ld, sizeof(T) * n,
+                                   cudaMemcpyDeviceToDevice, c.s));
+            // S_PP (keep x keep upper) from Rrow rows restricted to the picked columns
+            std::vector<T> Rh((size_t)keep * mr);
+            CK(cudaMemcpy(Rh.data(), Rrow.p, sizeof(T) * keep * mr, cudaMemcpyDeviceToHost));
+            std::vector<T> S((size_t)keep * keep, Sc<T>::zero());
+            for (long kk = 0; kk < keep; ++kk)
+                for (long i = 0; i <= kk; ++i) S[i + kk * keep] = Rh[(size_t)i * mr + piv[kk]];
+            Sp.ensure(sizeof(T) * keep * keep);
+            Sinv.ensure(sizeof(T) * keep * keep);
+            CK(cudaMemcpyAsync(Sp.p, S.data(), sizeof(T) * keep * keep, cudaMemcpyHostToDevice, c.s));
+            tri_inv_upper<T><<<1, 1024, 0, c.s>>>(Sp.template as<T>(), Sinv.template as<T>(), (int)keep);
+            c.check_launch();
+            T* QP = Qout.template as<T>() + rank * ld;
+            gemm<T, false>(c, ZP, ld, keep, Sinv.template as<T>(), keep, nullptr, 0, QP, ld, n, true);
+            for (int pass = 0; pass < 2; ++pass) {  // CholQR2 clean-up of Q_P
+                gram<T, true>(c, QP, ld, keep, QP, ld, keep, n, Sp.template as<T>(), true, work);
+                CholInfo ci = chol_inv<T, true>(c, Sp.template as<T>(), Sinv.template as<T>(), keep, false);
+                if (ci.bad) throw SolverError("rrqr: CholQR of the pivot block failed");
+                gemm<T, false>(c, QP, ld, keep, Sinv.template as<T>(), keep, nullptr, 0, ZP, ld, n, true);
+                CK(cudaMemcpyAsync(QP, ZP, sizeof(T) * n * keep, cudaMemcpyDeviceToDevice, c.s));
+            }
+            rank += keep;
+        }
+        // remaining columns (not picked at this level), compacted
+        std::vector<char> pk(mr, 0);
+        for (long k = 0; k < keep; ++k) pk[piv[k]] = 1;
+        std::vector<long> rest;
+        std::vector<long> rest_local;
+        for (long i = 0; i < mr; ++i)
+            if (!pk[i]) {
+                rest.push_back(remaining[i]);
+                rest_local.push_back(i);
+            }
+        if (done || rest.empty()) {
+            for (long v : rest) perm.push_back(v);
+            break;
+        }
+        for (long t = 0; t < (long)rest_local.size(); ++t)
+            if (rest_local[t] != t)
+                CK(cudaMemcpyAsync(Z.template as<T>() + t * ld, Z.template as<T>() + rest_local[t] * ld, sizeof(T) * n,
+                                   cudaMemcpyDeviceToDevice, c.s));
+        const long nr = (long)rest.size();
+        // Z_rest <- (I - Q Q^H)^2 Z_rest against every retained direction so far
+        tmp.ensure(sizeof(T) * rank * nr);
+        for (int pass = 0; pass < 2; ++pass) {
+            gram<T, true>(c, Qout.template as<T>(), ld, rank, Z.template as<T>(), ld, nr, n, tmp.template as<T>(), false,
+                          work);
+            gemm<T, true>(c, Qout.template as<T>(), ld, rank, tmp.template as<T>(), nr, Z.template as<T>(), ld,
+                          Z.template as<T>(), ld, n, false);
+        }
+        remaining = rest;
+        ++level;
+        if (level > 64) throw SolverError("rrqr: too many levels");
+    }
+    for (long j = 0; j < m; ++j)
+        if (std::find(perm.begin(), perm.end(), j) == perm.end()) perm.push_back(j);
+    (void)W;
+    return rank;
+}
+
 }  // namespace rd
 
 // ================================================================ C ABI ===
@@ -1800,20 +1944,27 @@ int rd_smallest_eigenpairs(rd_op* op, long k, double tol, double* lambda, void* 
 
 int rd_rrqr(rd_ctx* ctx, int dtype, long n, long m, const void* A, double tol, int normalize, long* rank, long* perm,
             double* rdiag, void* Q, int where) {
-    (void)ctx;
-    (void)dtype;
-    (void)n;
-    (void)m;
-    (void)A;
-    (void)tol;
-    (void)normalize;
-    (void)rank;
-    (void)perm;
-    (void)rdiag;
-    (void)Q;
-    (void)where;
-    g_err = "rd_rrqr: not built yet";
-    return 1;
+    return guard([&] {
+        Ctx& cx = ctx->c;
+        const size_t es = esize(dtype);
+        Staged As(cx, A, es * n * m, where);
+        std::vector<long> pv;
+        std::vector<double> rd_;
+        DevBuf Qd;
+        long rk = 0;
+        if (dtype == 0)
+            rk = rrqr_dev<double>(cx, n, m, (const double*)As.p, tol, normalize != 0, pv, rd_, Qd);
+        else
+            rk = rrqr_dev<cplx>(cx, n, m, (const cplx*)As.p, tol, normalize != 0, pv, rd_, Qd);
+        *rank = rk;
+        for (long j = 0; j < m; ++j) perm[j] = pv[j];
+        for (long j = 0; j < m; ++j) rdiag[j] = j < (long)rd_.size() ? rd_[j] : 0.0;
+        if (Q && rk > 0) {
+            const auto kind = where == 1 ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost;
+            CK(cudaMemcpyAsync(Q, Qd.p, es * n * rk, kind, cx.s));
+        }
+        cx.sync();
+    });
 }
 
 }  // extern "C"

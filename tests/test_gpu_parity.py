@@ -209,3 +209,49 @@ def test_device_eigen_seed_matches_oracle(rd, cfg):
         r = A.apply(U[:, i]) - lam[i] * U[:, i]
         assert np.linalg.norm(r) <= 1e-8 * lm
     assert np.linalg.norm(U.T @ U - np.eye(c.k)) <= 1e-7
+
+
+@pytest.mark.parametrize("m,want", [(64, 64), (256, 219)])
+def test_rrqr_known_rank_decay_09(rd, m, want):
+    """C5 RRQR shape at small n: A = Q diag(0.9^j) P (seeded permutation),
+    rank at 1e-10 is 64 / 219; same rank and R diagonal as the
+    oracle's Householder QRCP."""
+    rng = np.random.default_rng(3)
+    n = 4000
+    Q, _ = np.linalg.qr(rng.standard_normal((n, m)))
+    A = (Q * (0.9 ** np.arange(m)))[:, rng.permutation(m)]
+    rk, perm, rdiag, Qg = rd.rrqr(A, 1e-10, normalize=False)
+    ro, permo, rdo, Qo = orc.qrcp(A, 1e-10, normalize=False)
+    assert rk == want == ro
+    assert np.allclose(rdiag[:rk], rdo[:rk], rtol=1e-6)
+    assert np.linalg.norm(Qg.T @ Qg - np.eye(rk)) <= 1e-12
+    # principal angles between retained spaces
+    s = np.linalg.svd(Qo.T @ Qg, compute_uv=False)
+    assert np.sqrt(max(0.0, 1.0 - s.min() ** 2)) <= 1e-6
+
+
+@pytest.mark.parametrize("cplx", [False, True])
+def test_rrqr_candidate_basis_matches_oracle(rd, cplx):
+    """Compression of a real build's candidate basis (column-normalised, App. A9):
+    identical rank to the oracle QRCP and the same retained span on sigma >= 1e-6."""
+    c = P.CONFIGS["T2c" if cplx else "T2"]
+    g, lay = c.grid, c.layout()
+    U0, X0 = _shared_seed(c, g, lay)
+    gb = orc.GlobalBasis(U0, X0, c.cap)
+    for s, (pt, w) in enumerate(c.systems(), start=1):
+        orc.process_system(gb, orc.Operator.grid(g, c.fields(pt, w), c.dtype), lay, c.tol, s)
+    V = gb.V
+    rk, perm, rdiag, Qg = rd.rrqr(V, 1e-10, normalize=True)
+    ro, permo, rdo, Qo = orc.qrcp(V, 1e-10, normalize=True)
+    assert rk == ro
+    # pivot order is not unique here (every normalised column starts tied at norm 1),
+    # so R diagonals differ between valid QRCP runs; rank and span are the invariants
+    assert rdiag[0] == pytest.approx(1.0) and np.all(rdiag[:rk] > 1e-10)
+    assert np.linalg.norm(Qg.conj().T @ Qg - np.eye(rk)) <= 1e-10
+    # angles restricted to the well-determined part of the spectrum (App. C.1)
+    Un, sn, _ = np.linalg.svd(V / np.linalg.norm(V, axis=0), full_matrices=False)
+    keep = sn >= 1e-6 * sn[0]
+    Ut = Un[:, keep]
+    for Qx in (Qg, Qo):
+        s = np.linalg.svd(Qx.conj().T @ Ut, compute_uv=False)
+        assert np.sqrt(max(0.0, 1.0 - s.min() ** 2)) <= 1e-6
