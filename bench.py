@@ -149,6 +149,22 @@ def cpu_sample(cfg: P.ProblemConfig, width: int, mean_its: float, iters: int = 6
                       "global check/append excluded"}
 
 
+def aggregate_replicas(dist, device, solves, t_ms, e2e_ms=None):
+    """Replicas only: whole-job solves = sum over ranks, time =
+    max over ranks (device-timed). Returns (solves_all, t_max_ms, e2e_max_ms)."""
+    import torch
+    t = torch.tensor([float(t_ms)], device=device, dtype=torch.float64)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    s = torch.tensor([float(solves)], device=device, dtype=torch.float64)
+    dist.all_reduce(s)
+    te = None
+    if e2e_ms is not None:
+        e = torch.tensor([float(e2e_ms)], device=device, dtype=torch.float64)
+        dist.all_reduce(e, op=dist.ReduceOp.MAX)
+        te = float(e.item())
+    return int(round(s.item())), float(t.item()), te
+
+
 def log(*a):
     print("[bench]", *a, file=sys.stderr, flush=True)
 
@@ -330,19 +346,12 @@ def main():
                "d2h_bytes_per_step": n * nrhs * es + nrhs * 5 * 8, "ms": t_e2e_ms}
 
     # ---- multi-rank aggregation (replicas) ---------------------------------
-    t_max = t_val_ms
-    solves_all = solves
+    t_max, solves_all = t_val_ms, solves
     if dist is not None:
-        t = torch.tensor([t_val_ms], device=f"cuda:{local}", dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        t_max = float(t.item())
-        s = torch.tensor([solves], device=f"cuda:{local}", dtype=torch.float64)
-        dist.all_reduce(s)
-        solves_all = int(s.item())
+        solves_all, t_max, te = aggregate_replicas(dist, f"cuda:{local}", solves, t_val_ms,
+                                                   e2e["ms"] if e2e is not None else None)
         if e2e is not None:
-            te = torch.tensor([e2e["ms"]], device=f"cuda:{local}", dtype=torch.float64)
-            dist.all_reduce(te, op=dist.ReduceOp.MAX)
-            e2e["value"] = solves_all / (float(te.item()) / 1e3)
+            e2e["value"] = solves_all / (te / 1e3)
     value = solves_all / (t_max / 1e3) if t_max > 0 else 0.0
 
     # ---- roofline from the live samples ------------------------------------

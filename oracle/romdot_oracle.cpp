@@ -7,10 +7,10 @@
 // reference legs. Nothing in the product package (paper_1602_00138_b200/)
 // links, loads or calls it.
 //
-// Parity status: the reference cannot be compiled here (Eigen 3 and the
-// vendored doctest/CLI11 are absent), and it ships no golden
-// vectors. This restatement is pinned by porting the reference's own property
-// tests (test_krylov.cpp, test_basis.cpp, test_grid.cpp, acceptance.cpp C1/C4/
+// PARITY UNPINNED (by golden vectors): the reference cannot be compiled here
+// (Eigen 3 and the vendored doctest/CLI11 are absent) and it
+// ships no golden vectors or fixtures. This restatement is instead pinned by
+// porting the reference's own property tests (test_krylov.cpp, test_basis.cpp, test_grid.cpp, acceptance.cpp C1/C4/
 // C7/C8) to tests/test_oracle_*.py, plus independent scipy cross-checks.
 //
 // Faithful parts (reduce exactly to the reference for 2D / constant D /
