@@ -297,14 +297,16 @@ constexpr int TS_WARPS = 8;
 // FMAs wait until all loads of the batch have been issued (ILP, not one load
 // in flight per thread).
 template <class T> __device__ __forceinline__ T ldg_nc(const T* p);
+// Coherent (L2) loads: these kernels may write another column of the same
+// allocation in place, so the non-coherent texture path is not used.
 template <> __device__ __forceinline__ double ldg_nc<double>(const double* p) {
     double v;
-    asm volatile("ld.global.nc.f64 %0, [%1];" : "=d"(v) : "l"(p));
+    asm volatile("ld.global.cg.f64 %0, [%1];" : "=d"(v) : "l"(p));
     return v;
 }
 template <> __device__ __forceinline__ cplx ldg_nc<cplx>(const cplx* p) {
     cplx v;
-    asm volatile("ld.global.nc.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "l"(p));
+    asm volatile("ld.global.cg.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "l"(p));
     return v;
 }
 template <class T> __device__ __forceinline__ void reg_fence(T& v);
@@ -685,6 +687,29 @@ __global__ void __launch_bounds__(256) op_gershgorin(OpDev op, GridRed red, doub
         for (unsigned q = 0; q < gridDim.x * gridDim.y; ++q) b = fmax(b, __ldcg(red.partials + q));
         out[0] = b;
         *red.counter = 0u;
+    }
+}
+
+// out[i + j*ldo] = sgn * op(K[idx[j], col0 + i]) * val[j]  (i < ncols, j < nrhs): the
+// coordinates K^op b_j of single-nonzero right-hand sides, for many RHS at once.
+template <class T, bool HERM>
+__global__ void row_gather_multi(const T* __restrict__ K, long ldk, int col0, int ncols, const long* __restrict__ idx,
+                                 const double* __restrict__ val, int nrhs, double sgn, T* __restrict__ out, long ldo) {
+    const long tot = (long)ncols * nrhs;
+    for (long e = blockIdx.x * (long)blockDim.x + threadIdx.x; e < tot; e += (long)gridDim.x * blockDim.x) {
+        const int i = (int)(e % ncols), j = (int)(e / ncols);
+        const T k = K[(size_t)(col0 + i) * ldk + idx[j]];
+        out[(size_t)j * ldo + i] = opmul<T, HERM>(k, Sc<T>::from(sgn * val[j]));
+    }
+}
+
+// R[idx[j] + j*ldr] += val[j]
+template <class T>
+__global__ void scatter_add_rhs(T* R, long ldr, const long* __restrict__ idx, const double* __restrict__ val, int nrhs) {
+    const int j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (j < nrhs) {
+        T& v = R[(size_t)j * ldr + idx[j]];
+        v = Sc<T>::add(v, Sc<T>::from(val[j]));
     }
 }
 

@@ -61,6 +61,19 @@ static int verbose() {
                             std::to_string(__LINE__));                                               \
     } while (0)
 
+// ROMDOT_VERBOSE>=3: bitwise-sensitive checksum of a device buffer (debug of
+// determinism; copies to host, slow).
+template <class T> static void dbg_sum(const char* tag, const T* p, long count, cudaStream_t s) {
+    if (verbose() < 3 || !p || count <= 0) return;
+    std::vector<T> h(count);
+    cudaStreamSynchronize(s);
+    cudaMemcpy(h.data(), p, sizeof(T) * count, cudaMemcpyDeviceToHost);
+    unsigned long long x = 1469598103934665603ull;
+    const unsigned char* b = reinterpret_cast<const unsigned char*>(h.data());
+    for (size_t i = 0; i < sizeof(T) * (size_t)count; ++i) x = (x ^ b[i]) * 1099511628211ull;
+    std::fprintf(stderr, "[romdot-sum] %s %016llx\n", tag, x);
+}
+
 template <class T> constexpr int dt_of();
 template <> constexpr int dt_of<double>() { return 0; }
 template <> constexpr int dt_of<cplx>() { return 1; }
@@ -72,15 +85,32 @@ struct DevBuf {
     DevBuf() = default;
     DevBuf(const DevBuf&) = delete;
     DevBuf& operator=(const DevBuf&) = delete;
+    // cudaFree does not wait for work queued on the library's non-blocking
+    // stream: a buffer is only released after the device has drained, so a
+    // kernel still in flight never reads freed (and possibly reused) memory.
     ~DevBuf() {
-        if (p) cudaFree(p);
+        if (p) {
+            cudaDeviceSynchronize();
+            cudaFree(p);
+        }
     }
     void ensure(size_t b) {
         if (b <= bytes) return;
-        if (p) CK(cudaFree(p));
+        if (p) {
+            CK(cudaDeviceSynchronize());
+            CK(cudaFree(p));
+        }
         p = nullptr;
         CK(cudaMalloc(&p, b));
         bytes = b;
+        // ROMDOT_POISON=1: fill fresh allocations with NaN bytes so any read of
+        // unwritten device memory surfaces as a NaN (debug aid; sanitizers are
+        // not available on the GPU pool).
+        static const int poison = [] {
+            const char* e = std::getenv("ROMDOT_POISON");
+            return e ? std::atoi(e) : 0;
+        }();
+        if (poison) CK(cudaMemset(p, 0xFF, b));
     }
     template <class T> T* as() const { return static_cast<T*>(p); }
 };
@@ -580,7 +610,17 @@ SolveOut recycled_cg(Ctx& c, DevOp& op, const T* U, const T* K, long ncol, const
             cg_stencil_dots<T><<<grid_st, 256, 0, c.s>>>(op.d, r, w, st, c.hist.template as<double>(), c.red(), kz);
             c.check_launch();
             if (samp) c.prof_stop(e0, 0, n * (2 * es + 16.0), iter);
-            if (ncol > 0) {
+            static const int no_tma = [] {
+                const char* e = std::getenv("ROMDOT_NO_TMA");
+                return e ? std::atoi(e) : 0;
+            }();
+            if (ncol > 0 && no_tma) {
+                ts_T_launch<T, false, true>(c, Kit, ncol, ncol, w, n, c1, st);
+                ts_NT_launch<T, false, true>(c, Kit, ncol, ncol, w, w, n, c1, c2, st);
+                cg_update<T, true><<<c.grid_for(n, 256, 8), 256, smem_c, c.s>>>(Kit, ncol, (int)ncol, w, n, c2, r, p,
+                                                                                s, y, st);
+                c.check_launch();
+            } else if (ncol > 0) {
                 cudaEvent_t e1 = samp ? c.prof_start() : nullptr;
                 ts_tma_launch<T, 0>(c, Kit, (int)ncol, n, w, nullptr, nullptr, c1, nullptr, nullptr, nullptr, nullptr,
                                     st);
@@ -1111,16 +1151,22 @@ template <class T> struct DevBasis : BasisBase {
         for (long t = 0; t < m; ++t)
             CK(cudaMemcpyAsync(Ut + (size_t)t * n, Vp() + (size_t)cidx[ku + t] * n, sizeof(T) * n,
                                cudaMemcpyDeviceToDevice, c.s));
+        dbg_sum(" frs stencil", Kt, n * m, c.s);
         if (ku > 0) {
             T* C1 = (T*)c.sc(4);
             T* C2 = (T*)c.sc(5);
             if (ku * m * W > 8192) throw ConfigError("recycle space: trailing block too wide");
             gram<T, false>(c, Kb, n, ku, Kt, n, m, n, C1, false, gwork);
+            dbg_sum(" frs C1", C1, ku * m, c.s);
             gemm<T, true>(c, Kb, n, ku, C1, m, Kt, n, Kt, n, n, false);
+            dbg_sum(" frs Kt1", Kt, n * m, c.s);
             gram<T, false>(c, Kb, n, ku, Kt, n, m, n, C2, false, gwork);
+            dbg_sum(" frs C2", C2, ku * m, c.s);
             gemm<T, true>(c, Kb, n, ku, C2, m, Kt, n, Kt, n, n, false);
+            dbg_sum(" frs Kt2", Kt, n * m, c.s);
             launch_addsub(c, (int)(ku * m * W), (double*)C1, (double*)C2, 1.0, (double*)C1);
             gemm<T, true>(c, Ub, n, ku, C1, m, Ut, n, Ut, n, n, false);
+            dbg_sum(" frs Ut", Ut, n * m, c.s);
         }
         double* coef = c.sc(6);
         double* nrm = c.sc(7);
@@ -1131,7 +1177,10 @@ template <class T> struct DevBasis : BasisBase {
                 cgs2<T, false>(c, Kt, n, t, kt, kt, n, coef, c.sc(4), c.sc(5));
                 ts_N_launch<T>(c, Ut, n, t, ut, ut, n, coef);
             }
+            dbg_sum(" frs cgs kt", kt, n, c.s);
+            dbg_sum(" frs coef", coef, 2 * t, c.s);
             launch_norms<T>(c, kt, n, nrm);
+            dbg_sum(" frs nrm", nrm, 3, c.s);
             launch_scale<T>(c, kt, kt, n, nrm, 1);
             launch_scale<T>(c, ut, ut, n, nrm, 1);
         }
@@ -1176,7 +1225,6 @@ void process_system(DevBasis<T>& gb, DevOp& op, long nrhs, const long* bidx, con
                     int system_index, long maxit, T* Xdev, std::vector<LogRow>& log, long& inner_its,
                     long& appends) {
     Ctx& c = *gb.ctx;
-    constexpr int W = Sc<T>::W;
     const long n = gb.n;
     if (maxit <= 0) maxit = 2 * n;
     gb.refresh(op);
@@ -1184,68 +1232,117 @@ void process_system(DevBasis<T>& gb, DevOp& op, long nrhs, const long* bidx, con
          gb.stats_block_refresh, gb.stats_seq_refresh, gb.stats_second_pass);
     long cspace = 1;
     for (const auto& sp : gb.spaces) cspace = std::max(cspace, (long)sp.size() + 1);
+    dbg_sum("refresh K", gb.Kp(), gb.n * gb.cols, c.s);
+    dbg_sum("refresh W", gb.Wp(), gb.n * gb.cols, c.s);
     gb.factor_eig_block(op, cspace);
+    dbg_sum("eig Kr", gb.Kr.template as<T>(), gb.n * gb.ku, c.s);
+    dbg_sum("eig Ur", gb.Ur.template as<T>(), gb.n * gb.ku, c.s);
     log.clear();
     inner_its = 0;
     appends = 0;
-    gb.bvec.ensure(sizeof(T) * n);
-    gb.tmpv2.ensure(sizeof(T) * n);
-    T* b = gb.bvec.template as<T>();
-    T* rj = gb.tmpv2.template as<T>();
-    CK(cudaMemsetAsync(b, 0, sizeof(T) * n, c.s));
-    DevBuf wbuf, ybuf, gbuf, imbuf;
+    // ---- batched global check (basis.cpp:171-172 for every RHS at once) ----
+    // b_j = val_j e_{idx_j}: K_old^H B is a row gather; R_all = B - K_old K_old^H B
+    // is one tall GEMM per system; per RHS only the columns appended during the
+    // system are projected out of R_all[:, j].
+    const long r0 = gb.cols;
+    DevBuf idxd, vald, Wc, Rall, Coef, Cpk, rjbuf, wn, ybuf, gbuf, imbuf;
+    idxd.ensure(sizeof(long) * nrhs);
+    vald.ensure(sizeof(double) * nrhs);
+    CK(cudaMemcpyAsync(idxd.p, bidx, sizeof(long) * nrhs, cudaMemcpyHostToDevice, c.s));
+    CK(cudaMemcpyAsync(vald.p, bval, sizeof(double) * nrhs, cudaMemcpyHostToDevice, c.s));
+    Rall.ensure(sizeof(T) * n * nrhs);
+    if (r0 > 0) {
+        Wc.ensure(sizeof(T) * r0 * nrhs);
+        row_gather_multi<T, true><<<c.grid_for(r0 * nrhs, 256, 4), 256, 0, c.s>>>(
+            gb.Kp(), n, 0, (int)r0, idxd.template as<long>(), vald.template as<double>(), (int)nrhs, -1.0,
+            Wc.template as<T>(), r0);
+        c.check_launch();
+        gemm<T, false>(c, gb.Kp(), n, r0, Wc.template as<T>(), nrhs, nullptr, 0, Rall.template as<T>(), n, n, false);
+    } else {
+        CK(cudaMemsetAsync(Rall.p, 0, sizeof(T) * n * nrhs, c.s));
+    }
+    scatter_add_rhs<T><<<(int)((nrhs + 127) / 128), 128, 0, c.s>>>(Rall.template as<T>(), n, idxd.template as<long>(),
+                                                                   vald.template as<double>(), (int)nrhs);
+    c.check_launch();
+    dbg_sum("Rall", Rall.template as<T>(), n * nrhs, c.s);
+    // deferred solution assembly X = G + W Coef (solve_projected, basis.cpp:110-112)
+    const long capc = std::max(gb.capcols, r0 + nrhs + 1);
+    if (Xdev) {
+        Coef.ensure(sizeof(T) * capc * nrhs);
+        CK(cudaMemsetAsync(Coef.p, 0, sizeof(T) * capc * nrhs, c.s));
+    }
+    rjbuf.ensure(sizeof(T) * n);
+    wn.ensure(sizeof(T) * (nrhs + 8));
     ybuf.ensure(sizeof(T) * n);
     gbuf.ensure(sizeof(T) * n);
     imbuf.ensure(sizeof(T) * n);
     for (long j = 0; j < nrhs; ++j) {
-        const long bi = bidx[j];
-        const double bv = bval[j];
-        T bval_t = Sc<T>::from(bv);
-        CK(cudaMemcpyAsync(b + bi, &bval_t, sizeof(T), cudaMemcpyHostToDevice, c.s));
-        const double bnorm = std::fabs(bv);
-        const long r = gb.cols;
-        wbuf.ensure(sizeof(double) * W * std::max(1L, r) + 64);
-        double* w = wbuf.template as<double>();
-        gb.coords_single(bi, bv, w);
-        // r_j = b - K w
-        ts_N_launch<T>(c, gb.Kp(), n, r, b, rj, n, w);
+        const double bnorm = std::fabs(bval[j]);
+        const long rcur = gb.cols;
+        const T* rhs = Rall.template as<T>() + (size_t)j * n;
+        if (rcur > r0) {  // project out this system's appended columns
+            wn.ensure(sizeof(T) * (rcur - r0));
+            row_gather_multi<T, true><<<c.grid_for(rcur - r0, 256, 1), 256, 0, c.s>>>(
+                gb.Kp(), n, (int)r0, (int)(rcur - r0), idxd.template as<long>() + j, vald.template as<double>() + j, 1,
+                1.0, wn.template as<T>(), rcur - r0);
+            c.check_launch();
+            ts_N_launch<T>(c, gb.Kp() + (size_t)r0 * n, n, rcur - r0, rhs, rjbuf.template as<T>(), n,
+                           (const double*)wn.p);
+            rhs = rjbuf.template as<T>();
+        }
         double* nrm = c.sc(3);
-        launch_norms<T>(c, rj, n, nrm);
+        launch_norms<T>(c, rhs, n, nrm);
         double h;
         CK(cudaMemcpyAsync(&h, nrm, sizeof(double), cudaMemcpyDeviceToHost, c.s));
+        if (Xdev) {  // Coef[:rcur, j] = -K^H b_j (negated for the final Y - X M GEMM)
+            row_gather_multi<T, true><<<c.grid_for(rcur, 256, 1), 256, 0, c.s>>>(
+                gb.Kp(), n, 0, (int)rcur, idxd.template as<long>() + j, vald.template as<double>() + j, 1, -1.0,
+                Coef.template as<T>() + (size_t)j * capc, capc);
+            c.check_launch();
+        }
         c.sync();
         LogRow row{system_index, (int)j, std::sqrt(h) / bnorm, 0, false};
-        T* Xj = Xdev ? Xdev + (size_t)j * n : gbuf.template as<T>();
+        T* Gj = Xdev ? Xdev + (size_t)j * n : gbuf.template as<T>();
         if (row.init_relres <= tol) {
-            CK(cudaMemsetAsync(gbuf.p, 0, sizeof(T) * n, c.s));
-            ts_N_launch<T>(c, gb.Wp(), n, r, gbuf.template as<T>(), Xj, n, w, -1.0);  // X_j = W w
+            if (Xdev) CK(cudaMemsetAsync(Gj, 0, sizeof(T) * n, c.s));
         } else {
             auto& idx = gb.spaces[j];
             const long cj = (long)idx.size();
+            dbg_sum("rhs", rhs, n, c.s);
             gb.factor_rhs_space(op, idx);
-            SolveOut so = recycled_cg<T>(c, op, gb.Ur.template as<T>(), gb.Kr.template as<T>(), cj, rj, kInnerSafety * tol, maxit,
-                                         bnorm, gbuf.template as<T>(), ybuf.template as<T>(), imbuf.template as<T>(), gb.ws, false);
+            dbg_sum("space K", gb.Kr.template as<T>(), n * cj, c.s);
+            dbg_sum("space U", gb.Ur.template as<T>(), n * cj, c.s);
+            SolveOut so = recycled_cg<T>(c, op, gb.Ur.template as<T>(), gb.Kr.template as<T>(), cj, rhs,
+                                         kInnerSafety * tol, maxit, bnorm, Gj, ybuf.template as<T>(),
+                                         imbuf.template as<T>(), gb.ws, false);
             if (!so.converged)
                 throw SolverError("process_system: correction solve failed at system " +
                                   std::to_string(system_index) + ", rhs " + std::to_string(j));
-            ts_N_launch<T>(c, gb.Wp(), n, r, gbuf.template as<T>(), Xj, n, w, -1.0);  // X_j = g + W w
             row.iterations = so.iterations;
             inner_its += so.iterations;
+            dbg_sum("y", ybuf.template as<T>(), n, c.s);
+            dbg_sum("image", imbuf.template as<T>(), n, c.s);
             if (gb.append(ybuf.template as<T>(), imbuf.template as<T>(), kColCorrection)) {
                 idx.push_back((int)(gb.cols - 1));
                 row.appended = true;
                 ++appends;
+                dbg_sum("appended K col", gb.Kp() + (size_t)(gb.cols - 1) * n, n, c.s);
+                dbg_sum("appended W col", gb.Wp() + (size_t)(gb.cols - 1) * n, n, c.s);
             }
         }
-        T zero = Sc<T>::zero();
-        CK(cudaMemcpyAsync(b + bi, &zero, sizeof(T), cudaMemcpyHostToDevice, c.s));
-        c.sync();
         VLOG(2, "system %d rhs %ld: init_relres %.3e its %d appended %d cols %ld", system_index, j, row.init_relres,
              row.iterations, (int)row.appended, gb.cols);
         log.push_back(row);
     }
+    if (Xdev && gb.cols > 0) {
+        const long rf = gb.cols;
+        Cpk.ensure(sizeof(T) * rf * nrhs);
+        CK(cudaMemcpy2DAsync(Cpk.p, sizeof(T) * rf, Coef.p, sizeof(T) * capc, sizeof(T) * rf, nrhs,
+                             cudaMemcpyDeviceToDevice, c.s));
+        gemm<T, true>(c, gb.Wp(), n, rf, Cpk.template as<T>(), nrhs, Xdev, n, Xdev, n, n, false);
+    }
+    c.sync();
 }
-
 
 // ------------------------------------------------------------------ RRQR ---
 // Rank-revealing compression of the candidate basis (BASELINE RRQR, the

@@ -255,3 +255,30 @@ def test_rrqr_candidate_basis_matches_oracle(rd, cplx):
     for Qx in (Qg, Qo):
         s = np.linalg.svd(Qx.conj().T @ Ut, compute_uv=False)
         assert np.sqrt(max(0.0, 1.0 - s.min() ** 2)) <= 1e-6
+
+
+def test_build_deterministic_across_interleaved_builds(rd):
+    """Bitwise reproducibility (test_basis.cpp:210-223) must survive other builds
+    running in between (allocation reuse, cache state): T2c built 4 times with T3c
+    builds interleaved gives identical BuildLogs and V."""
+    c = P.CONFIGS["T2c"]
+    g, lay = c.grid, c.layout()
+    U0, X0 = _shared_seed(c, g, lay)
+    c3 = P.CONFIGS["T3c"]
+    z3 = _shared_seed(c3, c3.grid, c3.layout())
+
+    def build(cfg, U, X):
+        gb = rd.GlobalBasis(U, X, cfg.cap)
+        rows = []
+        for s, (pt, w) in enumerate(cfg.systems(), start=1):
+            pr = rd.process_system(gb, rd.SchurOperator(cfg.grid, cfg.fields(pt, w), cfg.dtype), cfg.layout(),
+                                   cfg.tol, s)
+            rows += [(r.init_relres, r.iterations, r.appended) for r in pr.log]
+        return rows, gb.V
+
+    ref_rows, ref_V = build(c, U0, X0)
+    for rep in range(3):
+        build(c3, *z3)
+        rows, V = build(c, U0, X0)
+        assert rows == ref_rows
+        assert V.tobytes() == ref_V.tobytes()
