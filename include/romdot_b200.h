@@ -126,6 +126,13 @@ int rd_process_system(rd_basis* b, rd_op* op, long nrhs, const long* bidx, const
 int rd_rrqr(rd_ctx* ctx, int dtype, long n, long m, const void* A, double tol, int normalize, long* rank,
             long* perm, double* rdiag, void* Q, int where);
 
+/* ------------------------------------------------------- bench hooks --- */
+/* Mean device ms per launch of the three inner-iteration projection kernels
+ * (ms_out[0] c = K^T x, [1] fused x' = x - K c1 ; c2 = K^T x', [2] update)
+ * on a seeded random n x c basis, and of the multi-column stencil apply.    */
+int rd_bench_projection(rd_ctx* ctx, int dtype, long n, long c, int iters, double* ms_out);
+int rd_bench_stencil(rd_op* op, int dtype, long ncols, int iters, double* ms_out);
+
 #ifdef __cplusplus
 }
 #endif

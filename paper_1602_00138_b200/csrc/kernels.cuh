@@ -133,36 +133,71 @@ __device__ __forceinline__ void node_coords(const OpDev& op, long p, int& i, int
 template <class T>
 __global__ void __launch_bounds__(256) stencil_kernel(OpDev op, const T* __restrict__ x, long ldx,
                                                       const int* __restrict__ xcol, T* __restrict__ y, long ldy,
-                                                      int ncols) {
-    const int i = blockIdx.x * 32 + (threadIdx.x & 31);
-    const int j = blockIdx.y * 8 + (threadIdx.x >> 5);
-    const int k = blockIdx.z;
-    if (i >= op.N0 || j >= op.N1) return;
+                                                      int ncols, int kz);
+
+// z-marching stencil sweep for one (i, j) column over planes [k0, k1): x at
+// k-1, k, k+1 and the -z face coefficient stay in registers from plane to
+// plane, so each plane loads x(k+1), four in-plane x neighbours and six
+// coefficients (the +x/+y/+z/diag of p and the -x/-y faces of the neighbours).
+// f(p, xc, y) is called per plane with the row result y = (A x)_p.
+template <class T, class F>
+__device__ __forceinline__ void zmarch(const OpDev& op, const T* __restrict__ x, int i, int j, int k0, int k1, F&& f) {
     const long n = op.n;
     const long s1 = op.N0, s2 = (long)op.N0 * op.N1;
-    const long p = i + s1 * j + s2 * k;
-    const double* __restrict__ F = op.F;
-    const double dg = __ldg(F + p);
-    const double fxm = i > 0 ? __ldg(F + n + p - 1) : 0.0, fxp = i < op.N0 - 1 ? __ldg(F + n + p) : 0.0;
-    const double fym = j > 0 ? __ldg(F + 2 * n + p - s1) : 0.0, fyp = j < op.N1 - 1 ? __ldg(F + 2 * n + p) : 0.0;
-    double fzm = 0.0, fzp = 0.0;
-    if (op.d == 3) {
-        fzm = k > 0 ? __ldg(F + 3 * n + p - s2) : 0.0;
-        fzp = k < op.N2 - 1 ? __ldg(F + 3 * n + p) : 0.0;
-    }
-    for (int c = 0; c < ncols; ++c) {
-        const T* xc = x + (size_t)(xcol ? xcol[c] : c) * ldx;
+    const double* __restrict__ Fd = op.F;
+    long p = i + s1 * (j + (long)op.N1 * k0);
+    const bool three = op.d == 3;
+    T xm = (three && k0 > 0) ? x[p - s2] : Sc<T>::zero();
+    double fzm = (three && k0 > 0) ? __ldg(Fd + 3 * n + p - s2) : 0.0;
+    T xc = x[p];
+    const bool hx_m = i > 0, hx_p = i < op.N0 - 1, hy_m = j > 0, hy_p = j < op.N1 - 1;
+#pragma unroll 2
+    for (int k = k0; k < k1; ++k) {
+        const bool hz_p = three && k < op.N2 - 1;
+        const T xp = hz_p ? x[p + s2] : Sc<T>::zero();
+        const double fzp = hz_p ? __ldg(Fd + 3 * n + p) : 0.0;
+        const double dg = __ldg(Fd + p);
+        const double fxm = hx_m ? __ldg(Fd + n + p - 1) : 0.0;
+        const double fxp = hx_p ? __ldg(Fd + n + p) : 0.0;
+        const double fym = hy_m ? __ldg(Fd + 2 * n + p - s1) : 0.0;
+        const double fyp = hy_p ? __ldg(Fd + 2 * n + p) : 0.0;
+        const T xim = hx_m ? x[p - 1] : Sc<T>::zero();
+        const T xip = hx_p ? x[p + 1] : Sc<T>::zero();
+        const T xjm = hy_m ? x[p - s1] : Sc<T>::zero();
+        const T xjp = hy_p ? x[p + s1] : Sc<T>::zero();
         T acc = Sc<T>::zero();
-        if (i > 0) acc = axpy_real(fxm, xc[p - 1], acc);
-        if (i < op.N0 - 1) acc = axpy_real(fxp, xc[p + 1], acc);
-        if (j > 0) acc = axpy_real(fym, xc[p - s1], acc);
-        if (j < op.N1 - 1) acc = axpy_real(fyp, xc[p + s1], acc);
-        if (op.d == 3) {
-            if (k > 0) acc = axpy_real(fzm, xc[p - s2], acc);
-            if (k < op.N2 - 1) acc = axpy_real(fzp, xc[p + s2], acc);
+        acc = axpy_real(fxm, xim, acc);
+        acc = axpy_real(fxp, xip, acc);
+        acc = axpy_real(fym, xjm, acc);
+        acc = axpy_real(fyp, xjp, acc);
+        if (three) {
+            acc = axpy_real(fzm, xm, acc);
+            acc = axpy_real(fzp, xp, acc);
         }
-        y[(size_t)c * ldy + p] = Sc<T>::sub(diag_apply<T>(dg, op.shift, xc[p]), acc);
+        const T yv = Sc<T>::sub(diag_apply<T>(dg, op.shift, xc), acc);
+        f(p, xc, yv);
+        xm = xc;
+        xc = xp;
+        fzm = fzp;
+        p += s2;
     }
+}
+
+// y[:, c] = A x[:, xcol ? xcol[c] : c]: blockIdx.z = (column, k chunk of kz planes)
+template <class T>
+__global__ void __launch_bounds__(256) stencil_kernel(OpDev op, const T* __restrict__ x, long ldx,
+                                                      const int* __restrict__ xcol, T* __restrict__ y, long ldy,
+                                                      int ncols, int kz) {
+    const int nkc = (op.N2 + kz - 1) / kz;
+    const int c = blockIdx.z / nkc;
+    const int kc = blockIdx.z - c * nkc;
+    const int i = blockIdx.x * 32 + (threadIdx.x & 31);
+    const int j = blockIdx.y * 8 + (threadIdx.x >> 5);
+    if (c >= ncols || i >= op.N0 || j >= op.N1) return;
+    const int k0 = kc * kz, k1 = min(op.N2, k0 + kz);
+    const T* xc = x + (size_t)(xcol ? xcol[c] : c) * ldx;
+    T* yc = y + (size_t)c * ldy;
+    zmarch<T>(op, xc, i, j, k0, k1, [&](long p, const T&, const T& v) { yc[p] = v; });
 }
 
 // ------------------------------------------------------------ CG state ---
@@ -195,15 +230,13 @@ __global__ void __launch_bounds__(256) cg_stencil_dots(OpDev op, const T* __rest
     const int i = blockIdx.x * 32 + (threadIdx.x & 31);
     const int j = blockIdx.y * 8 + (threadIdx.x >> 5);
     const int k0 = blockIdx.z * kz, k1 = min(op.N2, k0 + kz);
-    for (int k = k0; k < k1 && i < op.N0 && j < op.N1; ++k) {
-        const long p = i + (long)op.N0 * (j + (long)op.N1 * k);
-        const T wp = stencil_row<T>(op, r, p, i, j, k);
-        w[p] = wp;
-        const T rp = r[p];
-        g = Sc<T>::fma(rp, rp, g);
-        dl = Sc<T>::fma(rp, wp, dl);
-        h += Sc<T>::abs2(rp);
-    }
+    if (i < op.N0 && j < op.N1)
+        zmarch<T>(op, r, i, j, k0, k1, [&](long p, const T& rp, const T& wp) {
+            w[p] = wp;
+            g = Sc<T>::fma(rp, rp, g);
+            dl = Sc<T>::fma(rp, wp, dl);
+            h += Sc<T>::abs2(rp);
+        });
     __shared__ double s_red[32];
     __shared__ double s_vals[2 * W + 1];
     double v[2 * W + 1];

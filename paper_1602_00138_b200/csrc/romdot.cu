@@ -3,9 +3,12 @@
 // (include/romdot_b200.h). All control flow that the reference runs in
 // src/basis.cpp and src/krylov.cpp lives here in C++; all arithmetic on
 // n-vectors runs in the kernels of kernels.cuh / dense.cuh.
+#include <cuda.h>
+#include <cudaTypedefs.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -231,14 +234,25 @@ inline dim3 stencil_grid(const OpDev& op, long zmult) {
     return dim3((unsigned)((op.N0 + 31) / 32), (unsigned)((op.N1 + 7) / 8), (unsigned)(op.N2 * zmult));
 }
 
+// z-chunk length: enough (i, j, k-chunk) blocks per column to fill the GPU
+inline int stencil_kz(const OpDev& op, long ncols, int sms) {
+    const long xy = (long)((op.N0 + 31) / 32) * ((op.N1 + 7) / 8);
+    int kz = 1;
+    while (kz < op.N2 && xy * ncols * ((op.N2 + 2 * kz - 1) / (2 * kz)) >= 8L * sms) kz *= 2;
+    return kz;
+}
+
 template <class T> void launch_stencil(Ctx& c, const OpDev& op, const T* x, long ldx, const int* xcol, T* y,
                                        long ldy, long ncols) {
     if (ncols <= 0) return;
-    for (long c0 = 0; c0 < ncols; c0 += 16) {
-        const long nc = std::min(16L, ncols - c0);
-        stencil_kernel<T><<<stencil_grid(op, 1), 256, 0, c.s>>>(op, xcol ? x : x + (size_t)c0 * ldx, ldx,
-                                                                 xcol ? xcol + c0 : nullptr, y + (size_t)c0 * ldy,
-                                                                 ldy, (int)nc);
+    const int kz = stencil_kz(op, ncols, c.sms);
+    const long nkc = (op.N2 + kz - 1) / kz;
+    const long maxc = std::max(1L, 65535L / nkc);
+    for (long c0 = 0; c0 < ncols; c0 += maxc) {
+        const long nc = std::min(maxc, ncols - c0);
+        dim3 grid((unsigned)((op.N0 + 31) / 32), (unsigned)((op.N1 + 7) / 8), (unsigned)(nkc * nc));
+        stencil_kernel<T><<<grid, 256, 0, c.s>>>(op, xcol ? x : x + (size_t)c0 * ldx, ldx, xcol ? xcol + c0 : nullptr,
+                                                 y + (size_t)c0 * ldy, ldy, (int)nc, kz);
         c.check_launch();
     }
 }
@@ -334,6 +348,31 @@ void ts_NT_launch(Ctx& c, const T* K, long ldk, long ncol, const T* x, T* xo, lo
 constexpr long kRowPad = 256;  // row padding of RB bases and inner workspaces
 inline long padded_rows(long n) { return (n + kRowPad - 1) / kRowPad * kRowPad; }
 
+static CUtensorMap g_null_tmap;  // unused map passed to the 1D (row-blocked) variant
+
+// Encode a 2D tensor map over a column-major n x ncols matrix (ld = n) viewed
+// as doubles, box = 32 rows x bc columns (driver entry point, no -lcuda).
+template <class T> CUtensorMap make_colmajor_tmap(const T* base, long n, long ld, long ncols, int bc) {
+    static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
+    if (!encode) {
+        cudaDriverEntryPointQueryResult q;
+        CK(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", reinterpret_cast<void**>(&encode), cudaEnableDefault,
+                                   &q));
+        if (!encode) throw CudaError("cuTensorMapEncodeTiled unavailable");
+    }
+    constexpr int W = Sc<T>::W;
+    CUtensorMap m;
+    cuuint64_t gdim[2] = {(cuuint64_t)n * W, (cuuint64_t)ncols};
+    cuuint64_t gstride[1] = {(cuuint64_t)ld * sizeof(T)};
+    cuuint32_t box[2] = {(cuuint32_t)(32 * W), (cuuint32_t)bc};
+    cuuint32_t es[2] = {1, 1};
+    CUresult r = encode(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<T*>(base), gdim, gstride, box, es,
+                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) throw CudaError("cuTensorMapEncodeTiled failed: " + std::to_string((int)r));
+    return m;
+}
+
 template <class T, int MODE, int CPW>
 void ts_tma_inst(Ctx& c, const T* Krb, int C, long n, const T* x, T* xo, const double* cin, double* out, T* r, T* p,
                  T* s, T* y, CGState* st) {
@@ -352,16 +391,16 @@ void ts_tma_inst(Ctx& c, const T* Krb, int C, long n, const T* x, T* xo, const d
         int optin = 0;
         CK(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, c.device));
         cudaFuncAttributes fa;
-        CK(cudaFuncGetAttributes(&fa, ts_tma<T, MODE, false, CPW>));
-        CK(cudaFuncSetAttribute(ts_tma<T, MODE, false, CPW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        CK(cudaFuncGetAttributes(&fa, ts_tma<T, MODE, false, CPW, false>));
+        CK(cudaFuncSetAttribute(ts_tma<T, MODE, false, CPW, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 optin - (int)fa.sharedSizeBytes));
         configured = optin - (int)fa.sharedSizeBytes;
     }
     if ((int)L.total > configured) throw ConfigError("TMA projection: shared-memory ring too large");
     const long ntile = padded_rows(n) / TR;
     const int grid = (int)std::max(1L, std::min<long>(ntile, (long)c.sms));
-    ts_tma<T, MODE, false, CPW><<<grid, TMA_THREADS, L.total, c.s>>>(Krb, C, n, ntile, L, x, xo, cin, c.red(), out, r,
-                                                                     p, s, y, st);
+    ts_tma<T, MODE, false, CPW, false><<<grid, TMA_THREADS, L.total, c.s>>>(g_null_tmap, 0, Krb, C, n, ntile, L, x,
+                                                                            xo, cin, c.red(), out, r, p, s, y, st);
     c.check_launch();
 }
 
@@ -512,6 +551,86 @@ template <class T, bool HERM> CholInfo chol_inv(Ctx& c, T* G, T* Sinv, long r, b
     return ci;
 }
 
+
+// ---- column-major (global basis) TMA passes, 128-column chunks -----------
+// out[j] = sum_i op(K_ij) x_i (MODE 0) and xo = x - K c (MODE 3) over a
+// column-major n x ncols matrix with ld*sizeof(T) % 16 == 0. x / xo must be
+// padded to padded_rows(n) (the TMA x tile of the last row block).
+template <class T, int MODE, bool HERM>
+void global_tma_chunk(Ctx& c, const T* K, long ld, long ncols, long col0, int cc, const T* x, T* xo, const double* cin,
+                      double* out, long n) {
+    constexpr int CPW = 16;
+    const int es = sizeof(T);
+    TmaLayout L = tma_layout<T>(cc, 32, 2, 1);
+    const uint32_t per_stage = ((L.tile_bytes + 127u) & ~127u) + ((L.x_bytes + 127u) & ~127u);
+    const uint32_t fixed = L.total - 2 * per_stage;
+    int S = (int)std::min<long>(8, (196L * 1024 - fixed) / per_stage);
+    if (S < 2) S = 2;
+    L = tma_layout<T>(cc, 32, S, 1);
+    static int configured = 0;
+    if (!configured) {
+        int optin = 0;
+        CK(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, c.device));
+        cudaFuncAttributes fa;
+        CK(cudaFuncGetAttributes(&fa, ts_tma<T, MODE, HERM, CPW, true>));
+        CK(cudaFuncSetAttribute(ts_tma<T, MODE, HERM, CPW, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                optin - (int)fa.sharedSizeBytes));
+        configured = optin - (int)fa.sharedSizeBytes;
+    }
+    if ((int)L.total > configured) throw ConfigError("global TMA pass: shared-memory ring too large");
+    const CUtensorMap tm = make_colmajor_tmap<T>(K, n, ld, ncols, cc);
+    const long ntile = padded_rows(n) / 32;
+    const int grid = (int)std::max(1L, std::min<long>(ntile, (long)c.sms));
+    ts_tma<T, MODE, HERM, CPW, true><<<grid, TMA_THREADS, L.total, c.s>>>(
+        tm, (int)col0, nullptr, cc, n, ntile, L, x, xo, cin ? cin + col0 * Sc<T>::W : nullptr, c.red(),
+        out ? out + col0 * Sc<T>::W : nullptr, nullptr, nullptr, nullptr, nullptr, nullptr);
+    c.check_launch();
+    (void)es;
+}
+
+template <class T> bool tma_ok(long ld) { return (ld * (long)sizeof(T)) % 16 == 0; }
+
+// out = op(K)^T x   (x padded)
+template <class T, bool HERM>
+void global_T(Ctx& c, const T* K, long ld, long ncols, const T* x, long n, double* out) {
+    if (!tma_ok<T>(ld)) {
+        ts_T_launch<T, HERM>(c, K, ld, ncols, x, n, out);
+        return;
+    }
+    for (long c0 = 0; c0 < ncols; c0 += 128)
+        global_tma_chunk<T, 0, HERM>(c, K, ld, ncols, c0, (int)std::min(128L, ncols - c0), x, nullptr, nullptr, out, n);
+}
+
+// xo = x - K cin  (x, xo padded; may alias)
+template <class T>
+void global_N(Ctx& c, const T* K, long ld, long ncols, const T* x, T* xo, long n, const double* cin) {
+    if (!tma_ok<T>(ld) || ncols == 0) {
+        ts_N_launch<T>(c, K, ld, ncols, x, xo, n, cin);
+        return;
+    }
+    const T* src = x;
+    for (long c0 = 0; c0 < ncols; c0 += 128) {
+        global_tma_chunk<T, 3, false>(c, K, ld, ncols, c0, (int)std::min(128L, ncols - c0), src, xo, cin, nullptr, n);
+        src = xo;
+    }
+}
+
+// CGS2 of z against the first t columns of Q with padded vectors (TMA path)
+template <class T, bool HERM>
+void cgs2_global(Ctx& c, const T* Q, long ldq, long t, const T* z, T* q, long n, double* coef, double* tmp1,
+                 double* tmp2) {
+    constexpr int W = Sc<T>::W;
+    if (t == 0) {
+        if (q != z) CK(cudaMemcpyAsync(q, z, sizeof(T) * n, cudaMemcpyDeviceToDevice, c.s));
+        return;
+    }
+    global_T<T, HERM>(c, Q, ldq, t, z, n, tmp1);
+    global_N<T>(c, Q, ldq, t, z, q, n, tmp1);
+    global_T<T, HERM>(c, Q, ldq, t, q, n, tmp2);
+    global_N<T>(c, Q, ldq, t, q, q, n, tmp2);
+    launch_addsub(c, (int)(t * W), tmp1, tmp2, 1.0, coef);
+}
+
 // ---------------------------------------------------------- CG driver ---
 struct SolveOut {
     int iterations = 0;
@@ -538,9 +657,12 @@ template <class T> struct Workspace {
 // Recycled CG / COCG (the CPU checker under oracle/ restates the same recurrence).
 // rhs, U, K, g, y_out, image: device. g/y_out/image may alias workspace-free
 // buffers only.
+// padded_io: rhs, y_out and image are zero-tailed to padded_rows(n), so the
+// column-major U / K passes outside the iteration loop can use the TMA path.
 template <class T>
 SolveOut recycled_cg(Ctx& c, DevOp& op, const T* U, const T* K, long ncol, const T* rhs, double tol, long maxit,
-                     double rhs_scale, T* g, T* y_out, T* image, Workspace<T>& ws, bool want_hist) {
+                     double rhs_scale, T* g, T* y_out, T* image, Workspace<T>& ws, bool want_hist,
+                     bool padded_io = false) {
     constexpr int W = Sc<T>::W;
     const long n = op.n();
     const long npad = padded_rows(n);
@@ -559,7 +681,10 @@ SolveOut recycled_cg(Ctx& c, DevOp& op, const T* U, const T* K, long ncol, const
     CK(cudaMemsetAsync(w, 0, sizeof(T) * npad, c.s));
     // r0 = P rhs (CGS2), e = K^T rhs
     if (ncol > 0) {
-        cgs2<T, false>(c, K, n, ncol, rhs, r, n, e, c1, c2);
+        if (padded_io)
+            cgs2_global<T, false>(c, K, n, ncol, rhs, r, n, e, c1, c2);
+        else
+            cgs2<T, false>(c, K, n, ncol, rhs, r, n, e, c1, c2);
     } else {
         CK(cudaMemcpyAsync(r, rhs, sizeof(T) * n, cudaMemcpyDeviceToDevice, c.s));
     }
@@ -676,9 +801,15 @@ SolveOut recycled_cg(Ctx& c, DevOp& op, const T* U, const T* K, long ncol, const
     // image = A y ; g = y + U (e - K^T image)
     launch_stencil<T>(c, op.d, y, n, nullptr, image, n, 1);
     if (ncol > 0) {
-        ts_T_launch<T, false>(c, K, n, ncol, image, n, c1);
+        if (padded_io)
+            global_T<T, false>(c, K, n, ncol, image, n, c1);
+        else
+            ts_T_launch<T, false>(c, K, n, ncol, image, n, c1);
         launch_addsub(c, (int)(ncol * W), c1, e, -1.0, c2);  // c2 = K^T image - e
-        ts_N_launch<T>(c, U, n, ncol, y, g, n, c2);           // g = y - U c2
+        if (padded_io)
+            global_N<T>(c, U, n, ncol, y, g, n, c2);  // g = y - U c2
+        else
+            ts_N_launch<T>(c, U, n, ncol, y, g, n, c2);
     } else if (g != y) {
         CK(cudaMemcpyAsync(g, y, sizeof(T) * n, cudaMemcpyDeviceToDevice, c.s));
     }
@@ -988,15 +1119,28 @@ template <class T> struct DevBasis : BasisBase {
         (void)W;
     }
 
+    // Padded (zero-tailed) device vectors for the TMA passes over the basis.
+    DevBuf zpad, qpad, vpad;
+    T* padded(DevBuf& b) {
+        if (b.bytes < sizeof(T) * padded_rows(n)) {
+            b.ensure(sizeof(T) * padded_rows(n));
+            CK(cudaMemsetAsync(b.p, 0, b.bytes, ctx->s));
+        }
+        return b.template as<T>();
+    }
+
     bool factor_image(long j, const T* vj, const T* z, bool may_drop) {
         Ctx& c = *ctx;
         constexpr int W = Sc<T>::W;
-        T* q = Kp() + (size_t)j * n;
+        T* zp = padded(zpad);
+        T* qp = padded(qpad);
+        T* vp = padded(vpad);
+        if (zp != z) CK(cudaMemcpyAsync(zp, z, sizeof(T) * n, cudaMemcpyDeviceToDevice, c.s));
         double* coef = c.sc(4);
         double* nrm = c.sc(7);
-        cgs2<T, true>(c, Kp(), n, j, z, q, n, coef, c.sc(5), c.sc(6));
-        launch_norms<T>(c, q, n, nrm);
-        launch_norms<T>(c, z, n, nrm + 8);
+        cgs2_global<T, true>(c, Kp(), n, j, zp, qp, n, coef, c.sc(5), c.sc(6));
+        launch_norms<T>(c, qp, n, nrm);
+        launch_norms<T>(c, zp, n, nrm + 8);
         std::vector<double> hc(2 + (size_t)j * W);
         CK(cudaMemcpyAsync(hc.data(), nrm, sizeof(double), cudaMemcpyDeviceToHost, c.s));
         CK(cudaMemcpyAsync(hc.data() + 1, nrm + 8, sizeof(double), cudaMemcpyDeviceToHost, c.s));
@@ -1005,13 +1149,15 @@ template <class T> struct DevBasis : BasisBase {
         const double rho = std::sqrt(hc[0]);
         const double zn = std::sqrt(hc[1]);
         if (may_drop && rho <= 1e-12 * zn) return false;
-        launch_scale<T>(c, q, q, n, nrm, 0);
+        launch_scale<T>(c, qp, Kp() + (size_t)j * n, n, nrm, 0);  // K_img(:, j) = q / rho
         T* wj = Wp() + (size_t)j * n;
-        if (j > 0)
-            ts_N_launch<T>(c, Wp(), n, j, vj, wj, n, coef);
-        else if (wj != vj)
-            CK(cudaMemcpyAsync(wj, vj, sizeof(T) * n, cudaMemcpyDeviceToDevice, c.s));
-        launch_scale<T>(c, wj, wj, n, nrm, 0);
+        if (j > 0) {
+            CK(cudaMemcpyAsync(vp, vj, sizeof(T) * n, cudaMemcpyDeviceToDevice, c.s));
+            global_N<T>(c, Wp(), n, j, vp, vp, n, coef);             // W(:, j) = (v_j - W c) / rho
+            launch_scale<T>(c, vp, wj, n, nrm, 0);
+        } else {
+            launch_scale<T>(c, vj, wj, n, nrm, 0);
+        }
         for (long i = 0; i < j; ++i) {
             if constexpr (W == 1)
                 Rat(i, j) = hc[2 + i];
@@ -1220,6 +1366,18 @@ struct LogRow {
     bool appended;
 };
 
+// Host wall-clock phase accounting of process_system (ROMDOT_VERBOSE>=1);
+// every phase ends in a stream sync already, so this adds no device syncs.
+struct PhaseTimer {
+    double t[8] = {0};
+    std::chrono::steady_clock::time_point last = std::chrono::steady_clock::now();
+    void lap(int k) {
+        const auto now = std::chrono::steady_clock::now();
+        t[k] += std::chrono::duration<double, std::milli>(now - last).count();
+        last = now;
+    }
+};
+
 template <class T>
 void process_system(DevBasis<T>& gb, DevOp& op, long nrhs, const long* bidx, const double* bval, double tol,
                     int system_index, long maxit, T* Xdev, std::vector<LogRow>& log, long& inner_its,
@@ -1227,7 +1385,16 @@ void process_system(DevBasis<T>& gb, DevOp& op, long nrhs, const long* bidx, con
     Ctx& c = *gb.ctx;
     const long n = gb.n;
     if (maxit <= 0) maxit = 2 * n;
+    PhaseTimer pt;
+    const bool timing = verbose() >= 1;
+    auto lap = [&](int k) {
+        if (timing) {
+            c.sync();
+            pt.lap(k);
+        }
+    };
     gb.refresh(op);
+    lap(0);
     VLOG(1, "system %d: refresh done (cols %ld, block %ld seq %ld second-pass %ld)", system_index, gb.cols,
          gb.stats_block_refresh, gb.stats_seq_refresh, gb.stats_second_pass);
     long cspace = 1;
@@ -1235,6 +1402,7 @@ void process_system(DevBasis<T>& gb, DevOp& op, long nrhs, const long* bidx, con
     dbg_sum("refresh K", gb.Kp(), gb.n * gb.cols, c.s);
     dbg_sum("refresh W", gb.Wp(), gb.n * gb.cols, c.s);
     gb.factor_eig_block(op, cspace);
+    lap(1);
     dbg_sum("eig Kr", gb.Kr.template as<T>(), gb.n * gb.ku, c.s);
     dbg_sum("eig Ur", gb.Ur.template as<T>(), gb.n * gb.ku, c.s);
     log.clear();
@@ -1250,44 +1418,46 @@ void process_system(DevBasis<T>& gb, DevOp& op, long nrhs, const long* bidx, con
     vald.ensure(sizeof(double) * nrhs);
     CK(cudaMemcpyAsync(idxd.p, bidx, sizeof(long) * nrhs, cudaMemcpyHostToDevice, c.s));
     CK(cudaMemcpyAsync(vald.p, bval, sizeof(double) * nrhs, cudaMemcpyHostToDevice, c.s));
-    Rall.ensure(sizeof(T) * n * nrhs);
+    const long npad = padded_rows(n);
+    Rall.ensure(sizeof(T) * npad * nrhs);
+    CK(cudaMemsetAsync(Rall.p, 0, sizeof(T) * npad * nrhs, c.s));
     if (r0 > 0) {
         Wc.ensure(sizeof(T) * r0 * nrhs);
         row_gather_multi<T, true><<<c.grid_for(r0 * nrhs, 256, 4), 256, 0, c.s>>>(
             gb.Kp(), n, 0, (int)r0, idxd.template as<long>(), vald.template as<double>(), (int)nrhs, -1.0,
             Wc.template as<T>(), r0);
         c.check_launch();
-        gemm<T, false>(c, gb.Kp(), n, r0, Wc.template as<T>(), nrhs, nullptr, 0, Rall.template as<T>(), n, n, false);
-    } else {
-        CK(cudaMemsetAsync(Rall.p, 0, sizeof(T) * n * nrhs, c.s));
+        gemm<T, false>(c, gb.Kp(), n, r0, Wc.template as<T>(), nrhs, nullptr, 0, Rall.template as<T>(), npad, n,
+                       false);
     }
-    scatter_add_rhs<T><<<(int)((nrhs + 127) / 128), 128, 0, c.s>>>(Rall.template as<T>(), n, idxd.template as<long>(),
+    scatter_add_rhs<T><<<(int)((nrhs + 127) / 128), 128, 0, c.s>>>(Rall.template as<T>(), npad, idxd.template as<long>(),
                                                                    vald.template as<double>(), (int)nrhs);
     c.check_launch();
-    dbg_sum("Rall", Rall.template as<T>(), n * nrhs, c.s);
+    dbg_sum("Rall", Rall.template as<T>(), npad * nrhs, c.s);
     // deferred solution assembly X = G + W Coef (solve_projected, basis.cpp:110-112)
     const long capc = std::max(gb.capcols, r0 + nrhs + 1);
     if (Xdev) {
         Coef.ensure(sizeof(T) * capc * nrhs);
         CK(cudaMemsetAsync(Coef.p, 0, sizeof(T) * capc * nrhs, c.s));
     }
-    rjbuf.ensure(sizeof(T) * n);
+    for (DevBuf* b : {&rjbuf, &ybuf, &gbuf, &imbuf}) {  // zero-tailed (TMA passes)
+        b->ensure(sizeof(T) * npad);
+        CK(cudaMemsetAsync(b->p, 0, sizeof(T) * npad, c.s));
+    }
     wn.ensure(sizeof(T) * (nrhs + 8));
-    ybuf.ensure(sizeof(T) * n);
-    gbuf.ensure(sizeof(T) * n);
-    imbuf.ensure(sizeof(T) * n);
+    lap(2);
     for (long j = 0; j < nrhs; ++j) {
         const double bnorm = std::fabs(bval[j]);
         const long rcur = gb.cols;
-        const T* rhs = Rall.template as<T>() + (size_t)j * n;
+        const T* rhs = Rall.template as<T>() + (size_t)j * npad;
         if (rcur > r0) {  // project out this system's appended columns
             wn.ensure(sizeof(T) * (rcur - r0));
             row_gather_multi<T, true><<<c.grid_for(rcur - r0, 256, 1), 256, 0, c.s>>>(
                 gb.Kp(), n, (int)r0, (int)(rcur - r0), idxd.template as<long>() + j, vald.template as<double>() + j, 1,
                 1.0, wn.template as<T>(), rcur - r0);
             c.check_launch();
-            ts_N_launch<T>(c, gb.Kp() + (size_t)r0 * n, n, rcur - r0, rhs, rjbuf.template as<T>(), n,
-                           (const double*)wn.p);
+            global_N<T>(c, gb.Kp() + (size_t)r0 * n, n, rcur - r0, rhs, rjbuf.template as<T>(), n,
+                        (const double*)wn.p);
             rhs = rjbuf.template as<T>();
         }
         double* nrm = c.sc(3);
@@ -1301,6 +1471,7 @@ void process_system(DevBasis<T>& gb, DevOp& op, long nrhs, const long* bidx, con
             c.check_launch();
         }
         c.sync();
+        lap(2);
         LogRow row{system_index, (int)j, std::sqrt(h) / bnorm, 0, false};
         T* Gj = Xdev ? Xdev + (size_t)j * n : gbuf.template as<T>();
         if (row.init_relres <= tol) {
@@ -1310,14 +1481,16 @@ void process_system(DevBasis<T>& gb, DevOp& op, long nrhs, const long* bidx, con
             const long cj = (long)idx.size();
             dbg_sum("rhs", rhs, n, c.s);
             gb.factor_rhs_space(op, idx);
+            lap(3);
             dbg_sum("space K", gb.Kr.template as<T>(), n * cj, c.s);
             dbg_sum("space U", gb.Ur.template as<T>(), n * cj, c.s);
             SolveOut so = recycled_cg<T>(c, op, gb.Ur.template as<T>(), gb.Kr.template as<T>(), cj, rhs,
                                          kInnerSafety * tol, maxit, bnorm, Gj, ybuf.template as<T>(),
-                                         imbuf.template as<T>(), gb.ws, false);
+                                         imbuf.template as<T>(), gb.ws, false, true);
             if (!so.converged)
                 throw SolverError("process_system: correction solve failed at system " +
                                   std::to_string(system_index) + ", rhs " + std::to_string(j));
+            lap(4);
             row.iterations = so.iterations;
             inner_its += so.iterations;
             dbg_sum("y", ybuf.template as<T>(), n, c.s);
@@ -1329,6 +1502,7 @@ void process_system(DevBasis<T>& gb, DevOp& op, long nrhs, const long* bidx, con
                 dbg_sum("appended K col", gb.Kp() + (size_t)(gb.cols - 1) * n, n, c.s);
                 dbg_sum("appended W col", gb.Wp() + (size_t)(gb.cols - 1) * n, n, c.s);
             }
+            lap(5);
         }
         VLOG(2, "system %d rhs %ld: init_relres %.3e its %d appended %d cols %ld", system_index, j, row.init_relres,
              row.iterations, (int)row.appended, gb.cols);
@@ -1342,6 +1516,11 @@ void process_system(DevBasis<T>& gb, DevOp& op, long nrhs, const long* bidx, con
         gemm<T, true>(c, gb.Wp(), n, rf, Cpk.template as<T>(), nrhs, Xdev, n, Xdev, n, n, false);
     }
     c.sync();
+    lap(6);
+    VLOG(1,
+         "system %d phases (ms): refresh %.1f eig-block %.1f checks %.1f rhs-spaces %.1f solves %.1f appends %.1f "
+         "X-assembly %.1f | %ld its",
+         system_index, pt.t[0], pt.t[1], pt.t[2], pt.t[3], pt.t[4], pt.t[5], pt.t[6], inner_its);
 }
 
 // ------------------------------------------------------------------ RRQR ---
@@ -2061,6 +2240,107 @@ int rd_rrqr(rd_ctx* ctx, int dtype, long n, long m, const void* A, double tol, i
             CK(cudaMemcpyAsync(Q, Qd.p, es * n * rk, kind, cx.s));
         }
         cx.sync();
+    });
+}
+
+
+// ---------------------------------------------------------- bench hooks ---
+// Kernel-level timing hooks for the C5 sweep (scripts/sweep.py): run each
+// recycle-space projection kernel `iters` times on an n x c basis of seeded
+// random values and return the mean device time per launch (CUDA events).
+int rd_bench_projection(rd_ctx* ctx, int dtype, long n, long c, int iters, double* ms_out) {
+    return guard([&] {
+        Ctx& cx = ctx->c;
+        auto run = [&](auto tag) {
+            using T = decltype(tag);
+            const long npad = padded_rows(n);
+            DevBuf K, x, r, p, s, y;
+            K.ensure(sizeof(T) * npad * c);
+            for (DevBuf* b : {&x, &r, &p, &s, &y}) {
+                b->ensure(sizeof(T) * npad);
+                CK(cudaMemsetAsync(b->p, 0, b->bytes, cx.s));
+            }
+            vec_randn<<<cx.grid_for(npad * c * Sc<T>::W, 256, 8), 256, 0, cx.s>>>(K.template as<double>(),
+                                                                                 npad * c * Sc<T>::W, 7);
+            vec_randn<<<cx.grid_for(n * Sc<T>::W, 256, 8), 256, 0, cx.s>>>(x.template as<double>(), n * Sc<T>::W, 8);
+            cx.check_launch();
+            CGState init{};
+            init.maxit = 1 << 30;
+            init.tol = 0.0;
+            init.scale = 1.0;
+            CGState* st = cx.cgst.template as<CGState>();
+            cx.st_host[0] = init;
+            CK(cudaMemcpyAsync(st, &cx.st_host[0], sizeof(CGState), cudaMemcpyHostToDevice, cx.s));
+            double* c1 = cx.sc(1);
+            double* c2 = cx.sc(2);
+            CK(cudaMemsetAsync(c1, 0, sizeof(double) * 8192 * 2, cx.s));
+            cudaEvent_t a, b;
+            CK(cudaEventCreate(&a));
+            CK(cudaEventCreate(&b));
+            for (int mode = 0; mode < 3; ++mode) {
+                auto launch = [&]() {
+                    if (mode == 0)
+                        ts_tma_launch<T, 0>(cx, K.template as<T>(), (int)c, n, x.template as<T>(), nullptr, nullptr, c1);
+                    else if (mode == 1)
+                        ts_tma_launch<T, 1>(cx, K.template as<T>(), (int)c, n, x.template as<T>(), y.template as<T>(),
+                                            c1, c2);
+                    else
+                        ts_tma_launch<T, 2>(cx, K.template as<T>(), (int)c, n, x.template as<T>(), nullptr, c2,
+                                            nullptr, r.template as<T>(), p.template as<T>(), s.template as<T>(),
+                                            y.template as<T>(), st);
+                };
+                for (int w = 0; w < 3; ++w) launch();
+                CK(cudaEventRecord(a, cx.s));
+                for (int t = 0; t < iters; ++t) launch();
+                CK(cudaEventRecord(b, cx.s));
+                CK(cudaEventSynchronize(b));
+                float ms = 0.f;
+                CK(cudaEventElapsedTime(&ms, a, b));
+                ms_out[mode] = ms / iters;
+            }
+            cudaEventDestroy(a);
+            cudaEventDestroy(b);
+        };
+        if (dtype == 0)
+            run(double{});
+        else
+            run(cplx{});
+    });
+}
+
+// Multi-column stencil apply timing on the operator's current fields.
+int rd_bench_stencil(rd_op* o, int dtype, long ncols, int iters, double* ms_out) {
+    return guard([&] {
+        Ctx& cx = o->ctx->c;
+        const long n = o->op.d.n;
+        auto run = [&](auto tag) {
+            using T = decltype(tag);
+            DevBuf x, y;
+            x.ensure(sizeof(T) * n * ncols);
+            y.ensure(sizeof(T) * n * ncols);
+            vec_randn<<<cx.grid_for(n * ncols * Sc<T>::W, 256, 8), 256, 0, cx.s>>>(x.template as<double>(),
+                                                                                   n * ncols * Sc<T>::W, 9);
+            cx.check_launch();
+            cudaEvent_t a, b;
+            CK(cudaEventCreate(&a));
+            CK(cudaEventCreate(&b));
+            for (int w = 0; w < 3; ++w)
+                launch_stencil<T>(cx, o->op.d, x.template as<T>(), n, nullptr, y.template as<T>(), n, ncols);
+            CK(cudaEventRecord(a, cx.s));
+            for (int t = 0; t < iters; ++t)
+                launch_stencil<T>(cx, o->op.d, x.template as<T>(), n, nullptr, y.template as<T>(), n, ncols);
+            CK(cudaEventRecord(b, cx.s));
+            CK(cudaEventSynchronize(b));
+            float ms = 0.f;
+            CK(cudaEventElapsedTime(&ms, a, b));
+            *ms_out = ms / iters;
+            cudaEventDestroy(a);
+            cudaEventDestroy(b);
+        };
+        if (dtype == 0)
+            run(double{});
+        else
+            run(cplx{});
     });
 }
 

@@ -12,15 +12,32 @@
 //   MODE 1  x'  = x - K c1 ; c2 = op(K)^T x'         (fused second CGS pass)
 //   MODE 2  q   = w' - K c2 ; p = r + beta p ; s = q + beta s ;
 //           y  += alpha p ; r -= alpha s             (CG/COCG update)
+//   MODE 3  x'  = x - K c                            (N pass, global basis)
+//
+// TMAP = true streams a column-major matrix (the global basis V/W/K_img,
+// ld = n) through a 2D tensor map instead: one cp.async.bulk.tensor.2d per
+// 32-row x C-column box lands in shared memory in the same (column, 32-row)
+// order as a row-blocked tile, so the consumers are shared; rows >= n are
+// zero-filled by the TMA unit.
 //
 // Rows >= n are zero padding of K and of the x workspace. Reductions are the
 // deterministic per-block partial + last-block sum of common.cuh.
 #pragma once
 
+#include <cuda.h>
+
 #include "common.cuh"
 #include "kernels.cuh"
 
 namespace rd {
+
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int c0, int c1, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+            smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(smem_u32(bar))
+        : "memory");
+}
 
 constexpr int TMA_CONSUMERS = 256;  // 8 warps
 constexpr int TMA_THREADS = TMA_CONSUMERS + 32;
@@ -61,9 +78,10 @@ template <class T> __host__ __device__ inline TmaLayout tma_layout(int C, int TR
     return L;
 }
 
-template <class T, int MODE, bool HERM, int CPW>
+template <class T, int MODE, bool HERM, int CPW, bool TMAP>
 __global__ void __launch_bounds__(TMA_THREADS, 1)
-    ts_tma(const T* __restrict__ Krb, int C, long n, long ntile, TmaLayout L, const T* __restrict__ x,
+    ts_tma(const __grid_constant__ CUtensorMap tmap, int col0, const T* __restrict__ Krb, int C, long n, long ntile,
+           TmaLayout L, const T* __restrict__ x,
            T* __restrict__ xo, const double* __restrict__ cin, GridRed red, double* out, T* __restrict__ r,
            T* __restrict__ p, T* __restrict__ s, T* __restrict__ y, CGState* st) {
     if (st && st->done) return;
@@ -99,7 +117,11 @@ __global__ void __launch_bounds__(TMA_THREADS, 1)
                 const uint32_t use = (uint32_t)(k / S);
                 mbar_wait(&empty[stage], (use & 1u) ^ 1u);
                 mbar_arrive_expect_tx(&full[stage], L.tile_bytes + L.NV * L.x_bytes);
-                tma_load_1d(smem + L.off_k + stage * stride_k, Krb + (size_t)t * TR * C, L.tile_bytes, &full[stage]);
+                if constexpr (TMAP)
+                    tma_load_2d(smem + L.off_k + stage * stride_k, &tmap, (int)(t * TR * Sc<T>::W), col0, &full[stage]);
+                else
+                    tma_load_1d(smem + L.off_k + stage * stride_k, Krb + (size_t)t * TR * C, L.tile_bytes,
+                                &full[stage]);
                 unsigned char* xb = smem + L.off_x + (size_t)stage * L.NV * stride_x;
                 tma_load_1d(xb, x + (size_t)t * TR, L.x_bytes, &full[stage]);
                 if (MODE == 2) {
@@ -170,6 +192,15 @@ __global__ void __launch_bounds__(TMA_THREADS, 1)
                         for (int jj = 0; jj < CPW; ++jj)
                             if (jj < ncol) acc[jj] = opfma<T, HERM>(kb[(size_t)(j0 + jj) * 32], q, acc[jj]);
                     }
+                } else if (MODE == 3) {
+                    for (int rb = wid; rb < RBN; rb += 8) {
+                        T sum = pb[(rb * 8) * 32 + lane];
+#pragma unroll
+                        for (int w2 = 1; w2 < 8; ++w2) sum = Sc<T>::add(sum, pb[(rb * 8 + w2) * 32 + lane]);
+                        const int rr = rb * 32 + lane;
+                        const long row = row0 + rr;
+                        if (row < n) xo[row] = Sc<T>::sub(Xs[rr], sum);
+                    }
                 } else {
                     for (int rb = wid; rb < RBN; rb += 8) {
                         T sum = pb[(rb * 8) * 32 + lane];
@@ -196,7 +227,7 @@ __global__ void __launch_bounds__(TMA_THREADS, 1)
             __syncwarp();
             if (lane == 0) mbar_arrive(&empty[stage]);
         }
-        if (MODE != 2) {
+        if (MODE <= 1) {
 #pragma unroll
             for (int jj = 0; jj < CPW; ++jj) {
                 double a[W];
@@ -214,6 +245,7 @@ __global__ void __launch_bounds__(TMA_THREADS, 1)
             }
         }
     }
+    if (MODE == 3) return;
     if (MODE == 2) {
         if (blockIdx.x == 0 && tid == 0) {
             st->gamma_prev = st->gamma;

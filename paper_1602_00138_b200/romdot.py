@@ -32,7 +32,8 @@ EXPORTS = [
     "rd_op_lam_max", "rd_recycled_solve", "rd_recycle_space_from_raw", "rd_initial_solutions",
     "rd_smallest_eigenpairs", "rd_basis_create", "rd_basis_destroy", "rd_basis_cols", "rd_basis_eig_block",
     "rd_basis_get", "rd_basis_device_ptr", "rd_basis_markers", "rd_basis_space", "rd_basis_refresh",
-    "rd_basis_append", "rd_basis_solve_projected", "rd_process_system", "rd_rrqr",
+    "rd_basis_append", "rd_basis_solve_projected", "rd_process_system", "rd_rrqr", "rd_bench_projection",
+    "rd_bench_stencil",
 ]
 
 
@@ -116,6 +117,8 @@ def load_library(path: Optional[str] = None):
     L.rd_process_system.argtypes = [vp, vp, C.c_long, vp, vp, C.c_double, C.c_int, C.c_long, vp, C.c_int, vp, lp,
                                     lp]
     L.rd_rrqr.argtypes = [vp, C.c_int, C.c_long, C.c_long, vp, C.c_double, C.c_int, lp, vp, vp, vp, C.c_int]
+    L.rd_bench_projection.argtypes = [vp, C.c_int, C.c_long, C.c_long, C.c_int, vp]
+    L.rd_bench_stencil.argtypes = [vp, C.c_int, C.c_long, C.c_int, vp]
     _LIB = L
     return L
 
@@ -440,6 +443,20 @@ def init_basis(op0: SchurOperator, op0_real: SchurOperator, layout: P.Layout, k_
     X0, its = initial_solutions(op0, layout, tol)
     gb = GlobalBasis(U0.astype(op0.dtype), X0, cap, op0.ctx)
     return gb, X0, lam, U0
+
+
+def bench_projection(n: int, c: int, cplx: bool, iters: int = 10, ctx: Optional[Context] = None):
+    """Mean ms per launch of the three TMA projection kernels (C5 sweep hook)."""
+    ctx = ctx or default_context()
+    out = np.zeros(3)
+    _check(load_library().rd_bench_projection(ctx.h, int(cplx), n, c, iters, _p(out)))
+    return out
+
+
+def bench_stencil(op: SchurOperator, ncols: int, iters: int = 10) -> float:
+    out = np.zeros(1)
+    _check(load_library().rd_bench_stencil(op.h, _dt(op.dtype), ncols, iters, _p(out)))
+    return float(out[0])
 
 
 def rrqr(A: np.ndarray, tol: float = 1e-10, normalize: bool = True, ctx: Optional[Context] = None):
