@@ -44,21 +44,31 @@ __global__ void __launch_bounds__(256) gram_kernel(const T* __restrict__ X, long
     const long r0 = (long)sl * rows_per_slice;
     const long r1 = min(n, r0 + rows_per_slice);
     const int col_a0 = ta * TA, col_b0 = tb * TB;
-    for (long rc = r0; rc < r1; rc += KC) {
-        // load KC rows x TA cols of X and TB cols of Y (lane = row within chunk)
-        const int lr = threadIdx.x % KC, lc = threadIdx.x / KC;  // 32 rows x 8 col groups
+    // register double buffering: chunk c+1 is loaded while chunk c is consumed
+    const int lr = threadIdx.x % KC, lc = threadIdx.x / KC;  // 32 rows x 8 column groups
+    constexpr int NA = TA / (256 / KC), NB = TB / (256 / KC);
+    T pa[NA], pbv[NB];
+    auto fetch = [&](long rc) {
         const long row = rc + lr;
 #pragma unroll
-        for (int c = lc; c < TA; c += 256 / KC) {
-            const int col = col_a0 + c;
-            Xs[lr][c] = (row < r1 && col < a) ? X[(size_t)col * ldx + row] : Sc<T>::zero();
+        for (int q = 0; q < NA; ++q) {
+            const int col = col_a0 + lc + q * (256 / KC);
+            pa[q] = (row < r1 && col < a) ? X[(size_t)col * ldx + row] : Sc<T>::zero();
         }
 #pragma unroll
-        for (int c = lc; c < TB; c += 256 / KC) {
-            const int col = col_b0 + c;
-            Ys[lr][c] = (row < r1 && col < b) ? Y[(size_t)col * ldy + row] : Sc<T>::zero();
+        for (int q = 0; q < NB; ++q) {
+            const int col = col_b0 + lc + q * (256 / KC);
+            pbv[q] = (row < r1 && col < b) ? Y[(size_t)col * ldy + row] : Sc<T>::zero();
         }
+    };
+    if (r0 < r1) fetch(r0);
+    for (long rc = r0; rc < r1; rc += KC) {
+#pragma unroll
+        for (int q = 0; q < NA; ++q) Xs[lr][lc + q * (256 / KC)] = pa[q];
+#pragma unroll
+        for (int q = 0; q < NB; ++q) Ys[lr][lc + q * (256 / KC)] = pbv[q];
         __syncthreads();
+        if (rc + KC < r1) fetch(rc + KC);
 #pragma unroll 8
         for (int k = 0; k < KC; ++k) {
             T xa[RA], yb[RB];
@@ -127,18 +137,38 @@ __global__ void __launch_bounds__(256) gemm_tall(const T* __restrict__ X, long l
 #pragma unroll
         for (int j = 0; j < RC; ++j) acc[i][j] = Sc<T>::zero();
     const int kend = upper_tri ? min(a, col0 + TC) : a;  // M upper triangular: rows k > col are zero
-    for (int k0 = 0; k0 < kend; k0 += KC) {
-        // X chunk: TR rows x KC cols
-        for (int e = threadIdx.x; e < TR * KC; e += 256) {
+    // register double buffering of the X / M chunks
+    constexpr int NX = TR * KC / 256, NM = KC * TC / 256;
+    T px[NX], pm[NM];
+    auto fetch = [&](int k0) {
+#pragma unroll
+        for (int q = 0; q < NX; ++q) {
+            const int e = threadIdx.x + q * 256;
             const int r = e % TR, k = e / TR;
             const long row = row0 + r;
-            Xs[k][r] = (row < n && k0 + k < a) ? X[(size_t)(k0 + k) * ldx + row] : Sc<T>::zero();
+            px[q] = (row < n && k0 + k < a) ? X[(size_t)(k0 + k) * ldx + row] : Sc<T>::zero();
         }
-        for (int e = threadIdx.x; e < KC * TC; e += 256) {
-            const int k = e % KC, c = e / KC;
-            Ms[k][c] = (k0 + k < a && col0 + c < b) ? M[(size_t)(col0 + c) * a + k0 + k] : Sc<T>::zero();
+#pragma unroll
+        for (int q = 0; q < NM; ++q) {
+            const int e = threadIdx.x + q * 256;
+            const int k = e % KC, cc = e / KC;
+            pm[q] = (k0 + k < a && col0 + cc < b) ? M[(size_t)(col0 + cc) * a + k0 + k] : Sc<T>::zero();
+        }
+    };
+    if (kend > 0) fetch(0);
+    for (int k0 = 0; k0 < kend; k0 += KC) {
+#pragma unroll
+        for (int q = 0; q < NX; ++q) {
+            const int e = threadIdx.x + q * 256;
+            Xs[e / TR][e % TR] = px[q];
+        }
+#pragma unroll
+        for (int q = 0; q < NM; ++q) {
+            const int e = threadIdx.x + q * 256;
+            Ms[e % KC][e / KC] = pm[q];
         }
         __syncthreads();
+        if (k0 + KC < kend) fetch(k0 + KC);
 #pragma unroll
         for (int k = 0; k < KC; ++k) {
             T xr[RR], mc[RC];
@@ -403,6 +433,101 @@ __global__ void scale_columns(T* X, long ld, int c, long n, const double* nrm2) 
     T* xc = X + (size_t)j * ld;
     for (long i = blockIdx.x * (long)blockDim.x + threadIdx.x; i < n; i += (long)gridDim.x * blockDim.x)
         xc[i] = Sc<T>::scale(xc[i], s);
+}
+
+}  // namespace rd
+
+namespace rd {
+
+// Thin Gram G (a x b, b <= 8) = op(X)^T Y: a multi-vector T pass. Block y-index
+// selects 32 columns of X (4 per warp), lanes walk rows; per-lane accumulators
+// acc[4][b] live across the block's rows; deterministic grid reduction.
+template <class T, bool HERM, int B>
+__global__ void __launch_bounds__(256) gram_thin(const T* __restrict__ X, long ldx, int a, const T* __restrict__ Y,
+                                                 long ldy, int b, long n, GridRed red, T* __restrict__ G) {
+    constexpr int W = Sc<T>::W;
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const int c0 = blockIdx.y * 32 + wid * 4;
+    T acc[4][B];
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+#pragma unroll
+        for (int v = 0; v < B; ++v) acc[q][v] = Sc<T>::zero();
+    for (long row = (long)blockIdx.x * 32 + lane; row < n; row += (long)gridDim.x * 32) {
+        T yv[B], xv[4];
+#pragma unroll
+        for (int v = 0; v < B; ++v) yv[v] = v < b ? Y[(size_t)v * ldy + row] : Sc<T>::zero();
+#pragma unroll
+        for (int q = 0; q < 4; ++q) xv[q] = (c0 + q < a) ? X[(size_t)(c0 + q) * ldx + row] : Sc<T>::zero();
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+#pragma unroll
+            for (int v = 0; v < B; ++v) acc[q][v] = opfma<T, HERM>(xv[q], yv[v], acc[q][v]);
+    }
+    // block values: 32 columns x B vectors, column-major per block chunk
+    __shared__ double s_vals[32 * B * W];
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+#pragma unroll
+        for (int v = 0; v < B; ++v) {
+            double t[W];
+            if constexpr (W == 1) {
+                t[0] = (double&)acc[q][v];
+            } else {
+                t[0] = ((cplx&)acc[q][v]).x;
+                t[1] = ((cplx&)acc[q][v]).y;
+            }
+#pragma unroll
+            for (int w = 0; w < W; ++w) {
+                const double sv = warp_sum(t[w]);
+                if (lane == 0) s_vals[((wid * 4 + q) * B + v) * W + w] = sv;
+            }
+        }
+    __syncthreads();
+    // grid reduction over blockIdx.x for each column chunk (blockIdx.y): reuse the
+    // generic last-block sum over all blocks with a per-chunk value offset
+    const int nv = 32 * B * W;
+    if (!grid_commit(red, s_vals, nv)) return;
+    // last block of the whole grid: sum, per chunk y, the gridDim.x partials
+    __threadfence();
+    const int nyc = gridDim.y;
+    for (int e = threadIdx.x; e < nyc * nv; e += blockDim.x) {
+        const int yc = e / nv, vv = e % nv;
+        double sum = 0.0;
+        for (unsigned bx = 0; bx < gridDim.x; ++bx)
+            sum += __ldcg(red.partials + (size_t)(bx + gridDim.x * yc) * nv + vv);
+        const int colr = vv / (B * W), v = (vv / W) % B, w = vv % W;
+        const int col = yc * 32 + colr;
+        if (col < a && v < b) reinterpret_cast<double*>(G)[((size_t)v * a + col) * W + w] = sum;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) *red.counter = 0u;
+}
+
+// Thin GEMM Z[n x b] = Y - X M (b <= 8, X: n x a, M: a x b, ld a): thread per
+// row, M in shared memory, X row read once for all b outputs.
+template <class T, int B>
+__global__ void __launch_bounds__(256) gemm_thin_sub(const T* __restrict__ X, long ldx, int a, const T* __restrict__ M,
+                                                     int b, const T* __restrict__ Y, long ldy, T* __restrict__ Z,
+                                                     long ldz, long n) {
+    extern __shared__ unsigned char sm_raw[];
+    T* Ms = reinterpret_cast<T*>(sm_raw);
+    for (int e = threadIdx.x; e < a * b; e += blockDim.x) Ms[e] = M[e];
+    __syncthreads();
+    for (long row = blockIdx.x * (long)blockDim.x + threadIdx.x; row < n; row += (long)gridDim.x * blockDim.x) {
+        T acc[B];
+#pragma unroll
+        for (int v = 0; v < B; ++v) acc[v] = Sc<T>::zero();
+        for (int k = 0; k < a; ++k) {
+            const T xv = X[(size_t)k * ldx + row];
+#pragma unroll
+            for (int v = 0; v < B; ++v)
+                if (v < b) acc[v] = Sc<T>::fma(xv, Ms[(size_t)v * a + k], acc[v]);
+        }
+#pragma unroll
+        for (int v = 0; v < B; ++v)
+            if (v < b) Z[(size_t)v * ldz + row] = Sc<T>::sub(Y[(size_t)v * ldy + row], acc[v]);
+    }
 }
 
 }  // namespace rd

@@ -467,9 +467,26 @@ void cgs2(Ctx& c, const T* Q, long ldq, long t, const T* z, T* q, long n, double
 
 // ------------------------------------------------------- block helpers ---
 // G (a x b, device, ld a) = op(X)^T Y over n rows. sym: X == Y, upper tiles only.
+template <class T, bool HERM, int B>
+void gram_thin_launch(Ctx& c, const T* X, long ldx, long a, const T* Y, long ldy, long b, long n, T* G) {
+    const int gx = (int)std::max(1L, std::min<long>((n + 31) / 32, (long)c.sms * 4 / ((a + 31) / 32) + 1));
+    dim3 grid(gx, (unsigned)((a + 31) / 32));
+    gram_thin<T, HERM, B><<<grid, 256, 0, c.s>>>(X, ldx, (int)a, Y, ldy, (int)b, n, c.red(), G);
+    c.check_launch();
+}
+
 template <class T, bool HERM>
 void gram(Ctx& c, const T* X, long ldx, long a, const T* Y, long ldy, long b, long n, T* G, bool sym, DevBuf& work) {
     if (a == 0 || b == 0) return;
+    if (!sym && b <= 8 && a <= 256) {  // thin: multi-vector T pass (no wasted tile FLOPs)
+        if (b <= 2)
+            gram_thin_launch<T, HERM, 2>(c, X, ldx, a, Y, ldy, b, n, G);
+        else if (b <= 4)
+            gram_thin_launch<T, HERM, 4>(c, X, ldx, a, Y, ldy, b, n, G);
+        else
+            gram_thin_launch<T, HERM, 8>(c, X, ldx, a, Y, ldy, b, n, G);
+        return;
+    }
     const long ta = (a + GT<T>::TA - 1) / GT<T>::TA, tb = (b + GT<T>::TB - 1) / GT<T>::TB;
     const long tiles = sym ? ta * (ta + 1) / 2 : ta * tb;
     long slices = std::max(1L, std::min<long>((4L * c.sms + tiles - 1) / tiles, (n + 4095) / 4096));
@@ -487,10 +504,27 @@ void gram(Ctx& c, const T* X, long ldx, long a, const T* Y, long ldy, long b, lo
 }
 
 // Z = X M (SUB=false) or Z = Y - X M (SUB=true); M is a x b on the device (ld a).
+template <class T, int B>
+void gemm_thin_launch(Ctx& c, const T* X, long ldx, long a, const T* M, long b, const T* Y, long ldy, T* Z, long ldz,
+                      long n) {
+    gemm_thin_sub<T, B><<<c.grid_for(n, 256, 8), 256, sizeof(T) * a * b, c.s>>>(X, ldx, (int)a, M, (int)b, Y, ldy, Z,
+                                                                              ldz, n);
+    c.check_launch();
+}
+
 template <class T, bool SUB>
 void gemm(Ctx& c, const T* X, long ldx, long a, const T* M, long b, const T* Y, long ldy, T* Z, long ldz, long n,
           bool upper) {
     if (b == 0 || n == 0) return;
+    if (SUB && a > 0 && b <= 8 && sizeof(T) * a * b <= 48 * 1024) {  // thin: thread-per-row N pass
+        if (b <= 2)
+            gemm_thin_launch<T, 2>(c, X, ldx, a, M, b, Y, ldy, Z, ldz, n);
+        else if (b <= 4)
+            gemm_thin_launch<T, 4>(c, X, ldx, a, M, b, Y, ldy, Z, ldz, n);
+        else
+            gemm_thin_launch<T, 8>(c, X, ldx, a, M, b, Y, ldy, Z, ldz, n);
+        return;
+    }
     if (a == 0) {
         if (SUB && Z != Y)
             for (long j = 0; j < b; ++j)
