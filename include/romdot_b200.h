@@ -100,7 +100,11 @@ int rd_basis_create(rd_ctx* ctx, int dtype, long n, long ku, long nrhs, const vo
 void rd_basis_destroy(rd_basis* b);
 long rd_basis_cols(rd_basis* b);
 long rd_basis_eig_block(rd_basis* b);
-/* which: 0 V, 1 K_img, 2 R (cols x cols), 3 W = V R^-1. Host output. */
+/* 1 once the image factor (K_img, R, W) exists, i.e. after the first refresh;
+ * before it the reference's Kimg_/R_ are empty (include/romdot/basis.hpp:63). */
+int rd_basis_factored(rd_basis* b);
+/* which: 0 V, 1 K_img, 2 R (cols x cols), 3 W = V R^-1. Host output.
+ * which != 0 before the first refresh: status 2 (no image factor yet). */
 int rd_basis_get(rd_basis* b, int which, void* out);
 /* Device pointer of V / K_img / W (valid until the next call that grows the basis). */
 void* rd_basis_device_ptr(rd_basis* b, int which);
@@ -119,12 +123,21 @@ int rd_process_system(rd_basis* b, rd_op* op, long nrhs, const long* bidx, const
                       int system_index, long maxit, void* X, int where, double* log, long* inner_iterations,
                       long* appends);
 
+/* Explicit residuals ||b_j - A x_j|| / ||b_j|| of a solution block (the
+ * test_basis.cpp:180-193 check, at any size). X is n x nrhs.               */
+int rd_residual_norms(rd_op* op, int dtype, long nrhs, const long* bidx, const double* bval, const void* X, int where,
+                      double* out);
+
 /* ---------------------------------------------------------- compression --- */
 /* Rank-revealing compression of the n x m candidate basis (acceptance.cpp:368-383
  * truncation rule, BASELINE RRQR): column-normalised (if normalize) pivoted QR
  * at relative tolerance tol. Outputs rank, perm (m), rdiag (m), Q (n x rank). */
 int rd_rrqr(rd_ctx* ctx, int dtype, long n, long m, const void* A, double tol, int normalize, long* rank,
             long* perm, double* rdiag, void* Q, int where);
+/* In-place Algorithm-1 compression of a finished build: frees the
+ * factorisation workspace, RRQR on V's own buffer, V <- orthonormal Q
+ * (n x rank). perm / rdiag have basis-cols entries. The basis is final.   */
+int rd_basis_compress(rd_basis* b, double tol, int normalize, long* rank, long* perm, double* rdiag);
 
 /* ------------------------------------------------------- bench hooks --- */
 /* Mean device ms per launch of the three inner-iteration projection kernels

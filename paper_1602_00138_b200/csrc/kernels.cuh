@@ -454,7 +454,7 @@ __global__ void __launch_bounds__(TS_THREADS) ts_T(const T* __restrict__ K, long
 // Fused CGS pass: xo = x - K c1 (c1 = cin, device), out = op(K)^T xo.
 template <class T, bool HERM, int CPW, bool RB>
 __global__ void __launch_bounds__(TS_THREADS) ts_NT(const T* __restrict__ K, long ldk, int c,
-                                                    const T* __restrict__ x, T* __restrict__ xo, long n,
+                                                    const T* x, T* xo, long n,
                                                     const double* __restrict__ cin, GridRed red, double* out,
                                                     const CGState* st) {
     if (st && st->done) return;
@@ -485,12 +485,18 @@ __global__ void __launch_bounds__(TS_THREADS) ts_NT(const T* __restrict__ K, lon
             const long rr = row < n ? row : n - 1;
 #pragma unroll
             for (int jj = 0; jj < CPW; ++jj) kv[u][jj] = ldg_nc(K + kaddr<RB>(rr, jbase + (jj < ncol ? jj : ncol - 1), ldk));
-            xv[u] = x[rr];  // read before the barrier: xo may alias x
+            // xo may alias x (in-place CGS2) and every warp consumes x[row] after the
+            // barrier while warp 0 stores xo[row]: the load must stay before the
+            // barrier (volatile coherent load + register fence; no __restrict__ on
+            // x/xo, which would license a non-coherent reload after it).
+            xv[u] = ldg_nc(x + rr);
         }
 #pragma unroll
-        for (int u = 0; u < U; ++u)
+        for (int u = 0; u < U; ++u) {
+            reg_fence(xv[u]);
 #pragma unroll
             for (int jj = 0; jj < CPW; ++jj) reg_fence(kv[u][jj]);
+        }
 #pragma unroll
         for (int u = 0; u < U; ++u) {
             T part = Sc<T>::zero();

@@ -14,6 +14,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <memory>
+#include <new>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -66,8 +67,54 @@ static int verbose() {
 
 // ROMDOT_VERBOSE>=3: bitwise-sensitive checksum of a device buffer (debug of
 // determinism; copies to host, slow).
+// Level 4: non-perturbing trace. Each checkpoint enqueues an order-independent
+// exact hash (sum of position-mixed 64-bit words) into a device log on the
+// stream -- no host syncs -- and dbg_flush prints the log at a point where the
+// caller syncs anyway (end of process_system).
+__global__ void dbg_hash_kernel(const unsigned long long* w, long nw, unsigned long long* slot) {
+    unsigned long long acc = 0;
+    for (long i = blockIdx.x * (long)blockDim.x + threadIdx.x; i < nw; i += (long)gridDim.x * blockDim.x) {
+        unsigned long long z = w[i] ^ ((unsigned long long)i * 0x9e3779b97f4a7c15ull);
+        z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
+        z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
+        acc += z ^ (z >> 31);
+    }
+    atomicAdd(slot, acc);
+}
+struct DbgLog {
+    unsigned long long* d = nullptr;
+    std::vector<std::string> names;
+    static constexpr int kCap = 1 << 16;
+};
+static DbgLog& dbg_log() {
+    static DbgLog L;
+    return L;
+}
+static void dbg_flush(cudaStream_t s) {
+    DbgLog& L = dbg_log();
+    if (verbose() < 4 || !L.d || L.names.empty()) return;
+    std::vector<unsigned long long> h(L.names.size());
+    cudaStreamSynchronize(s);
+    cudaMemcpy(h.data(), L.d, sizeof(unsigned long long) * h.size(), cudaMemcpyDeviceToHost);
+    for (size_t i = 0; i < h.size(); ++i) std::fprintf(stderr, "[romdot-hash] %s %016llx\n", L.names[i].c_str(), h[i]);
+    cudaMemsetAsync(L.d, 0, sizeof(unsigned long long) * h.size(), s);
+    L.names.clear();
+}
+
 template <class T> static void dbg_sum(const char* tag, const T* p, long count, cudaStream_t s) {
     if (verbose() < 3 || !p || count <= 0) return;
+    if (verbose() >= 4) {
+        DbgLog& L = dbg_log();
+        if (!L.d) {
+            cudaMalloc(&L.d, sizeof(unsigned long long) * DbgLog::kCap);
+            cudaMemset(L.d, 0, sizeof(unsigned long long) * DbgLog::kCap);
+        }
+        if ((int)L.names.size() >= DbgLog::kCap) return;
+        const long nw = (long)(sizeof(T) * count / 8);
+        dbg_hash_kernel<<<64, 256, 0, s>>>(reinterpret_cast<const unsigned long long*>(p), nw, L.d + L.names.size());
+        L.names.push_back(tag);
+        return;
+    }
     std::vector<T> h(count);
     cudaStreamSynchronize(s);
     cudaMemcpy(h.data(), p, sizeof(T) * count, cudaMemcpyDeviceToHost);
@@ -408,10 +455,6 @@ template <class T, int MODE>
 void ts_tma_launch(Ctx& c, const T* Krb, int C, long n, const T* x, T* xo, const double* cin, double* out,
                    T* r = nullptr, T* p = nullptr, T* s = nullptr, T* y = nullptr, CGState* st = nullptr) {
     if (C > 128) throw ConfigError("TMA projection limited to 128 columns");
-    if (MODE == 2) {
-        ts_tma_inst<T, 2, 1>(c, Krb, C, n, x, xo, cin, out, r, p, s, y, st);
-        return;
-    }
     const int cpw = (C + 7) / 8;
     if (cpw <= 1)
         ts_tma_inst<T, MODE, 1>(c, Krb, C, n, x, xo, cin, out, r, p, s, y, st);
@@ -622,7 +665,13 @@ void global_tma_chunk(Ctx& c, const T* K, long ld, long ncols, long col0, int cc
     (void)es;
 }
 
-template <class T> bool tma_ok(long ld) { return (ld * (long)sizeof(T)) % 16 == 0; }
+template <class T> bool tma_ok(long ld) {
+    static const int off = [] {
+        const char* e = std::getenv("ROMDOT_NO_GLOBAL_TMA");
+        return e ? std::atoi(e) : 0;
+    }();
+    return !off && (ld * (long)sizeof(T)) % 16 == 0;
+}
 
 // out = op(K)^T x   (x padded)
 template <class T, bool HERM>
@@ -780,15 +829,31 @@ SolveOut recycled_cg(Ctx& c, DevOp& op, const T* U, const T* K, long ncol, const
                                                                                 s, y, st);
                 c.check_launch();
             } else if (ncol > 0) {
+                static const int tma_mask = [] {
+                    const char* e = std::getenv("ROMDOT_TMA_MASK");
+                    return e ? std::atoi(e) : 0;
+                }();
                 cudaEvent_t e1 = samp ? c.prof_start() : nullptr;
-                ts_tma_launch<T, 0>(c, Kit, (int)ncol, n, w, nullptr, nullptr, c1, nullptr, nullptr, nullptr, nullptr,
-                                    st);
+                if (tma_mask & 1)
+                    ts_T_launch<T, false, true>(c, Kit, ncol, ncol, w, n, c1, st);
+                else
+                    ts_tma_launch<T, 0>(c, Kit, (int)ncol, n, w, nullptr, nullptr, c1, nullptr, nullptr, nullptr,
+                                        nullptr, st);
                 if (samp) c.prof_stop(e1, 1, n * es * (ncol + 1.0), iter);
                 cudaEvent_t e2 = samp ? c.prof_start() : nullptr;
-                ts_tma_launch<T, 1>(c, Kit, (int)ncol, n, w, w, c1, c2, nullptr, nullptr, nullptr, nullptr, st);
+                if (tma_mask & 2)
+                    ts_NT_launch<T, false, true>(c, Kit, ncol, ncol, w, w, n, c1, c2, st);
+                else
+                    ts_tma_launch<T, 1>(c, Kit, (int)ncol, n, w, w, c1, c2, nullptr, nullptr, nullptr, nullptr, st);
                 if (samp) c.prof_stop(e2, 2, n * es * (ncol + 2.0), iter);
                 cudaEvent_t e3 = samp ? c.prof_start() : nullptr;
-                ts_tma_launch<T, 2>(c, Kit, (int)ncol, n, w, nullptr, c2, nullptr, r, p, s, y, st);
+                if (tma_mask & 4) {
+                    cg_update<T, true><<<c.grid_for(n, 256, 8), 256, smem_c, c.s>>>(Kit, ncol, (int)ncol, w, n, c2, r,
+                                                                                    p, s, y, st);
+                    c.check_launch();
+                } else {
+                    ts_tma_launch<T, 2>(c, Kit, (int)ncol, n, w, nullptr, c2, nullptr, r, p, s, y, st);
+                }
                 if (samp) c.prof_stop(e3, 3, n * es * (ncol + 9.0), iter);
             } else {
                 cudaEvent_t e3 = samp ? c.prof_start() : nullptr;
@@ -1550,6 +1615,7 @@ void process_system(DevBasis<T>& gb, DevOp& op, long nrhs, const long* bidx, con
         gemm<T, true>(c, gb.Wp(), n, rf, Cpk.template as<T>(), nrhs, Xdev, n, Xdev, n, n, false);
     }
     c.sync();
+    dbg_flush(c.s);
     lap(6);
     VLOG(1,
          "system %d phases (ms): refresh %.1f eig-block %.1f checks %.1f rhs-spaces %.1f solves %.1f appends %.1f "
@@ -1571,22 +1637,27 @@ void process_system(DevBasis<T>& gb, DevOp& op, long nrhs, const long* bidx, con
 // rank = #{R_kk > tol * R_00}; Q (n x rank) spans the retained columns.
 template <class T>
 long rrqr_dev(Ctx& c, long n, long m, const T* A, double tol, bool normalize, std::vector<long>& perm,
-              std::vector<double>& rdiag_out, DevBuf& Qout) {
+              std::vector<double>& rdiag_out, DevBuf& Qout, T* inplace = nullptr) {
     constexpr int W = Sc<T>::W;
     const long ld = n;
-    DevBuf Z, Zb, G, Sp, Sinv, Rrow, pivd, rdg, infod, work, tmp, nrm;
-    Z.ensure(sizeof(T) * n * std::max(1L, m));
-    CK(cudaMemcpyAsync(Z.p, A, sizeof(T) * n * m, cudaMemcpyDeviceToDevice, c.s));
+    DevBuf Zown, Zb, G, Sp, Sinv, Rrow, pivd, rdg, infod, work, tmp, nrm;
+    // Zp: working copy of the candidate columns (or the caller's buffer when in place)
+    T* Zp = inplace;
+    if (!inplace) {
+        Zown.ensure(sizeof(T) * n * std::max(1L, m));
+        CK(cudaMemcpyAsync(Zown.p, A, sizeof(T) * n * m, cudaMemcpyDeviceToDevice, c.s));
+        Zp = Zown.template as<T>();
+    }
     nrm.ensure(sizeof(double) * std::max(1L, m));
     if (normalize && m > 0) {
         for (long j0 = 0; j0 < m; j0 += 1024) {
             const long cc = std::min(1024L, m - j0);
-            col_norms<T><<<c.grid_for(n, 256, 2), 256, sizeof(double) * cc, c.s>>>(Z.template as<T>() + j0 * ld, ld,
+            col_norms<T><<<c.grid_for(n, 256, 2), 256, sizeof(double) * cc, c.s>>>(Zp + j0 * ld, ld,
                                                                                    (int)cc, n, c.red(),
                                                                                    nrm.template as<double>() + j0);
             c.check_launch();
         }
-        scale_columns<T><<<dim3(c.grid_for(n, 256, 1), (unsigned)m), 256, 0, c.s>>>(Z.template as<T>(), ld, (int)m, n,
+        scale_columns<T><<<dim3(c.grid_for(n, 256, 1), (unsigned)m), 256, 0, c.s>>>(Zp, ld, (int)m, n,
                                                                                    nrm.template as<double>());
         c.check_launch();
     }
@@ -1602,7 +1673,7 @@ long rrqr_dev(Ctx& c, long n, long m, const T* A, double tol, bool normalize, st
     while (!done && !remaining.empty()) {
         const long mr = (long)remaining.size();
         G.ensure(sizeof(T) * mr * mr);
-        gram<T, true>(c, Z.template as<T>(), ld, mr, Z.template as<T>(), ld, mr, n, G.template as<T>(), true, work);
+        gram<T, true>(c, Zp, ld, mr, Zp, ld, mr, n, G.template as<T>(), true, work);
         Rrow.ensure(sizeof(T) * mr * mr);
         pivd.ensure(sizeof(int) * mr);
         rdg.ensure(sizeof(double) * mr);
@@ -1639,7 +1710,7 @@ long rrqr_dev(Ctx& c, long n, long m, const T* A, double tol, bool normalize, st
             Zb.ensure(sizeof(T) * n * keep);
             T* ZP = Zb.template as<T>();
             for (long k = 0; k < keep; ++k)
-                CK(cudaMemcpyAsync(ZP + k * ld, Z.template as<T>() + (long)piv[k] * ld, sizeof(T) * n,
+                CK(cudaMemcpyAsync(ZP + k * ld, Zp + (long)piv[k] * ld, sizeof(T) * n,
                                    cudaMemcpyDeviceToDevice, c.s));
             // S_PP (keep x keep upper) from Rrow rows restricted to the picked columns
             std::vector<T> Rh((size_t)keep * mr);
@@ -1679,16 +1750,16 @@ long rrqr_dev(Ctx& c, long n, long m, const T* A, double tol, bool normalize, st
         }
         for (long t = 0; t < (long)rest_local.size(); ++t)
             if (rest_local[t] != t)
-                CK(cudaMemcpyAsync(Z.template as<T>() + t * ld, Z.template as<T>() + rest_local[t] * ld, sizeof(T) * n,
+                CK(cudaMemcpyAsync(Zp + t * ld, Zp + rest_local[t] * ld, sizeof(T) * n,
                                    cudaMemcpyDeviceToDevice, c.s));
         const long nr = (long)rest.size();
         // Z_rest <- (I - Q Q^H)^2 Z_rest against every retained direction so far
         tmp.ensure(sizeof(T) * rank * nr);
         for (int pass = 0; pass < 2; ++pass) {
-            gram<T, true>(c, Qout.template as<T>(), ld, rank, Z.template as<T>(), ld, nr, n, tmp.template as<T>(), false,
+            gram<T, true>(c, Qout.template as<T>(), ld, rank, Zp, ld, nr, n, tmp.template as<T>(), false,
                           work);
-            gemm<T, true>(c, Qout.template as<T>(), ld, rank, tmp.template as<T>(), nr, Z.template as<T>(), ld,
-                          Z.template as<T>(), ld, n, false);
+            gemm<T, true>(c, Qout.template as<T>(), ld, rank, tmp.template as<T>(), nr, Zp, ld,
+                          Zp, ld, n, false);
         }
         remaining = rest;
         ++level;
@@ -2099,6 +2170,11 @@ long rd_basis_cols(rd_basis* b) {
     BASIS_DISPATCH(b, v = B.cols);
     return v;
 }
+int rd_basis_factored(rd_basis* b) {
+    int v = 0;
+    BASIS_DISPATCH(b, v = B.factored ? 1 : 0);
+    return v;
+}
 long rd_basis_eig_block(rd_basis* b) {
     long v = 0;
     BASIS_DISPATCH(b, v = B.ku);
@@ -2113,6 +2189,7 @@ int rd_basis_get(rd_basis* b, int which, void* out) {
     return guard([&] {
         BASIS_DISPATCH(b, {
             using T = std::remove_reference_t<decltype(B.R[0])>;
+            if (which != 0 && !B.factored) throw ConfigError("basis has no image factor yet (refresh first)");
             if (which == 2) {
                 T* o = (T*)out;
                 for (long j = 0; j < B.cols; ++j)
@@ -2375,6 +2452,86 @@ int rd_bench_stencil(rd_op* o, int dtype, long ncols, int iters, double* ms_out)
             run(double{});
         else
             run(cplx{});
+    });
+}
+
+
+// Explicit residual check of a solution block (test_basis.cpp:180-193 at any
+// size): out[j] = ||b_j - A x_j|| / ||b_j|| with b_j = bval[j] e_{bidx[j]}.
+int rd_residual_norms(rd_op* o, int dtype, long nrhs, const long* bidx, const double* bval, const void* X, int where,
+                      double* out) {
+    return guard([&] {
+        Ctx& cx = o->ctx->c;
+        const long n = o->op.d.n;
+        auto run = [&](auto tag) {
+            using T = decltype(tag);
+            Staged Xs(cx, X, sizeof(T) * n * nrhs, where);
+            DevBuf AX, idxd, vald;
+            const long chunk = 16;
+            AX.ensure(sizeof(T) * n * chunk);
+            idxd.ensure(sizeof(long) * nrhs);
+            vald.ensure(sizeof(double) * nrhs);
+            std::vector<double> negval(bval, bval + nrhs);
+            for (auto& v : negval) v = -v;
+            CK(cudaMemcpyAsync(idxd.p, bidx, sizeof(long) * nrhs, cudaMemcpyHostToDevice, cx.s));
+            CK(cudaMemcpyAsync(vald.p, negval.data(), sizeof(double) * nrhs, cudaMemcpyHostToDevice, cx.s));
+            for (long j0 = 0; j0 < nrhs; j0 += chunk) {
+                const long cc = std::min(chunk, nrhs - j0);
+                launch_stencil<T>(cx, o->op.d, (const T*)Xs.p + (size_t)j0 * n, n, nullptr, AX.template as<T>(), n, cc);
+                // A x_j - b_j
+                scatter_add_rhs<T><<<1, 128, 0, cx.s>>>(AX.template as<T>(), n, idxd.template as<long>() + j0,
+                                                       vald.template as<double>() + j0, (int)cc);
+                cx.check_launch();
+                for (long t = 0; t < cc; ++t) {
+                    double* nrm = cx.sc(3);
+                    launch_norms<T>(cx, AX.template as<T>() + (size_t)t * n, n, nrm);
+                    double h;
+                    CK(cudaMemcpyAsync(&h, nrm, sizeof(double), cudaMemcpyDeviceToHost, cx.s));
+                    cx.sync();
+                    out[j0 + t] = std::sqrt(h) / std::fabs(bval[j0 + t]);
+                }
+            }
+        };
+        if (dtype == 0)
+            run(double{});
+        else
+            run(cplx{});
+    });
+}
+
+
+// Algorithm 1 compression of a finished build (acceptance.cpp:368-383, BASELINE
+// RRQR): releases the factorisation workspace (W, K_img, scratch), runs the
+// RRQR directly on V's buffer and leaves the orthonormal compressed basis Q
+// (n x rank) as the basis' V. The basis is final afterwards (no more
+// refresh / process_system).
+int rd_basis_compress(rd_basis* b, double tol, int normalize, long* rank, long* perm, double* rdiag) {
+    return guard([&] {
+        Ctx& cx = b->ctx->c;
+        BASIS_DISPATCH(b, {
+            using T = std::remove_reference_t<decltype(B.R[0])>;
+            const long n = B.n, m = B.cols;
+            B.Wm.~DevBuf();
+            new (&B.Wm) DevBuf();
+            B.K.~DevBuf();
+            new (&B.K) DevBuf();
+            B.Ktmp.~DevBuf();
+            new (&B.Ktmp) DevBuf();
+            B.AW.~DevBuf();
+            new (&B.AW) DevBuf();
+            std::vector<long> pv;
+            std::vector<double> rd_;
+            DevBuf Q;
+            const long rk = rrqr_dev<T>(cx, n, m, B.Vp(), tol, normalize != 0, pv, rd_, Q, B.Vp());
+            if (rk > 0) CK(cudaMemcpyAsync(B.Vp(), Q.p, sizeof(T) * n * rk, cudaMemcpyDeviceToDevice, cx.s));
+            cx.sync();
+            B.cols = rk;
+            B.factored = false;
+            B.markers.assign(rk, kColCorrection);
+            *rank = rk;
+            for (long j = 0; j < m; ++j) perm[j] = pv[j];
+            for (long j = 0; j < m; ++j) rdiag[j] = j < (long)rd_.size() ? rd_[j] : 0.0;
+        });
     });
 }
 

@@ -30,10 +30,10 @@ EXPORTS = [
     "rd_ctx_create", "rd_ctx_destroy", "rd_last_error", "rd_ctx_sync", "rd_ctx_mark", "rd_ctx_elapsed_ms",
     "rd_ctx_launches", "rd_ctx_stream", "rd_ctx_profile", "rd_ctx_prof_get", "rd_op_create", "rd_op_destroy", "rd_op_set_fields", "rd_op_apply",
     "rd_op_lam_max", "rd_recycled_solve", "rd_recycle_space_from_raw", "rd_initial_solutions",
-    "rd_smallest_eigenpairs", "rd_basis_create", "rd_basis_destroy", "rd_basis_cols", "rd_basis_eig_block",
+    "rd_smallest_eigenpairs", "rd_basis_create", "rd_basis_destroy", "rd_basis_cols", "rd_basis_factored", "rd_basis_eig_block",
     "rd_basis_get", "rd_basis_device_ptr", "rd_basis_markers", "rd_basis_space", "rd_basis_refresh",
     "rd_basis_append", "rd_basis_solve_projected", "rd_process_system", "rd_rrqr", "rd_bench_projection",
-    "rd_bench_stencil",
+    "rd_bench_stencil", "rd_residual_norms", "rd_basis_compress",
 ]
 
 
@@ -103,6 +103,8 @@ def load_library(path: Optional[str] = None):
     L.rd_basis_destroy.argtypes = [vp]
     L.rd_basis_cols.argtypes = [vp]
     L.rd_basis_cols.restype = C.c_long
+    L.rd_basis_factored.argtypes = [vp]
+    L.rd_basis_factored.restype = C.c_int
     L.rd_basis_eig_block.argtypes = [vp]
     L.rd_basis_eig_block.restype = C.c_long
     L.rd_basis_get.argtypes = [vp, C.c_int, vp]
@@ -119,6 +121,8 @@ def load_library(path: Optional[str] = None):
     L.rd_rrqr.argtypes = [vp, C.c_int, C.c_long, C.c_long, vp, C.c_double, C.c_int, lp, vp, vp, vp, C.c_int]
     L.rd_bench_projection.argtypes = [vp, C.c_int, C.c_long, C.c_long, C.c_int, vp]
     L.rd_bench_stencil.argtypes = [vp, C.c_int, C.c_long, C.c_int, vp]
+    L.rd_basis_compress.argtypes = [vp, C.c_double, C.c_int, lp, vp, vp]
+    L.rd_residual_norms.argtypes = [vp, C.c_int, C.c_long, vp, vp, vp, C.c_int, vp]
     _LIB = L
     return L
 
@@ -366,15 +370,27 @@ class GlobalBasis:
         return self._get(0, (self.n, self.cols))
 
     @property
+    def factored(self) -> bool:
+        """True once refresh has built the image factor A V = K_img R."""
+        return bool(load_library().rd_basis_factored(self.h))
+
+    @property
     def K_img(self):
+        """Orthonormal image basis; empty (n x 0) before the first refresh, like the reference."""
+        if not self.factored:
+            return np.zeros((self.n, 0), dtype=self.dtype, order="F")
         return self._get(1, (self.n, self.cols))
 
     @property
     def R(self):
+        if not self.factored:
+            return np.zeros((0, 0), dtype=self.dtype, order="F")
         return self._get(2, (self.cols, self.cols))
 
     @property
     def W(self):
+        if not self.factored:
+            return np.zeros((self.n, 0), dtype=self.dtype, order="F")
         return self._get(3, (self.n, self.cols))
 
     @property
@@ -388,6 +404,16 @@ class GlobalBasis:
         out = np.zeros(max(m, 1), dtype=np.int32)
         load_library().rd_basis_space(self.h, j, _p(out))
         return out[:m].tolist()
+
+    def compress(self, tol: float = 1e-10, normalize: bool = True):
+        """Algorithm 1 compression in place (RRQR); V becomes the orthonormal
+        retained basis. Returns (rank, perm, rdiag)."""
+        m = self.cols
+        rank = C.c_long()
+        perm = np.zeros(max(m, 1), dtype=np.int64)
+        rdiag = np.zeros(max(m, 1))
+        _check(load_library().rd_basis_compress(self.h, tol, int(normalize), C.byref(rank), _p(perm), _p(rdiag)))
+        return rank.value, perm[:m], rdiag[:m]
 
     def refresh(self, op: SchurOperator):
         _check(load_library().rd_basis_refresh(self.h, op.h))
@@ -457,6 +483,16 @@ def bench_stencil(op: SchurOperator, ncols: int, iters: int = 10) -> float:
     out = np.zeros(1)
     _check(load_library().rd_bench_stencil(op.h, _dt(op.dtype), ncols, iters, _p(out)))
     return float(out[0])
+
+
+def residual_norms(op: SchurOperator, layout: P.Layout, X, where: int = HOST) -> np.ndarray:
+    """||b_j - A x_j|| / ||b_j|| per column, on the device (X host array or device pointer)."""
+    idx = np.ascontiguousarray(layout.idx, dtype=np.int64)
+    val = np.ascontiguousarray(layout.val, dtype=np.float64)
+    out = np.zeros(layout.n_rhs)
+    xp = _p(_f(X, op.dtype)) if where == HOST else C.c_void_p(X)
+    _check(load_library().rd_residual_norms(op.h, _dt(op.dtype), layout.n_rhs, _p(idx), _p(val), xp, where, _p(out)))
+    return out
 
 
 def rrqr(A: np.ndarray, tol: float = 1e-10, normalize: bool = True, ctx: Optional[Context] = None):

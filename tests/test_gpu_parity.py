@@ -155,8 +155,13 @@ def test_refresh_factorisation_properties(rd):
     U0 = np.linalg.qr(np.random.default_rng(1).standard_normal((d.grid.n, 4)))[0]
     X0, _ = orc.initial_solutions(op_o, d.layout, 1e-8)
     gb = rd.GlobalBasis(U0, X0)
+    # before the first refresh the image factor is empty, as the reference's
+    # default-constructed Kimg_ / R_ (include/romdot/basis.hpp:63)
+    assert not gb.factored
+    assert gb.K_img.shape == (d.grid.n, 0) and gb.R.shape == (0, 0) and gb.W.shape == (d.grid.n, 0)
     op = rd.SchurOperator(d.grid, P.constant_fields(d.grid, d.mu_of(0.0)))
     gb.refresh(op)
+    assert gb.factored
     A = op_o.matrix()
     Kf = A @ gb.V
     K, R = gb.K_img, gb.R
@@ -282,3 +287,36 @@ def test_build_deterministic_across_interleaved_builds(rd):
         rows, V = build(c, U0, X0)
         assert rows == ref_rows
         assert V.tobytes() == ref_V.tobytes()
+
+
+def test_device_residual_norms_match_numpy(rd):
+    c = P.CONFIGS["T3c"]
+    g, lay = c.grid, c.layout()
+    f = c.fields(1, 0.1)
+    op_o = orc.Operator.grid(g, f, c.dtype)
+    rng = np.random.default_rng(3)
+    X = (rng.standard_normal((g.n, lay.n_rhs)) + 1j * rng.standard_normal((g.n, lay.n_rhs))).astype(c.dtype)
+    B = lay.dense(g.n, c.dtype)
+    want = np.linalg.norm(op_o.apply(X) - B, axis=0) / np.linalg.norm(B, axis=0)
+    got = rd.residual_norms(rd.SchurOperator(g, f, c.dtype), lay, X)
+    assert np.allclose(got, want, rtol=1e-12)
+
+
+def test_basis_compress_in_place(rd):
+    c = P.CONFIGS["T2"]
+    g, lay = c.grid, c.layout()
+    U0, X0 = _shared_seed(c, g, lay)
+    gb = rd.GlobalBasis(U0, X0)
+    for s, (pt, w) in enumerate(c.systems(), start=1):
+        rd.process_system(gb, rd.SchurOperator(g, c.fields(pt, w)), lay, c.tol, s)
+    V = gb.V
+    ro, *_ = orc.qrcp(V, 1e-10, normalize=True)
+    rank, perm, rdiag = gb.compress(1e-10)
+    assert rank == ro == gb.cols
+    Q = gb.V
+    assert np.linalg.norm(Q.T @ Q - np.eye(rank)) <= 1e-10
+    Vn = V / np.linalg.norm(V, axis=0)
+    Un, sn, _ = np.linalg.svd(Vn, full_matrices=False)
+    Ut = Un[:, sn >= 1e-6 * sn[0]]
+    s = np.linalg.svd(Q.T @ Ut, compute_uv=False)
+    assert np.sqrt(max(0.0, 1 - s.min() ** 2)) <= 1e-6
