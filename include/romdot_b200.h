@@ -29,6 +29,7 @@ extern "C" {
 typedef struct rd_ctx rd_ctx;     /* device, stream, reduction workspace */
 typedef struct rd_op rd_op;       /* Schur operator A~(p) on the device */
 typedef struct rd_basis rd_basis; /* GlobalBasis + PerRhsSpaces on the device */
+typedef struct rd_rom rd_rom;     /* ReducedModel: V and the reduced-system workspace */
 
 typedef struct rd_report {
     int iterations;      /* SolveReport::iterations   (include/romdot/krylov.hpp:10-15) */
@@ -138,6 +139,37 @@ int rd_rrqr(rd_ctx* ctx, int dtype, long n, long m, const void* A, double tol, i
  * factorisation workspace, RRQR on V's own buffer, V <- orthonormal Q
  * (n x rank). perm / rdiag have basis-cols entries. The basis is final.   */
 int rd_basis_compress(rd_basis* b, double tol, int normalize, long* rank, long* perm, double* rdiag);
+
+/* -------------------------------------------------------- reduced model --- */
+/* ReducedModel (include/romdot/rom.hpp:12-41, src/rom.cpp:9-67) on the device.
+ * V (n x r, column-major) is copied for where = 0 and BORROWED for where = 1
+ * (e.g. rd_basis_device_ptr of a compressed basis; it must outlive the rom).
+ * The constructor's E_r = V^T V SPD check (rom.cpp:12-14) is the Cholesky of
+ * V^H V: status 3 "basis is numerically rank deficient" when it fails.
+ * Projections are bilinear (V^T A V, V^T B, V^T C) for complex bases, which
+ * keeps the reduced system complex symmetric (SURVEY §8 hard parts).      */
+int rd_rom_create(rd_ctx* ctx, int dtype, long n, long r, const void* V, int where, rd_rom** out);
+void rd_rom_destroy(rd_rom* rom);
+long rd_rom_order(rd_rom* rom);
+/* E_r = V^T V (ReducedModel::E_r, rom.hpp:24), r x r.                     */
+int rd_rom_E(rd_rom* rom, void* E, int where);
+/* A_r(p) = sym(V^T A(p) V) for the operator's current fields
+ * (ReducedModel::reduced_system, rom.cpp:21-27), r x r.                    */
+int rd_rom_reduced_system(rd_rom* rom, rd_op* op, void* Ar, int where);
+/* Psi_r = C_r^T A_r^-1 B_r, n_det x n_src (ReducedModel::transfer,
+ * rom.cpp:29-35). B~ / C~ columns have one nonzero each (grid.cpp:146-158),
+ * passed as host (index, value) pairs; LU with partial pivoting replaces the
+ * LDLT (status 3 on a singular reduced system, like rom.cpp:32-33).        */
+int rd_rom_transfer(rd_rom* rom, rd_op* op, long n_src, const long* src_idx, const double* src_val, long n_det,
+                    const long* det_idx, const double* det_val, void* Psi, int where);
+/* Reduced Jacobian (ReducedModel::jacobian, rom.cpp:37-67): column k =
+ * scale * vec(sum_t w_t (V Z)[i_t,:]^T (V Y)[i_t,:]) with Y = A_r^-1 B_r,
+ * Z = A_r^-1 C_r and the k-th parameter's compact support (i_t, w_t) in CSR
+ * form (sup_ptr[n_par+1], sup_idx, sup_val: absorption_jacobian's SparseDiag
+ * lists). The reference's scale is -h^2. J is (n_det*n_src) x n_par.      */
+int rd_rom_jacobian(rd_rom* rom, rd_op* op, long n_src, const long* src_idx, const double* src_val, long n_det,
+                    const long* det_idx, const double* det_val, long n_par, const long* sup_ptr, const long* sup_idx,
+                    const double* sup_val, double scale, void* J, int where);
 
 /* ------------------------------------------------------- bench hooks --- */
 /* Mean device ms per launch of the three inner-iteration projection kernels

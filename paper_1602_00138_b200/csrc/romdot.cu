@@ -23,6 +23,7 @@
 #include "dense.cuh"
 #include "kernels.cuh"
 #include "ts_tma.cuh"
+#include "rom.cuh"
 
 namespace rd {
 
@@ -1776,6 +1777,173 @@ long rrqr_dev(Ctx& c, long n, long m, const T* A, double tol, bool normalize, st
 // ================================================================ C ABI ===
 using namespace rd;
 
+// ------------------------------------------------------- reduced model ---
+// ReducedModel (src/rom.cpp:9-67) on the device, one-sided bilinear projection
+// onto V: A_r(p) = V^T A(p) V assembled per call by a
+// multi-column stencil pass + Gram in 64-column chunks (variable D makes the
+// reference's affine A*_r + V^T diag(mu) V split unavailable; the cost is the
+// same O(n r^2)), symmetrised, LU with partial pivoting, multi-RHS solve.
+namespace rd {
+template <class T> struct DevRom {
+    Ctx* ctx = nullptr;
+    long n = 0, r = 0;
+    DevBuf own;  // owned copy when V came from the host; else V is borrowed
+    const T* V = nullptr;
+    DevBuf E, Ar, AV, piv, info, B, Cr, WY, WZ, G, Sinv, gwork, ix, vx, Pd;
+    static constexpr long kChunk = 64;
+
+    void init(Ctx& c, long n_, long r_, const void* Vin, int where) {
+        ctx = &c;
+        n = n_;
+        r = r_;
+        if (r <= 0 || n <= 0 || r > n) throw ConfigError("rom: need 0 < r <= n");
+        if (r > 2048) throw ConfigError("rom: order limited to 2048");
+        if (where == 1) {
+            V = static_cast<const T*>(Vin);
+        } else {
+            own.ensure(sizeof(T) * n * r);
+            CK(cudaMemcpyAsync(own.p, Vin, sizeof(T) * n * r, cudaMemcpyHostToDevice, c.s));
+            V = own.template as<T>();
+        }
+        // E_r = V^T V (rom.cpp:11); the rank check is the Cholesky of the
+        // Hermitian Gram V^H V (= V^T V for real bases, rom.cpp:12-14)
+        E.ensure(sizeof(T) * r * r);
+        gram<T, false>(c, V, n, r, V, n, r, n, E.template as<T>(), true, gwork);
+        G.ensure(sizeof(T) * r * r);
+        Sinv.ensure(sizeof(T) * r * r);
+        gram<T, true>(c, V, n, r, V, n, r, n, G.template as<T>(), true, gwork);
+        const CholInfo ci = chol_inv<T, true>(c, G.template as<T>(), Sinv.template as<T>(), r, false);
+        if (ci.bad) throw SolverError("rom: basis is numerically rank deficient (E_r not SPD)");
+    }
+
+    // A_r = sym(V^T A V) into Ar (device, ld r)
+    void reduced_system(const OpDev& op) {
+        Ctx& c = *ctx;
+        if (op.n != n) throw ConfigError("rom: operator dimension mismatch");
+        Ar.ensure(sizeof(T) * r * r);
+        AV.ensure(sizeof(T) * n * std::min(r, kChunk));
+        T* A = Ar.template as<T>();
+        for (long c0 = 0; c0 < r; c0 += kChunk) {
+            const long cw = std::min(kChunk, r - c0);
+            launch_stencil<T>(c, op, V + (size_t)c0 * n, n, nullptr, AV.template as<T>(), n, cw);
+            gram<T, false>(c, V, n, r, AV.template as<T>(), n, cw, n, A + (size_t)c0 * r, false, gwork);
+        }
+        rom_symmetrize<T><<<c.grid_for(r * r, 256, 2), 256, 0, c.s>>>(A, (int)r);
+        c.check_launch();
+    }
+
+    // in-place LU of Ar (partial pivoting); throws on an exactly singular pivot
+    void factor() {
+        Ctx& c = *ctx;
+        piv.ensure(sizeof(int) * r);
+        info.ensure(sizeof(int));
+        CK(cudaMemsetAsync(info.p, 0, sizeof(int), c.s));
+        T* A = Ar.template as<T>();
+        for (long k = 0; k < r; ++k) {
+            lu_pivot_col<T><<<1, 1024, 0, c.s>>>(A, (int)r, (int)k, piv.template as<int>(), info.template as<int>());
+            c.check_launch();
+            const long m = r - k - 1;
+            if (m > 0) {
+                lu_update<T><<<c.grid_for(m * m, 256, 4), 256, 0, c.s>>>(A, (int)r, (int)k);
+                c.check_launch();
+            }
+        }
+        int h = 0;
+        CK(cudaMemcpyAsync(&h, info.p, sizeof(int), cudaMemcpyDeviceToHost, c.s));
+        c.sync();
+        if (h) throw SolverError("rom: reduced system factorization failed");
+    }
+
+    void solve(T* X, long nrhs) {
+        Ctx& c = *ctx;
+        if (nrhs <= 0) return;
+        const size_t smem = sizeof(T) * r;
+        lu_solve<T><<<(unsigned)nrhs, 512, smem, c.s>>>(Ar.template as<T>(), (int)r, piv.template as<int>(), X, r);
+        c.check_launch();
+    }
+
+    // B_r = V^T B for a layout block with one nonzero per column (grid.cpp:146-158)
+    void gather(const long* idx, const double* val, long m, T* out) {
+        Ctx& c = *ctx;
+        if (m <= 0) return;
+        ix.ensure(sizeof(long) * m);
+        vx.ensure(sizeof(double) * m);
+        CK(cudaMemcpyAsync(ix.p, idx, sizeof(long) * m, cudaMemcpyHostToDevice, c.s));
+        CK(cudaMemcpyAsync(vx.p, val, sizeof(double) * m, cudaMemcpyHostToDevice, c.s));
+        for (long j = 0; j < m; ++j)
+            if (idx[j] < 0 || idx[j] >= n) throw ConfigError("rom: layout index out of range");
+        row_gather_multi<T, false><<<c.grid_for(r * m, 256, 4), 256, 0, c.s>>>(
+            V, n, 0, (int)r, ix.template as<long>(), vx.template as<double>(), (int)m, 1.0, out, r);
+        c.check_launch();
+        c.sync();  // ix / vx are reused by the next gather
+    }
+
+    // Y = A_r^-1 B_r (and Z = A_r^-1 C_r when want_z), C_r kept in Cr
+    void solve_layout(const OpDev& op, long ns, const long* sidx, const double* sval, long nd, const long* didx,
+                      const double* dval, bool want_z) {
+        reduced_system(op);
+        factor();
+        B.ensure(sizeof(T) * r * (ns + nd));
+        Cr.ensure(sizeof(T) * r * std::max(1L, nd));
+        gather(sidx, sval, ns, B.template as<T>());
+        gather(didx, dval, nd, Cr.template as<T>());
+        if (want_z)
+            CK(cudaMemcpyAsync(B.template as<T>() + (size_t)ns * r, Cr.p, sizeof(T) * r * nd, cudaMemcpyDeviceToDevice,
+                               ctx->s));
+        solve(B.template as<T>(), want_z ? ns + nd : ns);
+    }
+
+    // Psi_r = C_r^T Y (n_det x n_src, rom.cpp:29-35)
+    void transfer(const OpDev& op, long ns, const long* sidx, const double* sval, long nd, const long* didx,
+                  const double* dval, T* Psi) {
+        solve_layout(op, ns, sidx, sval, nd, didx, dval, false);
+        gram<T, false>(*ctx, Cr.template as<T>(), r, nd, B.template as<T>(), r, ns, r, Psi, false, gwork);
+    }
+
+    // J[:, k] = scale * vec(sum_t w_t (V Z)[i_t,:]^T (V Y)[i_t,:])   (rom.cpp:37-67)
+    void jacobian(const OpDev& op, long ns, const long* sidx, const double* sval, long nd, const long* didx,
+                  const double* dval, long npar, const long* ptr, const long* sidx_k, const double* sval_k,
+                  double scale, T* J) {
+        Ctx& c = *ctx;
+        solve_layout(op, ns, sidx, sval, nd, didx, dval, true);
+        WY.ensure(sizeof(T) * n * ns);
+        WZ.ensure(sizeof(T) * n * std::max(1L, nd));
+        gemm<T, false>(c, V, n, r, B.template as<T>(), ns, nullptr, 0, WY.template as<T>(), n, n, false);
+        gemm<T, false>(c, V, n, r, B.template as<T>() + (size_t)ns * r, nd, nullptr, 0, WZ.template as<T>(), n, n,
+                       false);
+        if (npar <= 0) return;
+        const long nnz = ptr[npar];
+        for (long k = 0; k < npar; ++k)
+            if (ptr[k + 1] < ptr[k]) throw ConfigError("rom: support pointers not monotone");
+        for (long t = 0; t < nnz; ++t)
+            if (sidx_k[t] < 0 || sidx_k[t] >= n) throw ConfigError("rom: support index out of range");
+        Pd.ensure(sizeof(long) * (npar + 1) + sizeof(long) * std::max(1L, nnz) + sizeof(double) * std::max(1L, nnz));
+        long* dptr = Pd.template as<long>();
+        long* didx2 = dptr + (npar + 1);
+        double* dval2 = reinterpret_cast<double*>(didx2 + std::max(1L, nnz));
+        CK(cudaMemcpyAsync(dptr, ptr, sizeof(long) * (npar + 1), cudaMemcpyHostToDevice, c.s));
+        if (nnz > 0) {
+            CK(cudaMemcpyAsync(didx2, sidx_k, sizeof(long) * nnz, cudaMemcpyHostToDevice, c.s));
+            CK(cudaMemcpyAsync(dval2, sval_k, sizeof(double) * nnz, cudaMemcpyHostToDevice, c.s));
+        }
+        for (long k0 = 0; k0 < npar; k0 += 65535) {
+            const long kk = std::min(65535L, npar - k0);
+            dim3 grid((unsigned)std::max(1L, std::min<long>((ns * nd + 255) / 256, 64)), (unsigned)kk);
+            rom_jacobian<T><<<grid, 256, 0, c.s>>>(WY.template as<T>(), WZ.template as<T>(), n, (int)ns, (int)nd,
+                                                   dptr + k0, didx2, dval2, scale, J + (size_t)k0 * ns * nd, ns * nd);
+            c.check_launch();
+        }
+        c.sync();
+    }
+};
+
+struct RomHandle {
+    int dtype = 0;
+    std::unique_ptr<DevRom<double>> r;
+    std::unique_ptr<DevRom<cplx>> c;
+};
+}  // namespace rd
+
 struct rd_ctx {
     Ctx c;
 };
@@ -2531,6 +2699,111 @@ int rd_basis_compress(rd_basis* b, double tol, int normalize, long* rank, long* 
             *rank = rk;
             for (long j = 0; j < m; ++j) perm[j] = pv[j];
             for (long j = 0; j < m; ++j) rdiag[j] = j < (long)rd_.size() ? rd_[j] : 0.0;
+        });
+    });
+}
+
+struct rd_rom {
+    rd_ctx* ctx;
+    rd::RomHandle h;
+};
+
+#define ROM_DISPATCH(rm, ...)        \
+    if ((rm)->h.dtype == 0) {        \
+        auto& M = *(rm)->h.r;        \
+        __VA_ARGS__;                 \
+    } else {                         \
+        auto& M = *(rm)->h.c;        \
+        __VA_ARGS__;                 \
+    }
+
+static void rom_check_op(rd_rom* rm, rd_op* op) {
+    if (!op->op.have_fields) throw rd::ConfigError("operator: fields not set");
+    if (rm->h.dtype == 0 && op->op.d.shift != 0.0)
+        throw rd::ConfigError("rom: real reduced model with a complex (omega != 0) operator");
+}
+
+int rd_rom_create(rd_ctx* ctx, int dtype, long n, long r, const void* V, int where, rd_rom** out) {
+    return guard([&] {
+        if (dtype != 0 && dtype != 1) throw rd::ConfigError("rom: dtype must be 0 (f64) or 1 (c128)");
+        if (!V) throw rd::ConfigError("rom: V is null");
+        auto rm = std::make_unique<rd_rom>();
+        rm->ctx = ctx;
+        rm->h.dtype = dtype;
+        if (dtype == 0) {
+            rm->h.r = std::make_unique<rd::DevRom<double>>();
+            rm->h.r->init(ctx->c, n, r, V, where);
+        } else {
+            rm->h.c = std::make_unique<rd::DevRom<cplx>>();
+            rm->h.c->init(ctx->c, n, r, V, where);
+        }
+        *out = rm.release();
+    });
+}
+
+void rd_rom_destroy(rd_rom* rm) { delete rm; }
+
+long rd_rom_order(rd_rom* rm) {
+    long v = 0;
+    ROM_DISPATCH(rm, v = M.r);
+    return v;
+}
+
+int rd_rom_E(rd_rom* rm, void* E, int where) {
+    return guard([&] {
+        ROM_DISPATCH(rm, {
+            using T = std::remove_const_t<std::remove_pointer_t<decltype(M.V)>>;
+            Out es(rm->ctx->c, E, sizeof(T) * M.r * M.r, where);
+            CK(cudaMemcpyAsync(es.p, M.E.p, sizeof(T) * M.r * M.r, cudaMemcpyDeviceToDevice, rm->ctx->c.s));
+            es.finish();
+            if (where == 1) rm->ctx->c.sync();
+        });
+    });
+}
+
+int rd_rom_reduced_system(rd_rom* rm, rd_op* op, void* Ar, int where) {
+    return guard([&] {
+        rom_check_op(rm, op);
+        ROM_DISPATCH(rm, {
+            using T = std::remove_const_t<std::remove_pointer_t<decltype(M.V)>>;
+            M.reduced_system(op->op.d);
+            Out as(rm->ctx->c, Ar, sizeof(T) * M.r * M.r, where);
+            CK(cudaMemcpyAsync(as.p, M.Ar.p, sizeof(T) * M.r * M.r, cudaMemcpyDeviceToDevice, rm->ctx->c.s));
+            as.finish();
+            if (where == 1) rm->ctx->c.sync();
+        });
+    });
+}
+
+int rd_rom_transfer(rd_rom* rm, rd_op* op, long n_src, const long* src_idx, const double* src_val, long n_det,
+                    const long* det_idx, const double* det_val, void* Psi, int where) {
+    return guard([&] {
+        rom_check_op(rm, op);
+        if (n_src <= 0 || n_det <= 0) throw rd::ConfigError("rom: need sources and detectors");
+        ROM_DISPATCH(rm, {
+            using T = std::remove_const_t<std::remove_pointer_t<decltype(M.V)>>;
+            Out ps(rm->ctx->c, Psi, sizeof(T) * n_det * n_src, where);
+            M.transfer(op->op.d, n_src, src_idx, src_val, n_det, det_idx, det_val, static_cast<T*>(ps.p));
+            ps.finish();
+            if (where == 1) rm->ctx->c.sync();
+        });
+    });
+}
+
+int rd_rom_jacobian(rd_rom* rm, rd_op* op, long n_src, const long* src_idx, const double* src_val, long n_det,
+                    const long* det_idx, const double* det_val, long n_par, const long* sup_ptr, const long* sup_idx,
+                    const double* sup_val, double scale, void* J, int where) {
+    return guard([&] {
+        rom_check_op(rm, op);
+        if (n_src <= 0 || n_det <= 0) throw rd::ConfigError("rom: need sources and detectors");
+        if (n_par < 0 || (n_par > 0 && !sup_ptr)) throw rd::ConfigError("rom: bad parameter supports");
+        ROM_DISPATCH(rm, {
+            using T = std::remove_const_t<std::remove_pointer_t<decltype(M.V)>>;
+            Out js(rm->ctx->c, J, sizeof(T) * n_src * n_det * std::max(1L, n_par), where);
+            M.jacobian(op->op.d, n_src, src_idx, src_val, n_det, det_idx, det_val, n_par, sup_ptr, sup_idx, sup_val,
+                       scale, static_cast<T*>(js.p));
+            js.finish();
+            if (where == 1) rm->ctx->c.sync();
         });
     });
 }

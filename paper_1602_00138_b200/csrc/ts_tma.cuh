@@ -93,7 +93,6 @@ __global__ void __launch_bounds__(TMA_THREADS, 1)
     uint64_t* full = reinterpret_cast<uint64_t*>(smem + L.off_bar);
     uint64_t* empty = full + S;
     T* part = reinterpret_cast<T*>(smem + L.off_part);
-    T* xs2 = reinterpret_cast<T*>(smem + L.off_xs);
     T* cw = reinterpret_cast<T*>(smem + L.off_cw);
     double* vals = reinterpret_cast<double*>(smem + L.off_vals);
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;

@@ -33,7 +33,8 @@ EXPORTS = [
     "rd_smallest_eigenpairs", "rd_basis_create", "rd_basis_destroy", "rd_basis_cols", "rd_basis_factored", "rd_basis_eig_block",
     "rd_basis_get", "rd_basis_device_ptr", "rd_basis_markers", "rd_basis_space", "rd_basis_refresh",
     "rd_basis_append", "rd_basis_solve_projected", "rd_process_system", "rd_rrqr", "rd_bench_projection",
-    "rd_bench_stencil", "rd_residual_norms", "rd_basis_compress",
+    "rd_bench_stencil", "rd_residual_norms", "rd_basis_compress", "rd_rom_create", "rd_rom_destroy",
+    "rd_rom_order", "rd_rom_E", "rd_rom_reduced_system", "rd_rom_transfer", "rd_rom_jacobian",
 ]
 
 
@@ -123,6 +124,15 @@ def load_library(path: Optional[str] = None):
     L.rd_bench_stencil.argtypes = [vp, C.c_int, C.c_long, C.c_int, vp]
     L.rd_basis_compress.argtypes = [vp, C.c_double, C.c_int, lp, vp, vp]
     L.rd_residual_norms.argtypes = [vp, C.c_int, C.c_long, vp, vp, vp, C.c_int, vp]
+    L.rd_rom_create.argtypes = [vp, C.c_int, C.c_long, C.c_long, vp, C.c_int, C.POINTER(vp)]
+    L.rd_rom_destroy.argtypes = [vp]
+    L.rd_rom_order.argtypes = [vp]
+    L.rd_rom_order.restype = C.c_long
+    L.rd_rom_E.argtypes = [vp, vp, C.c_int]
+    L.rd_rom_reduced_system.argtypes = [vp, vp, vp, C.c_int]
+    L.rd_rom_transfer.argtypes = [vp, vp, C.c_long, vp, vp, C.c_long, vp, vp, vp, C.c_int]
+    L.rd_rom_jacobian.argtypes = [vp, vp, C.c_long, vp, vp, C.c_long, vp, vp, C.c_long, vp, vp, vp, C.c_double,
+                                  vp, C.c_int]
     _LIB = L
     return L
 
@@ -506,3 +516,79 @@ def rrqr(A: np.ndarray, tol: float = 1e-10, normalize: bool = True, ctx: Optiona
     _check(load_library().rd_rrqr(ctx.h, _dt(A.dtype), n, m, _p(A), tol, int(normalize), C.byref(rank), _p(perm),
                                   _p(rdiag), _p(Q), HOST))
     return rank.value, perm, rdiag, Q[:, : rank.value].copy()
+
+
+class ReducedModel:
+    """ReducedModel (include/romdot/rom.hpp:12-41, src/rom.cpp:9-67) on the device.
+
+    V: host array (copied) or, with where=DEVICE, a device pointer that is
+    borrowed and must outlive the model (e.g. a compressed GlobalBasis's V).
+    Complex bases use bilinear projections (V^T A V, V^T B, V^T C)."""
+
+    def __init__(self, V, dtype=None, ctx: Optional[Context] = None, where: int = HOST, n: int = 0, r: int = 0):
+        self.ctx = ctx or default_context()
+        if where == HOST:
+            V = np.asfortranarray(V, dtype=dtype or np.asarray(V).dtype)
+            self.dtype = V.dtype
+            n, r = V.shape
+            vp = _p(V)
+        else:
+            self.dtype = np.dtype(dtype)
+            vp = C.c_void_p(V)
+        self.n, self.r = int(n), int(r)
+        h = C.c_void_p()
+        _check(load_library().rd_rom_create(self.ctx.h, _dt(self.dtype), self.n, self.r, vp, where, C.byref(h)))
+        self.h = h
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            load_library().rd_rom_destroy(self.h)
+            self.h = None
+
+    def order(self) -> int:
+        return load_library().rd_rom_order(self.h)
+
+    @property
+    def E_r(self) -> np.ndarray:
+        out = np.zeros((self.r, self.r), dtype=self.dtype, order="F")
+        _check(load_library().rd_rom_E(self.h, _p(out), HOST))
+        return out
+
+    def reduced_system(self, op: SchurOperator) -> np.ndarray:
+        out = np.zeros((self.r, self.r), dtype=self.dtype, order="F")
+        _check(load_library().rd_rom_reduced_system(self.h, op.h, _p(out), HOST))
+        return out
+
+    @staticmethod
+    def _split(layout: P.Layout):
+        idx = np.ascontiguousarray(layout.idx, dtype=np.int64)
+        val = np.ascontiguousarray(layout.val, dtype=np.float64)
+        s = layout.n_src
+        return (np.ascontiguousarray(idx[:s]), np.ascontiguousarray(val[:s]),
+                np.ascontiguousarray(idx[s:]), np.ascontiguousarray(val[s:]))
+
+    def transfer(self, op: SchurOperator, layout: P.Layout) -> np.ndarray:
+        """Psi_r = C_r^T A_r^-1 B_r, n_det x n_src."""
+        si, sv, di, dv = self._split(layout)
+        out = np.zeros((layout.n_det, layout.n_src), dtype=self.dtype, order="F")
+        _check(load_library().rd_rom_transfer(self.h, op.h, layout.n_src, _p(si), _p(sv), layout.n_det, _p(di),
+                                              _p(dv), _p(out), HOST))
+        return out
+
+    def jacobian(self, op: SchurOperator, layout: P.Layout, supports, scale: float) -> np.ndarray:
+        """supports: one (index array, value array) pair per parameter (the
+        reference's SparseDiag from absorption_jacobian); column k of the result
+        is scale * vec(sum_t w_t (V Z)[i_t,:]^T (V Y)[i_t,:]), (n_det*n_src) x n_par."""
+        si, sv, di, dv = self._split(layout)
+        ptr = np.zeros(len(supports) + 1, dtype=np.int64)
+        for k, (ix, _) in enumerate(supports):
+            ptr[k + 1] = ptr[k] + len(ix)
+        sidx = np.ascontiguousarray(np.concatenate([np.asarray(ix, dtype=np.int64) for ix, _ in supports])
+                                    if supports else np.zeros(1, dtype=np.int64))
+        sval = np.ascontiguousarray(np.concatenate([np.asarray(w, dtype=np.float64) for _, w in supports])
+                                    if supports else np.zeros(1))
+        out = np.zeros((layout.n_det * layout.n_src, max(1, len(supports))), dtype=self.dtype, order="F")
+        _check(load_library().rd_rom_jacobian(self.h, op.h, layout.n_src, _p(si), _p(sv), layout.n_det, _p(di),
+                                              _p(dv), len(supports), _p(ptr), _p(sidx), _p(sval), float(scale),
+                                              _p(out), HOST))
+        return out[:, : len(supports)]

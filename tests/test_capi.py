@@ -17,7 +17,7 @@ def so():
 
 def header_symbols():
     txt = open(os.path.join(ROOT, "include", "romdot_b200.h")).read()
-    return sorted(set(re.findall(r"\b(rd_[a-z_]+)\s*\(", txt)))
+    return sorted(set(re.findall(r"\b(rd_[A-Za-z0-9_]+)\s*\(", txt)))
 
 
 def test_header_declares_expected_surface():
@@ -29,7 +29,7 @@ def test_header_declares_expected_surface():
 
 def test_library_exports_every_header_symbol(so):
     out = subprocess.run(["nm", "-D", "--defined-only", so], capture_output=True, text=True).stdout
-    exported = set(re.findall(r"\bT (rd_[a-z_]+)\b", out))
+    exported = set(re.findall(r"\bT (rd_[A-Za-z0-9_]+)\b", out))
     missing = [s for s in header_symbols() if s not in exported]
     assert not missing, missing
 

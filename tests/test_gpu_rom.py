@@ -1,0 +1,128 @@
+"""Device ReducedModel (reference src/rom.cpp:9-67,
+tests/test_rom.cpp, acceptance C3) against numpy on the same inputs.
+
+* E_r, A_r = sym(V^T A V), Psi_r = C_r^T A_r^-1 B_r and the support-row
+  Jacobian, real and complex (bilinear projections), <= 1e-10 relative;
+* the rank-deficiency error of the constructor (rom.cpp:12-14);
+* interpolation: the ROM of a device-built, device-compressed basis matches
+  the full-order transfer at the build's own parameters (acceptance.cpp
+  C3 `:252-274`, tolerance 1e-5 there).
+"""
+import numpy as np
+import pytest
+
+import oracle as orc
+from paper_1602_00138_b200 import problem as P
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def rd():
+    from paper_1602_00138_b200 import romdot
+    return romdot
+
+
+def _orth(n, r, cplx, seed):
+    g = np.random.default_rng(seed)
+    A = g.standard_normal((n, r))
+    if cplx:
+        A = A + 1j * g.standard_normal((n, r))
+    return np.linalg.qr(A)[0]
+
+
+def _supports(n, npar, seed):
+    g = np.random.default_rng(seed)
+    out = []
+    for k in range(npar):
+        m = int(g.integers(1, n // 4))
+        ix = np.sort(g.choice(n, size=m, replace=False))
+        out.append((ix, g.uniform(0.1, 1.0, m)))
+    out.append((np.zeros(0, dtype=np.int64), np.zeros(0)))  # empty support -> zero column (rom.cpp:52-55)
+    return out
+
+
+def _expected(V, A, B, C, supports, scale):
+    Ar = V.T @ (A @ V)
+    Ar = 0.5 * (Ar + Ar.T)
+    Y = np.linalg.solve(Ar, V.T @ B)
+    Z = np.linalg.solve(Ar, V.T @ C)
+    Psi = (V.T @ C).T @ Y
+    WY, WZ = V @ Y, V @ Z
+    J = np.zeros((C.shape[1] * B.shape[1], len(supports)), dtype=np.result_type(V, A))
+    for k, (ix, w) in enumerate(supports):
+        M = (WZ[ix] * w[:, None]).T @ WY[ix]  # n_det x n_src (rom.cpp:60)
+        J[:, k] = scale * M.ravel(order="F")  # Eigen column-major vec (rom.cpp:61)
+    return Ar, Psi, J
+
+
+def _rel(a, b):
+    return np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300)
+
+
+@pytest.mark.parametrize("name", ["T3", "T3c", "T2c"])
+def test_rom_matches_numpy(rd, name):
+    c = P.CONFIGS[name]
+    g, lay = c.grid, c.layout()
+    pt, w = c.systems()[-1]
+    f = c.fields(pt, w)
+    A = orc.Operator.grid(g, f, c.dtype).matrix()
+    Bc = lay.dense(g.n)
+    B, C = Bc[:, : lay.n_src], Bc[:, lay.n_src:]
+    V = _orth(g.n, 24, c.complex, 7)
+    rom = rd.ReducedModel(V)
+    op = rd.SchurOperator(g, f, c.dtype)
+    sup = _supports(g.n, 3, 11)
+    scale = -g.h ** 2
+    Ar, Psi, J = _expected(V, A, B, C, sup, scale)
+    assert rom.order() == 24
+    assert _rel(rom.E_r, V.T @ V) <= 1e-13
+    assert _rel(rom.reduced_system(op), Ar) <= 1e-12
+    assert _rel(rom.transfer(op, lay), Psi) <= 1e-10
+    Jd = rom.jacobian(op, lay, sup, scale)
+    assert Jd.shape == J.shape
+    assert _rel(Jd, J) <= 1e-10
+    assert np.all(Jd[:, -1] == 0)
+
+
+def test_rom_rank_deficient_basis_is_solver_error(rd):
+    c = P.CONFIGS["T3"]
+    V = _orth(c.grid.n, 6, False, 3)
+    V = np.concatenate([V, V[:, :1]], axis=1)
+    with pytest.raises(rd.SolverError, match="rank deficient"):
+        rd.ReducedModel(V)
+
+
+def test_rom_real_model_rejects_complex_operator(rd):
+    c = P.CONFIGS["T3c"]
+    rom = rd.ReducedModel(_orth(c.grid.n, 5, False, 2))
+    op = rd.SchurOperator(c.grid, c.fields(1, 0.1), np.complex128)
+    with pytest.raises(rd.ConfigError):
+        rom.transfer(op, c.layout())
+
+
+@pytest.mark.parametrize("name", ["T3", "T3c"])
+def test_rom_of_compressed_device_basis_interpolates_fom(rd, name):
+    """acceptance.cpp C3 (:252-274): ROM transfer at the basis parameters
+    equals the FOM transfer (reference tolerance 1e-5)."""
+    c = P.CONFIGS[name]
+    g, lay = c.grid, c.layout()
+    op0r = rd.SchurOperator(g, c.fields(0), np.float64)
+    op0 = rd.SchurOperator(g, c.fields(0), c.dtype)
+    gb, _, _, _ = rd.init_basis(op0, op0r, lay, c.k, c.tol, c.cap)
+    for s, (pt, w) in enumerate(c.systems(), start=1):
+        rd.process_system(gb, rd.SchurOperator(g, c.fields(pt, w), c.dtype), lay, c.tol, s, want_X=False)
+    rank, _, _ = gb.compress(1e-10)
+    assert rank == gb.cols
+    from paper_1602_00138_b200 import romdot as R
+    vptr = R.load_library().rd_basis_device_ptr(gb.h, 0)
+    rom = rd.ReducedModel(vptr, dtype=c.dtype, where=rd.DEVICE, n=g.n, r=rank)
+    Bc = lay.dense(g.n)
+    B, C = Bc[:, : lay.n_src], Bc[:, lay.n_src:]
+    for pt, w in c.systems():
+        f = c.fields(pt, w)
+        A = orc.Operator.grid(g, f, c.dtype).matrix()
+        fom = C.T @ np.linalg.solve(A, B)
+        psi = rom.transfer(rd.SchurOperator(g, f, c.dtype), lay)
+        assert _rel(psi, fom) <= 1e-5, (pt, w, _rel(psi, fom))
+    del rom
