@@ -178,14 +178,23 @@ __global__ void __launch_bounds__(TMA_THREADS, 1)
                 }
                 consumer_sync();
                 if (MODE == 1) {
-                    for (int rb = 0; rb < RBN; ++rb) {
+                    // the owner warp of each 32-row block reduces the 8 partial sums once
+                    // into the shared q tile; a second barrier publishes it to every warp
+                    // (reading all partials in every warp costs 8x the smem traffic)
+                    T* qs = reinterpret_cast<T*>(smem + L.off_xs);
+                    for (int rb = wid; rb < RBN; rb += 8) {
                         T sum = pb[(rb * 8) * 32 + lane];
 #pragma unroll
                         for (int w2 = 1; w2 < 8; ++w2) sum = Sc<T>::add(sum, pb[(rb * 8 + w2) * 32 + lane]);
                         const long row = row0 + rb * 32 + lane;
                         T q = Sc<T>::sub(Xs[rb * 32 + lane], sum);
                         if (row >= n) q = Sc<T>::zero();
-                        if (wid == (rb & 7) && row < n) xo[row] = q;
+                        else xo[row] = q;
+                        qs[rb * 32 + lane] = q;
+                    }
+                    consumer_sync();
+                    for (int rb = 0; rb < RBN; ++rb) {
+                        const T q = qs[rb * 32 + lane];
                         const T* kb = Ks + (size_t)rb * 32 * C + lane;
 #pragma unroll
                         for (int jj = 0; jj < CPW; ++jj)

@@ -26,6 +26,7 @@ def main():
     ap.add_argument("--config", default="C4")
     ap.add_argument("--systems", type=int, default=0, help="0 = all")
     ap.add_argument("--repeat", action="store_true", help="rebuild once and compare BuildLogs")
+    ap.add_argument("--rom", action="store_true", help="GPU ROM on the compressed basis at the last system")
     args = ap.parse_args()
     import torch
     build.build()
@@ -98,12 +99,42 @@ def main():
         R._check(L.rd_basis_compress(bh, 1e-10, 1, C.byref(rank), R._p(pv), R._p(rdg)))
         ctx.sync()
         t_rrqr = time.perf_counter() - t0
+        # GPU ROM on the compressed basis, at the last system's
+        # parameters: its transfer must reproduce C~^T X of that system's own solves
+        rom_out = {}
+        if args.rom:
+            vptr = L.rd_basis_device_ptr(bh, 0)
+            t0 = time.perf_counter()
+            rom = R.ReducedModel(vptr, dtype=dt, ctx=ctx, where=R.DEVICE, n=n, r=rank.value)
+            ctx.sync()
+            t_create = time.perf_counter() - t0
+            t0 = time.perf_counter()
+            psi = rom.transfer(op, lay)
+            t_transfer = time.perf_counter() - t0
+            ns = lay.n_src
+            didx = torch.from_numpy(np.asarray(lay.idx[ns:], dtype=np.int64)).cuda()
+            dval = torch.from_numpy(np.asarray(lay.val[ns:])).cuda()
+            fom = (X[:ns][:, didx] * dval.to(X.dtype)).T.cpu().numpy()  # (C~^T X)[d, s]
+            rel = float(np.linalg.norm(psi - fom) / np.linalg.norm(fom))
+            rng = np.random.default_rng(5)
+            sup = []
+            for _ in range(8):
+                ix = np.sort(rng.choice(n, size=20000, replace=False))
+                sup.append((ix, rng.uniform(0.1, 1.0, ix.size)))
+            t0 = time.perf_counter()
+            Jm = rom.jacobian(op, lay, sup, -g.h ** 2)
+            t_jac = time.perf_counter() - t0
+            del rom
+            rom_out = {"order": rank.value, "create_s": round(t_create, 3), "transfer_s": round(t_transfer, 3),
+                       "jacobian_8par_s": round(t_jac, 3), "transfer_vs_build_solutions_rel": rel,
+                       "jacobian_finite": bool(np.isfinite(Jm).all())}
+            print(json.dumps({"rom": rom_out}), file=sys.stderr, flush=True)
         L.rd_basis_destroy(bh)
         total = time.perf_counter() - t_start
         return {"seed_s": round(t_seed, 3), "X0_iterations": tot.value, "systems_s": round(t_sys_total, 3),
                 "rrqr_s": round(t_rrqr, 3), "basis_build_s": round(total, 3),
                 "basis_build_without_seed_s": round(total - t_seed, 3), "candidate_cols": cols, "rank": rank.value,
-                "max_rel_residual_all_solves": worst, "tol": cfg.tol, "per_system": per}, logs
+                "max_rel_residual_all_solves": worst, "tol": cfg.tol, "rom": rom_out, "per_system": per}, logs
 
     out, logs = run_build()
     out["config"] = args.config
