@@ -171,6 +171,21 @@ int rd_rom_jacobian(rd_rom* rom, rd_op* op, long n_src, const long* src_idx, con
                     const long* det_idx, const double* det_val, long n_par, const long* sup_ptr, const long* sup_idx,
                     const double* sup_val, double scale, void* J, int where);
 
+/* ----------------------------------------------------- full-order model --- */
+/* fom_transfer (src/rom.cpp:86-91, FomSolve::Minres): Psi = C~^T A^-1 B~,
+ * n_det x n_src, by batched independent CG (omega = 0) / COCG solves at
+ * relative tolerance tol (the reference's default is 1e-10).               */
+int rd_fom_transfer(rd_op* op, int dtype, long n_src, const long* src_idx, const double* src_val, long n_det,
+                    const long* det_idx, const double* det_val, double tol, void* Psi, int where,
+                    long* total_iterations);
+/* fom_jacobian / jacobian_from_solutions (src/rom.cpp:101-129): X = A^-1 B~,
+ * Z = A^-1 C~ (one batched solve), column k = scale * vec(sum_t w_t
+ * Z[i_t,:]^T X[i_t,:]) over the k-th CSR support; the reference's scale is
+ * -h^2. J is (n_det*n_src) x n_par.                                        */
+int rd_fom_jacobian(rd_op* op, int dtype, long n_src, const long* src_idx, const double* src_val, long n_det,
+                    const long* det_idx, const double* det_val, long n_par, const long* sup_ptr, const long* sup_idx,
+                    const double* sup_val, double scale, double tol, void* J, int where);
+
 /* ------------------------------------------------------- bench hooks --- */
 /* Mean device ms per launch of the three inner-iteration projection kernels
  * (ms_out[0] c = K^T x, [1] fused x' = x - K c1 ; c2 = K^T x', [2] update)

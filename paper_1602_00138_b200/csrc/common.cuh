@@ -125,12 +125,26 @@ __device__ inline bool grid_commit(const GridRed& g, const double* vals, int nv)
     return s_ticket == nb - 1;
 }
 
+// Explicit-slot variant for several independent reductions in one launch
+// (the batched CG: one counter and one partial block per column): this block
+// commits slot b of nb; true in the last of the nb blocks.
+__device__ inline bool grid_commit_at(const GridRed& g, const double* vals, int nv, unsigned b, unsigned nb) {
+    for (int v = threadIdx.x; v < nv; v += blockDim.x) g.partials[(size_t)b * nv + v] = vals[v];
+    __threadfence();
+    __syncthreads();
+    __shared__ unsigned s_ticket2;
+    if (threadIdx.x == 0) s_ticket2 = atomicAdd(g.counter, 1u);
+    __syncthreads();
+    return s_ticket2 == nb - 1;
+}
+
 // In the last block: out[v] = sum_b partials[b][v] in block order (fixed
 // association: TPC threads per value each sum a strided block subset, then a
 // fixed-order combine). Resets the counter.
-__device__ inline void grid_finish(const GridRed& g, int nv, double* out /* shared or global */) {
+__device__ inline void grid_finish(const GridRed& g, int nv, double* out /* shared or global */,
+                                   unsigned nb = 0u) {
     __threadfence();
-    const unsigned nb = gridDim.x * gridDim.y * gridDim.z;
+    if (nb == 0u) nb = gridDim.x * gridDim.y * gridDim.z;
     int tpc = 1;
     while (tpc * 2 * nv <= (int)blockDim.x && tpc < 32) tpc *= 2;
     const int groups = blockDim.x / tpc;

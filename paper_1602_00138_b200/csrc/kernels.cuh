@@ -217,6 +217,69 @@ template <> __device__ __forceinline__ double2 st2<cplx>(cplx v) { return v; }
 
 __device__ inline bool finite_(double v) { return isfinite(v); }
 
+// Chronopoulos-Gear scalar step of one CG / COCG solve from the merged
+// reduction s_tot = {r^T r (W), r^T A r (W), r^H r}: convergence, the 1000-step
+// stagnation window, then alpha / beta. Runs in one thread.
+template <class T>
+__device__ __forceinline__ void cg_recurrence(CGState* st, const double* s_tot, double* hist) {
+    constexpr int W = Sc<T>::W;
+    T gamma, delta;
+    if constexpr (W == 1) {
+        gamma = s_tot[0];
+        delta = s_tot[1];
+    } else {
+        gamma = make_double2(s_tot[0], s_tot[1]);
+        delta = make_double2(s_tot[2], s_tot[3]);
+    }
+    const double rho2 = s_tot[2 * W];
+    const int it = st->it;
+    const double relres = st->scale > 0.0 ? sqrt(rho2) / st->scale : 0.0;
+    st->relres = relres;
+    if (hist && it < st->hist_cap) hist[it] = relres;
+    if (it == 0) {
+        st->best = relres;
+        if (rho2 == 0.0 || st->scale == 0.0 || relres <= st->tol) {
+            st->converged = 1;
+            st->done = 1;
+            return;
+        }
+    } else {
+        if (!finite_(relres)) {
+            st->done = 1;
+            return;
+        }
+        if (relres <= st->tol) {
+            st->converged = 1;
+            st->done = 1;
+            return;
+        }
+        // CG residuals are not monotone: 1000-step window (the reference's 50 is for MINRES)
+        if (relres < st->best * (1.0 - 1e-12)) {
+            st->best = relres;
+            st->stagnant = 0;
+        } else if (++st->stagnant >= 1000) {
+            st->done = 1;
+            return;
+        }
+    }
+    if (it >= st->maxit) {
+        st->done = 1;
+        return;
+    }
+    T alpha, beta;
+    if (it == 0) {
+        beta = Sc<T>::zero();
+        alpha = Sc<T>::div(gamma, delta);
+    } else {
+        const T gp = ld2<T>(st->gamma_prev), ap = ld2<T>(st->alpha_prev);
+        beta = Sc<T>::div(gamma, gp);
+        alpha = Sc<T>::div(gamma, Sc<T>::sub(delta, Sc<T>::div(Sc<T>::mul(beta, gamma), ap)));
+    }
+    st->alpha = st2<T>(alpha);
+    st->beta = st2<T>(beta);
+    st->gamma = st2<T>(gamma);
+}
+
 // K2: w = A r ; partials of {r^T r (W), r^T w (W), r^H r (1)} ; last block runs
 // the scalar recurrence. One grid reduction per iteration.
 template <class T>
@@ -261,61 +324,100 @@ __global__ void __launch_bounds__(256) cg_stencil_dots(OpDev op, const T* __rest
     __shared__ double s_tot[2 * W + 1];
     grid_finish(red, 2 * W + 1, s_tot);
     if (threadIdx.x != 0) return;
-    T gamma, delta;
+    cg_recurrence<T>(st, s_tot, hist);
+}
+
+// Batched independent CG / COCG (X0 seed solves, full-order transfer): column
+// c of R/Wv (ld) is its own solve with state st[c]. blockIdx.z = c * nkc + k
+// chunk; each column's blocks commit to their own partial slots and counter,
+// and the column's last block runs its scalar step. Converged columns return.
+// The assembled coefficients are re-read per column from L2 (64 MB at 128^3).
+template <class T>
+__global__ void __launch_bounds__(256) bcg_stencil_dots(OpDev op, const T* __restrict__ R, T* __restrict__ Wv, long ld,
+                                                        CGState* st, double* partials, unsigned* counters, int kz) {
+    constexpr int W = Sc<T>::W;
+    constexpr int NV = 2 * W + 1;
+    const int nkc = (op.N2 + kz - 1) / kz;
+    const int c = blockIdx.z / nkc;
+    const int kc = blockIdx.z - c * nkc;
+    CGState* sc = st + c;
+    if (sc->done) return;
+    const T* r = R + (size_t)c * ld;
+    T* w = Wv + (size_t)c * ld;
+    T g = Sc<T>::zero(), dl = Sc<T>::zero();
+    double h = 0.0;
+    const int i = blockIdx.x * 32 + (threadIdx.x & 31);
+    const int j = blockIdx.y * 8 + (threadIdx.x >> 5);
+    const int k0 = kc * kz, k1 = min(op.N2, k0 + kz);
+    if (i < op.N0 && j < op.N1)
+        zmarch<T>(op, r, i, j, k0, k1, [&](long p, const T& rp, const T& wp) {
+            w[p] = wp;
+            g = Sc<T>::fma(rp, rp, g);
+            dl = Sc<T>::fma(rp, wp, dl);
+            h += Sc<T>::abs2(rp);
+        });
+    __shared__ double s_red[32];
+    __shared__ double s_vals[NV];
+    double v[NV];
     if constexpr (W == 1) {
-        gamma = s_tot[0];
-        delta = s_tot[1];
+        v[0] = g;
+        v[1] = dl;
+        v[2] = h;
     } else {
-        gamma = make_double2(s_tot[0], s_tot[1]);
-        delta = make_double2(s_tot[2], s_tot[3]);
+        v[0] = ((cplx&)g).x;
+        v[1] = ((cplx&)g).y;
+        v[2] = ((cplx&)dl).x;
+        v[3] = ((cplx&)dl).y;
+        v[4] = h;
     }
-    const double rho2 = s_tot[2 * W];
-    const int it = st->it;
-    const double relres = st->scale > 0.0 ? sqrt(rho2) / st->scale : 0.0;
-    st->relres = relres;
-    if (it < st->hist_cap) hist[it] = relres;
-    if (it == 0) {
-        st->best = relres;
-        if (rho2 == 0.0 || st->scale == 0.0 || relres <= st->tol) {
-            st->converged = 1;
-            st->done = 1;
-            return;
-        }
-    } else {
-        if (!finite_(relres)) {
-            st->done = 1;
-            return;
-        }
-        if (relres <= st->tol) {
-            st->converged = 1;
-            st->done = 1;
-            return;
-        }
-        // CG residuals are not monotone: 1000-step window (the reference's 50 is for MINRES)
-        if (relres < st->best * (1.0 - 1e-12)) {
-            st->best = relres;
-            st->stagnant = 0;
-        } else if (++st->stagnant >= 1000) {
-            st->done = 1;
-            return;
-        }
+#pragma unroll
+    for (int t = 0; t < NV; ++t) {
+        const double sv = block_sum(v[t], s_red);
+        if (threadIdx.x == 0) s_vals[t] = sv;
     }
-    if (it >= st->maxit) {
-        st->done = 1;
-        return;
+    __syncthreads();
+    const unsigned nbc = gridDim.x * gridDim.y * nkc;
+    const unsigned b = blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * kc);
+    GridRed red{partials + (size_t)c * nbc * NV, counters + c};
+    if (!grid_commit_at(red, s_vals, NV, b, nbc)) return;
+    __shared__ double s_tot[NV];
+    grid_finish(red, NV, s_tot, nbc);
+    if (threadIdx.x != 0) return;
+    cg_recurrence<T>(sc, s_tot, nullptr);
+}
+
+// Batched CG update, blockIdx.y = column: p = r + beta p ; s = w + beta s ;
+// y += alpha p ; r -= alpha s (thread per row).
+template <class T>
+__global__ void __launch_bounds__(256) bcg_update(T* __restrict__ R, T* __restrict__ Pv, T* __restrict__ S,
+                                                  T* __restrict__ Y, const T* __restrict__ Wv, long ld, long n,
+                                                  CGState* st) {
+    const int c = blockIdx.y;
+    CGState* sc = st + c;
+    if (sc->done) return;
+    const T alpha = ld2<T>(sc->alpha), beta = ld2<T>(sc->beta);
+    const size_t off = (size_t)c * ld;
+    for (long row = blockIdx.x * (long)blockDim.x + threadIdx.x; row < n; row += (long)gridDim.x * blockDim.x) {
+        const T rv = R[off + row];
+        const T pn = Sc<T>::fma(beta, Pv[off + row], rv);
+        const T sn = Sc<T>::fma(beta, S[off + row], Wv[off + row]);
+        Pv[off + row] = pn;
+        S[off + row] = sn;
+        Y[off + row] = Sc<T>::fma(alpha, pn, Y[off + row]);
+        R[off + row] = Sc<T>::sub(rv, Sc<T>::mul(alpha, sn));
     }
-    T alpha, beta;
-    if (it == 0) {
-        beta = Sc<T>::zero();
-        alpha = Sc<T>::div(gamma, delta);
-    } else {
-        const T gp = ld2<T>(st->gamma_prev), ap = ld2<T>(st->alpha_prev);
-        beta = Sc<T>::div(gamma, gp);
-        alpha = Sc<T>::div(gamma, Sc<T>::sub(delta, Sc<T>::div(Sc<T>::mul(beta, gamma), ap)));
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        sc->gamma_prev = sc->gamma;
+        sc->alpha_prev = sc->alpha;
+        sc->it = sc->it + 1;
     }
-    st->alpha = st2<T>(alpha);
-    st->beta = st2<T>(beta);
-    st->gamma = st2<T>(gamma);
+}
+
+// R[idx[c] + c*ld] = val[c] (unit right-hand sides of the layout)
+template <class T>
+__global__ void scatter_unit_rhs(T* R, long ld, const long* __restrict__ idx, const double* __restrict__ val, int m) {
+    const int c = blockIdx.x * blockDim.x + threadIdx.x;
+    if (c < m) R[(size_t)c * ld + idx[c]] = Sc<T>::from(val[c]);
 }
 
 // ------------------------------------------------- tall-skinny passes ---

@@ -916,6 +916,114 @@ SolveOut recycled_cg(Ctx& c, DevOp& op, const T* U, const T* K, long ncol, const
     return out;
 }
 
+// Batched independent CG / COCG on unit right-hand sides b_c = val[c] e_idx[c]
+// (the X0 seed solves, basis.cpp:141-149, and the
+// full-order transfer, rom.cpp:71-96). X (n x m, ld n) receives the solutions;
+// each column runs the single-solve recurrence (cg_recurrence) with its own
+// state, scale |val[c]| and the same stopping rules. Two polls in flight.
+template <class T>
+std::vector<CGState> batched_cg(Ctx& c, DevOp& op, long m, const long* bidx, const double* bval, double tol,
+                                long maxit, T* X) {
+    constexpr int W = Sc<T>::W;
+    constexpr int NV = 2 * W + 1;
+    const long n = op.n();
+    std::vector<CGState> fin(m);
+    if (m <= 0) return fin;
+    for (long j = 0; j < m; ++j)
+        if (bidx[j] < 0 || bidx[j] >= n) throw ConfigError("batched CG: right-hand side index out of range");
+    const size_t bytes = sizeof(T) * n * m;
+    DevBuf Rb, Wb, Pb, Sb, stb, cnt, part, ix, vx;
+    for (DevBuf* b : {&Rb, &Wb, &Pb, &Sb}) {
+        b->ensure(bytes);
+        CK(cudaMemsetAsync(b->p, 0, bytes, c.s));
+    }
+    CK(cudaMemsetAsync(X, 0, bytes, c.s));
+    ix.ensure(sizeof(long) * m);
+    vx.ensure(sizeof(double) * m);
+    CK(cudaMemcpyAsync(ix.p, bidx, sizeof(long) * m, cudaMemcpyHostToDevice, c.s));
+    CK(cudaMemcpyAsync(vx.p, bval, sizeof(double) * m, cudaMemcpyHostToDevice, c.s));
+    scatter_unit_rhs<T><<<(int)((m + 127) / 128), 128, 0, c.s>>>(Rb.template as<T>(), n, ix.template as<long>(),
+                                                                 vx.template as<double>(), (int)m);
+    c.check_launch();
+    CGState* hs = nullptr;
+    CK(cudaMallocHost(&hs, sizeof(CGState) * m * 2));
+    struct HostFree {
+        CGState* p;
+        ~HostFree() { cudaFreeHost(p); }
+    } hf{hs};
+    for (long j = 0; j < m; ++j) {
+        CGState s0{};
+        s0.scale = std::fabs(bval[j]);
+        s0.tol = tol;
+        s0.maxit = (int)std::min<long>(maxit, 0x7fffffff);
+        hs[j] = s0;
+    }
+    stb.ensure(sizeof(CGState) * m);
+    CK(cudaMemcpyAsync(stb.p, hs, sizeof(CGState) * m, cudaMemcpyHostToDevice, c.s));
+    CK(cudaStreamSynchronize(c.s));
+    CGState* st = stb.template as<CGState>();
+    // stencil grid: one column per block slice; enough blocks per column to fill the GPU
+    dim3 g0 = stencil_grid(op.d, 1);
+    int kz = 1;
+    while ((long)g0.x * g0.y * ((op.d.N2 + kz - 1) / kz) * m > 16L * c.sms && kz < op.d.N2) kz *= 2;
+    const long nkc = (op.d.N2 + kz - 1) / kz;
+    if (nkc * m > 65535) throw ConfigError("batched CG: too many columns for one launch");
+    const dim3 gst(g0.x, g0.y, (unsigned)(nkc * m));
+    const long nbc = (long)g0.x * g0.y * nkc;
+    part.ensure(sizeof(double) * m * nbc * NV);
+    cnt.ensure(sizeof(unsigned) * m);
+    CK(cudaMemsetAsync(cnt.p, 0, sizeof(unsigned) * m, c.s));
+    const long gxu = std::max(1L, std::min<long>((n + 255) / 256, std::max(8L, 32L * c.sms / m)));
+    const dim3 gup((unsigned)gxu, (unsigned)m);
+    const int batch = 8;
+    auto launch_batch = [&]() {
+        for (int b = 0; b < batch; ++b) {
+            bcg_stencil_dots<T><<<gst, 256, 0, c.s>>>(op.d, Rb.template as<T>(), Wb.template as<T>(), n, st,
+                                                      part.template as<double>(), cnt.template as<unsigned>(), kz);
+            c.check_launch();
+            bcg_update<T><<<gup, 256, 0, c.s>>>(Rb.template as<T>(), Pb.template as<T>(), Sb.template as<T>(), X,
+                                                Wb.template as<T>(), n, n, st);
+            c.check_launch();
+        }
+    };
+    auto all_done = [&](const CGState* h) {
+        for (long j = 0; j < m; ++j)
+            if (!h[j].done) return false;
+        return true;
+    };
+    int slot = 0;
+    launch_batch();
+    CK(cudaMemcpyAsync(hs, st, sizeof(CGState) * m, cudaMemcpyDeviceToHost, c.s));
+    CK(cudaEventRecord(c.ev[0], c.s));
+    launch_batch();
+    CK(cudaMemcpyAsync(hs + m, st, sizeof(CGState) * m, cudaMemcpyDeviceToHost, c.s));
+    CK(cudaEventRecord(c.ev[1], c.s));
+    long guard = 0;
+    while (true) {
+        CK(cudaEventSynchronize(c.ev[slot]));
+        if (all_done(hs + slot * m)) break;
+        if (++guard > maxit / batch + 8) break;
+        launch_batch();
+        CK(cudaMemcpyAsync(hs + slot * m, st, sizeof(CGState) * m, cudaMemcpyDeviceToHost, c.s));
+        CK(cudaEventRecord(c.ev[slot], c.s));
+        slot ^= 1;
+    }
+    CK(cudaMemcpyAsync(hs, st, sizeof(CGState) * m, cudaMemcpyDeviceToHost, c.s));
+    c.sync();
+    for (long j = 0; j < m; ++j) fin[j] = hs[j];
+    return fin;
+}
+
+// (C~^T X)[d, s] = val[d] X[idx[d], s] (C~ has one nonzero per column)
+template <class T>
+__global__ void fom_gather(const T* __restrict__ X, long n, int ns, const long* __restrict__ didx,
+                           const double* __restrict__ dval, int nd, T* __restrict__ Psi) {
+    const int e = blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= ns * nd) return;
+    const int d = e % nd, s = e / nd;
+    Psi[e] = Sc<T>::scale(X[(size_t)s * n + didx[d]], dval[d]);
+}
+
 // RecycleSpace::from_raw on the device: sequential CGS2 (bilinear for complex)
 // of AW's columns; U = W R^-1 formed column by column. W columns are read
 // through `wcol` (indices into Wbase) when given.
@@ -2252,27 +2360,29 @@ int rd_initial_solutions(rd_op* o, int dtype, long nrhs, const long* bidx, const
         Ctx& cx = o->ctx->c;
         const long n = o->op.d.n;
         const size_t es = esize(dtype);
+        if (!o->op.have_fields) throw rd::ConfigError("operator: fields not set");
+        if (dtype == 0 && o->op.d.shift != 0.0) throw rd::ConfigError("real solve with a complex operator");
         Out Xs(cx, X0, es * n * nrhs, where);
-        DevBuf b, y, im, g;
-        b.ensure(es * n);
-        y.ensure(es * n);
-        im.ensure(es * n);
-        if (!Xs.p) g.ensure(es * n);
+        DevBuf g;
+        if (!Xs.p) g.ensure(es * n * std::max(1L, nrhs));
+        void* xp = Xs.p ? Xs.p : g.p;
+        // batched independent solves (basis.cpp:141-149), chunked to bound the
+        // 5 n-vectors per column of workspace
+        const long chunk = std::max(1L, std::min(nrhs, (long)(24e9 / (5.0 * es * (double)n))));
         long tot = 0;
         auto run = [&](auto tag) {
             using T = decltype(tag);
-            Workspace<T> ws;
-            for (long j = 0; j < nrhs; ++j) {
-                CK(cudaMemsetAsync(b.p, 0, es * n, cx.s));
-                T v = Sc<T>::from(bval[j]);
-                CK(cudaMemcpyAsync(b.template as<T>() + bidx[j], &v, sizeof(T), cudaMemcpyHostToDevice, cx.s));
-                T* gj = Xs.p ? (T*)Xs.p + (size_t)j * n : g.template as<T>();
-                SolveOut so = recycled_cg<T>(cx, o->op, nullptr, nullptr, 0, b.template as<T>(), kInnerSafety * tol, 2 * n,
-                                             0.0, gj, y.template as<T>(), im.template as<T>(), ws, false);
-                if (!so.converged)
-                    throw rd::SolverError("init_basis: CG failed on initial solution column " + std::to_string(j));
-                tot += so.iterations;
-                VLOG(2, "X0 column %ld: %d its", j, so.iterations);
+            for (long j0 = 0; j0 < nrhs; j0 += chunk) {
+                const long m = std::min(chunk, nrhs - j0);
+                const auto st = batched_cg<T>(cx, o->op, m, bidx + j0, bval + j0, kInnerSafety * tol, 2 * n,
+                                              static_cast<T*>(xp) + (size_t)j0 * n);
+                for (long j = 0; j < m; ++j) {
+                    if (!st[j].converged)
+                        throw rd::SolverError("init_basis: CG failed on initial solution column " +
+                                              std::to_string(j0 + j));
+                    tot += st[j].it;
+                    VLOG(2, "X0 column %ld: %d its", j0 + j, st[j].it);
+                }
             }
         };
         if (dtype == 0)
@@ -2282,6 +2392,111 @@ int rd_initial_solutions(rd_op* o, int dtype, long nrhs, const long* bidx, const
         Xs.finish();
         cx.sync();
         if (total_iterations) *total_iterations = tot;
+    });
+}
+
+// fom_transfer (rom.cpp:86-91) with the batched CG / COCG in place of MINRES
+int rd_fom_transfer(rd_op* o, int dtype, long n_src, const long* src_idx, const double* src_val, long n_det,
+                    const long* det_idx, const double* det_val, double tol, void* Psi, int where,
+                    long* total_iterations) {
+    return guard([&] {
+        Ctx& cx = o->ctx->c;
+        const long n = o->op.d.n;
+        const size_t es = esize(dtype);
+        if (!o->op.have_fields) throw rd::ConfigError("operator: fields not set");
+        if (dtype == 0 && o->op.d.shift != 0.0) throw rd::ConfigError("real solve with a complex operator");
+        if (n_src <= 0 || n_det <= 0) throw rd::ConfigError("fom: need sources and detectors");
+        for (long d = 0; d < n_det; ++d)
+            if (det_idx[d] < 0 || det_idx[d] >= n) throw rd::ConfigError("fom: detector index out of range");
+        Out ps(cx, Psi, es * n_src * n_det, where);
+        DevBuf Xb, ix, vx;
+        Xb.ensure(es * n * n_src);
+        ix.ensure(sizeof(long) * n_det);
+        vx.ensure(sizeof(double) * n_det);
+        long tot = 0;
+        auto run = [&](auto tag) {
+            using T = decltype(tag);
+            const auto st = batched_cg<T>(cx, o->op, n_src, src_idx, src_val, tol, 2 * n, Xb.template as<T>());
+            for (long j = 0; j < n_src; ++j) {
+                if (!st[j].converged) throw rd::SolverError("fom: CG did not converge");
+                tot += st[j].it;
+            }
+            CK(cudaMemcpyAsync(ix.p, det_idx, sizeof(long) * n_det, cudaMemcpyHostToDevice, cx.s));
+            CK(cudaMemcpyAsync(vx.p, det_val, sizeof(double) * n_det, cudaMemcpyHostToDevice, cx.s));
+            fom_gather<T><<<(int)((n_src * n_det + 255) / 256), 256, 0, cx.s>>>(
+                Xb.template as<T>(), n, (int)n_src, ix.template as<long>(), vx.template as<double>(), (int)n_det,
+                static_cast<T*>(ps.p));
+            cx.check_launch();
+        };
+        if (dtype == 0)
+            run(double{});
+        else
+            run(cplx{});
+        ps.finish();
+        cx.sync();
+        if (total_iterations) *total_iterations = tot;
+    });
+}
+
+// fom_jacobian / jacobian_from_solutions (rom.cpp:101-129): X = A^-1 B~,
+// Z = A^-1 C~ by one batched solve, then the support-row contraction of the
+// reduced model's kernel with Wy = X, Wz = Z.
+int rd_fom_jacobian(rd_op* o, int dtype, long n_src, const long* src_idx, const double* src_val, long n_det,
+                    const long* det_idx, const double* det_val, long n_par, const long* sup_ptr, const long* sup_idx,
+                    const double* sup_val, double scale, double tol, void* J, int where) {
+    return guard([&] {
+        Ctx& cx = o->ctx->c;
+        const long n = o->op.d.n;
+        const size_t es = esize(dtype);
+        if (!o->op.have_fields) throw rd::ConfigError("operator: fields not set");
+        if (dtype == 0 && o->op.d.shift != 0.0) throw rd::ConfigError("real solve with a complex operator");
+        if (n_src <= 0 || n_det <= 0) throw rd::ConfigError("fom: need sources and detectors");
+        if (n_par < 0 || (n_par > 0 && !sup_ptr)) throw rd::ConfigError("fom: bad parameter supports");
+        const long nnz = n_par > 0 ? sup_ptr[n_par] : 0;
+        for (long k = 0; k < n_par; ++k)
+            if (sup_ptr[k + 1] < sup_ptr[k]) throw rd::ConfigError("fom: support pointers not monotone");
+        for (long t = 0; t < nnz; ++t)
+            if (sup_idx[t] < 0 || sup_idx[t] >= n) throw rd::ConfigError("fom: support index out of range");
+        Out js(cx, J, es * n_src * n_det * std::max(1L, n_par), where);
+        const long m = n_src + n_det;
+        std::vector<long> bi(m);
+        std::vector<double> bv(m);
+        for (long j = 0; j < n_src; ++j) bi[j] = src_idx[j], bv[j] = src_val[j];
+        for (long j = 0; j < n_det; ++j) bi[n_src + j] = det_idx[j], bv[n_src + j] = det_val[j];
+        DevBuf Xb, Pd;
+        Xb.ensure(es * n * m);
+        Pd.ensure(sizeof(long) * (n_par + 1) + sizeof(long) * std::max(1L, nnz) + sizeof(double) * std::max(1L, nnz));
+        long* dptr = Pd.template as<long>();
+        long* didx = dptr + (n_par + 1);
+        double* dval = reinterpret_cast<double*>(didx + std::max(1L, nnz));
+        auto run = [&](auto tag) {
+            using T = decltype(tag);
+            const auto st = batched_cg<T>(cx, o->op, m, bi.data(), bv.data(), tol, 2 * n, Xb.template as<T>());
+            for (long j = 0; j < m; ++j)
+                if (!st[j].converged) throw rd::SolverError("fom: CG did not converge");
+            if (n_par <= 0) return;
+            CK(cudaMemcpyAsync(dptr, sup_ptr, sizeof(long) * (n_par + 1), cudaMemcpyHostToDevice, cx.s));
+            if (nnz > 0) {
+                CK(cudaMemcpyAsync(didx, sup_idx, sizeof(long) * nnz, cudaMemcpyHostToDevice, cx.s));
+                CK(cudaMemcpyAsync(dval, sup_val, sizeof(double) * nnz, cudaMemcpyHostToDevice, cx.s));
+            }
+            const T* X = Xb.template as<T>();
+            for (long k0 = 0; k0 < n_par; k0 += 65535) {
+                const long kk = std::min(65535L, n_par - k0);
+                dim3 grid((unsigned)std::max(1L, std::min<long>((n_src * n_det + 255) / 256, 64)), (unsigned)kk);
+                rom_jacobian<T><<<grid, 256, 0, cx.s>>>(X, X + (size_t)n_src * n, n, (int)n_src, (int)n_det, dptr + k0,
+                                                        didx, dval, scale,
+                                                        static_cast<T*>(js.p) + (size_t)k0 * n_src * n_det,
+                                                        n_src * n_det);
+                cx.check_launch();
+            }
+        };
+        if (dtype == 0)
+            run(double{});
+        else
+            run(cplx{});
+        js.finish();
+        cx.sync();
     });
 }
 

@@ -35,6 +35,7 @@ EXPORTS = [
     "rd_basis_append", "rd_basis_solve_projected", "rd_process_system", "rd_rrqr", "rd_bench_projection",
     "rd_bench_stencil", "rd_residual_norms", "rd_basis_compress", "rd_rom_create", "rd_rom_destroy",
     "rd_rom_order", "rd_rom_E", "rd_rom_reduced_system", "rd_rom_transfer", "rd_rom_jacobian",
+    "rd_fom_transfer", "rd_fom_jacobian",
 ]
 
 
@@ -124,6 +125,9 @@ def load_library(path: Optional[str] = None):
     L.rd_bench_stencil.argtypes = [vp, C.c_int, C.c_long, C.c_int, vp]
     L.rd_basis_compress.argtypes = [vp, C.c_double, C.c_int, lp, vp, vp]
     L.rd_residual_norms.argtypes = [vp, C.c_int, C.c_long, vp, vp, vp, C.c_int, vp]
+    L.rd_fom_transfer.argtypes = [vp, C.c_int, C.c_long, vp, vp, C.c_long, vp, vp, C.c_double, vp, C.c_int, lp]
+    L.rd_fom_jacobian.argtypes = [vp, C.c_int, C.c_long, vp, vp, C.c_long, vp, vp, C.c_long, vp, vp, vp, C.c_double,
+                                  C.c_double, vp, C.c_int]
     L.rd_rom_create.argtypes = [vp, C.c_int, C.c_long, C.c_long, vp, C.c_int, C.POINTER(vp)]
     L.rd_rom_destroy.argtypes = [vp]
     L.rd_rom_order.argtypes = [vp]
@@ -518,6 +522,52 @@ def rrqr(A: np.ndarray, tol: float = 1e-10, normalize: bool = True, ctx: Optiona
     return rank.value, perm, rdiag, Q[:, : rank.value].copy()
 
 
+def _csr(supports):
+    ptr = np.zeros(len(supports) + 1, dtype=np.int64)
+    for k, (ix, _) in enumerate(supports):
+        ptr[k + 1] = ptr[k] + len(ix)
+    if supports:
+        sidx = np.ascontiguousarray(np.concatenate([np.asarray(ix, dtype=np.int64) for ix, _ in supports]))
+        sval = np.ascontiguousarray(np.concatenate([np.asarray(w, dtype=np.float64) for _, w in supports]))
+    else:
+        sidx, sval = np.zeros(1, dtype=np.int64), np.zeros(1)
+    if sidx.size == 0:
+        sidx, sval = np.zeros(1, dtype=np.int64), np.zeros(1)
+    return ptr, sidx, sval
+
+
+def _layout_split(layout: P.Layout):
+    idx = np.ascontiguousarray(layout.idx, dtype=np.int64)
+    val = np.ascontiguousarray(layout.val, dtype=np.float64)
+    s = layout.n_src
+    return (np.ascontiguousarray(idx[:s]), np.ascontiguousarray(val[:s]),
+            np.ascontiguousarray(idx[s:]), np.ascontiguousarray(val[s:]))
+
+
+def fom_transfer(op: SchurOperator, layout: P.Layout, tol: float = 1e-10):
+    """Full-order transfer C~^T A^-1 B~ (rom.cpp:86-91) by batched CG / COCG.
+    Returns (Psi n_det x n_src, total iterations)."""
+    si, sv, di, dv = _layout_split(layout)
+    out = np.zeros((layout.n_det, layout.n_src), dtype=op.dtype, order="F")
+    its = C.c_long()
+    _check(load_library().rd_fom_transfer(op.h, _dt(op.dtype), layout.n_src, _p(si), _p(sv), layout.n_det, _p(di),
+                                          _p(dv), tol, _p(out), HOST, C.byref(its)))
+    return out, its.value
+
+
+def fom_jacobian(op: SchurOperator, layout: P.Layout, supports, scale: float, tol: float = 1e-10):
+    """Full-order Jacobian (rom.cpp:101-129): column k = scale * vec(sum_t w_t
+    Z[i_t,:]^T X[i_t,:]) with X = A^-1 B~, Z = A^-1 C~; supports as in
+    ReducedModel.jacobian."""
+    si, sv, di, dv = _layout_split(layout)
+    ptr, sidx, sval = _csr(supports)
+    out = np.zeros((layout.n_det * layout.n_src, max(1, len(supports))), dtype=op.dtype, order="F")
+    _check(load_library().rd_fom_jacobian(op.h, _dt(op.dtype), layout.n_src, _p(si), _p(sv), layout.n_det, _p(di),
+                                          _p(dv), len(supports), _p(ptr), _p(sidx), _p(sval), float(scale), tol,
+                                          _p(out), HOST))
+    return out[:, : len(supports)]
+
+
 class ReducedModel:
     """ReducedModel (include/romdot/rom.hpp:12-41, src/rom.cpp:9-67) on the device.
 
@@ -561,11 +611,7 @@ class ReducedModel:
 
     @staticmethod
     def _split(layout: P.Layout):
-        idx = np.ascontiguousarray(layout.idx, dtype=np.int64)
-        val = np.ascontiguousarray(layout.val, dtype=np.float64)
-        s = layout.n_src
-        return (np.ascontiguousarray(idx[:s]), np.ascontiguousarray(val[:s]),
-                np.ascontiguousarray(idx[s:]), np.ascontiguousarray(val[s:]))
+        return _layout_split(layout)
 
     def transfer(self, op: SchurOperator, layout: P.Layout) -> np.ndarray:
         """Psi_r = C_r^T A_r^-1 B_r, n_det x n_src."""
@@ -580,13 +626,7 @@ class ReducedModel:
         reference's SparseDiag from absorption_jacobian); column k of the result
         is scale * vec(sum_t w_t (V Z)[i_t,:]^T (V Y)[i_t,:]), (n_det*n_src) x n_par."""
         si, sv, di, dv = self._split(layout)
-        ptr = np.zeros(len(supports) + 1, dtype=np.int64)
-        for k, (ix, _) in enumerate(supports):
-            ptr[k + 1] = ptr[k] + len(ix)
-        sidx = np.ascontiguousarray(np.concatenate([np.asarray(ix, dtype=np.int64) for ix, _ in supports])
-                                    if supports else np.zeros(1, dtype=np.int64))
-        sval = np.ascontiguousarray(np.concatenate([np.asarray(w, dtype=np.float64) for _, w in supports])
-                                    if supports else np.zeros(1))
+        ptr, sidx, sval = _csr(supports)
         out = np.zeros((layout.n_det * layout.n_src, max(1, len(supports))), dtype=self.dtype, order="F")
         _check(load_library().rd_rom_jacobian(self.h, op.h, layout.n_src, _p(si), _p(sv), layout.n_det, _p(di),
                                               _p(dv), len(supports), _p(ptr), _p(sidx), _p(sval), float(scale),

@@ -126,3 +126,67 @@ def test_rom_of_compressed_device_basis_interpolates_fom(rd, name):
         psi = rom.transfer(rd.SchurOperator(g, f, c.dtype), lay)
         assert _rel(psi, fom) <= 1e-5, (pt, w, _rel(psi, fom))
     del rom
+
+
+# ---------------------------------------------------------------------------
+# Full-order model and batched X0 solves
+
+@pytest.mark.parametrize("name", ["T3", "T3c", "T2c"])
+def test_fom_transfer_and_jacobian_match_dense(rd, name):
+    """fom_transfer / fom_jacobian (rom.cpp:86-129) by batched CG/COCG vs
+    dense solves. Psi samples X at far-field detector nodes (~1e-3 of ||x||),
+    so the solves run at 1e-12 for a 1e-8 bound on the outputs."""
+    c = P.CONFIGS[name]
+    g, lay = c.grid, c.layout()
+    pt, w = c.systems()[-1]
+    f = c.fields(pt, w)
+    A = orc.Operator.grid(g, f, c.dtype).matrix()
+    Bc = lay.dense(g.n)
+    B, C = Bc[:, : lay.n_src], Bc[:, lay.n_src:]
+    X = np.linalg.solve(A, B)
+    Z = np.linalg.solve(A, C)
+    op = rd.SchurOperator(g, f, c.dtype)
+    psi, its = rd.fom_transfer(op, lay, 1e-12)
+    assert its > 0
+    assert _rel(psi, C.T @ X) <= 1e-8
+    sup = _supports(g.n, 4, 5)
+    scale = -g.h ** 2
+    J = np.zeros((lay.n_det * lay.n_src, len(sup)), dtype=X.dtype)
+    for k, (ix, wv) in enumerate(sup):
+        M = (Z[ix] * wv[:, None]).T @ X[ix]  # jacobian_from_solutions, rom.cpp:118-124
+        J[:, k] = scale * M.ravel(order="F")
+    Jd = rd.fom_jacobian(op, lay, sup, scale, 1e-12)
+    assert _rel(Jd[:, :-1], J[:, :-1]) <= 1e-8
+    assert np.all(Jd[:, -1] == 0)
+
+
+@pytest.mark.parametrize("name", ["T2", "T3c"])
+def test_batched_initial_solutions_match_oracle(rd, name):
+    """init_basis X0 (basis.cpp:141-149): the batched device solves meet the
+    0.25 tol residual per column and agree with the CPU checker's solutions."""
+    c = P.CONFIGS[name]
+    g, lay = c.grid, c.layout()
+    f0 = c.fields(0)
+    X0, its = rd.initial_solutions(rd.SchurOperator(g, f0, c.dtype), lay, c.tol)
+    Xo, its_o = orc.initial_solutions(orc.Operator.grid(g, f0, c.dtype), lay, c.tol)
+    A = orc.Operator.grid(g, f0, c.dtype).matrix()
+    B = lay.dense(g.n, c.dtype)
+    res = np.linalg.norm(A @ X0 - B, axis=0) / np.linalg.norm(B, axis=0)
+    assert res.max() <= 0.25 * c.tol * 1.01
+    assert abs(its - its_o) <= 2 * lay.n_rhs
+    err = np.linalg.norm(X0 - Xo, axis=0) / np.linalg.norm(Xo, axis=0)
+    assert err.max() <= 1e-6
+
+
+def test_fom_errors(rd):
+    c = P.CONFIGS["T3c"]
+    lay = c.layout()
+    op = rd.SchurOperator(c.grid, c.fields(1, 0.2), np.complex128)
+    opr = rd.SchurOperator(c.grid, c.fields(1, 0.0), np.float64)
+    with pytest.raises(rd.ConfigError):
+        bad = P.Layout(idx=np.array(list(lay.idx[:-1]) + [c.grid.n]), val=lay.val, n_src=lay.n_src, n_det=lay.n_det)
+        rd.fom_transfer(op, bad, 1e-10)
+    # real dtype with a complex shift is a configuration error
+    opr.set_fields(c.fields(1, 0.2))
+    with pytest.raises(rd.ConfigError):
+        rd.fom_transfer(opr, lay, 1e-10)
