@@ -140,6 +140,21 @@ int rd_rrqr(rd_ctx* ctx, int dtype, long n, long m, const void* A, double tol, i
  * (n x rank). perm / rdiag have basis-cols entries. The basis is final.   */
 int rd_basis_compress(rd_basis* b, double tol, int normalize, long* rank, long* perm, double* rdiag);
 
+/* ------------------------------------------- per-RHS-only comparator --- */
+/* BaselinePerRhsRecycler (include/romdot/basis.hpp:102-119, src/basis.cpp:
+ * 209-266): each RHS recycles only its own space U_j = [U0, X0_j, own new
+ * directions]; no global check, no cross-RHS sharing, inner solves at tol.
+ * The handle is an rd_basis holding V and the per-RHS index lists only
+ * (rd_basis_cols/get(0)/space work; refresh/append/process_system refuse it);
+ * free it with rd_basis_destroy.                                            */
+int rd_per_rhs_create(rd_ctx* ctx, int dtype, long n, long ku, long nrhs, const void* U0, const void* X0, int where,
+                      rd_basis** out);
+/* BaselinePerRhsRecycler::solve_system (basis.cpp:221-264): X (n x nrhs) and
+ * the same 5-column log as rd_process_system.                              */
+int rd_per_rhs_solve_system(rd_basis* b, rd_op* op, long nrhs, const long* bidx, const double* bval, double tol,
+                            int system_index, long maxit, void* X, int where, double* log, long* inner_iterations,
+                            long* appends);
+
 /* -------------------------------------------------------- reduced model --- */
 /* ReducedModel (include/romdot/rom.hpp:12-41, src/rom.cpp:9-67) on the device.
  * V (n x r, column-major) is copied for where = 0 and BORROWED for where = 1

@@ -74,6 +74,11 @@ def lib():
         L.orc_process_system.argtypes = [vp, vp, C.c_long, vp, vp, C.c_double, C.c_int, C.c_long, C.c_int,
                                          vp, vp, c_long_p, c_long_p]
         L.orc_initial_solutions.argtypes = [vp, C.c_long, vp, vp, C.c_double, C.c_int, vp, c_long_p]
+        L.orc_per_rhs_create.argtypes = [C.c_int, C.c_long, C.c_long, C.c_long, vp, vp]
+        L.orc_per_rhs_create.restype = vp
+        L.orc_per_rhs_destroy.argtypes = [vp]
+        L.orc_per_rhs_solve_system.argtypes = [vp, vp, C.c_long, vp, vp, C.c_double, C.c_int, C.c_long, C.c_int,
+                                               vp, vp, c_long_p, c_long_p]
         L.orc_thin_qr.argtypes = [C.c_int, C.c_long, C.c_long, vp, vp, vp]
         L.orc_qrcp.argtypes = [C.c_int, C.c_long, C.c_long, vp, C.c_double, C.c_int, c_long_p, vp, vp, vp]
         L.orc_normal_stream.argtypes = [C.c_uint64, C.c_long, vp]
@@ -356,6 +361,35 @@ def process_system(gb: GlobalBasis, op: Operator, layout, tol, system_index, max
                                     _p(log), C.byref(its), C.byref(app)))
     rows = [LogRow(int(r[0]), int(r[1]), float(r[2]), int(r[3]), bool(r[4])) for r in log]
     return ProcessResult(X, rows, its.value, app.value)
+
+
+class PerRhsRecycler:
+    """BaselinePerRhsRecycler (basis.hpp:102-119, basis.cpp:209-266)."""
+
+    def __init__(self, U0, X0):
+        dt = np.result_type(U0.dtype, X0.dtype)
+        U0 = np.asfortranarray(U0, dtype=dt)
+        X0 = np.asfortranarray(X0, dtype=dt)
+        self.dtype, self.n = dt, X0.shape[0]
+        self.h = lib().orc_per_rhs_create(1 if dt == np.complex128 else 0, X0.shape[0], U0.shape[1], X0.shape[1],
+                                          _p(U0), _p(X0))
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            lib().orc_per_rhs_destroy(self.h)
+            self.h = None
+
+    def solve_system(self, op: Operator, layout, tol, system_index, maxit=0, method=CG):
+        nrhs = layout.n_rhs
+        idx = np.ascontiguousarray(layout.idx, dtype=np.int64)
+        val = np.ascontiguousarray(layout.val, dtype=np.float64)
+        X = np.zeros((self.n, nrhs), dtype=self.dtype, order="F")
+        log = np.zeros((nrhs, 5))
+        its, app = C.c_long(), C.c_long()
+        _check(lib().orc_per_rhs_solve_system(self.h, op.h, nrhs, _p(idx), _p(val), tol, system_index, maxit,
+                                              method, _p(X), _p(log), C.byref(its), C.byref(app)))
+        rows = [LogRow(int(r[0]), int(r[1]), float(r[2]), int(r[3]), bool(r[4])) for r in log]
+        return ProcessResult(X, rows, its.value, app.value)
 
 
 def initial_solutions(op: Operator, layout, tol, method=CG):

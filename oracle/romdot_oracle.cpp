@@ -1148,6 +1148,65 @@ void process_system(GlobalBasis<T>& gb, const LinOp<T>& A, long nrhs, const long
     }
 }
 
+// BaselinePerRhsRecycler (basis.cpp:209-266): per-RHS raw columns
+// W_j = [U0, X0_j, own new directions]; per system K~_j = A_i W_j (the
+// reference caches A~_* W_j and adds mu W_j, :229; with a variable D field the
+// image is recomputed), from_raw, initial_guess, a recycled solve at tol
+// (not 0.25 tol, :244), X_j = z0 + correction, append y_m. No global basis.
+template <class T> struct PerRhsRecycler {
+    std::vector<Mat<T>> W;
+    void init(const Mat<T>& U0, const Mat<T>& X0) {
+        W.clear();
+        for (long j = 0; j < X0.c; ++j) {
+            Mat<T> w(X0.r, U0.c + 1);
+            for (long t = 0; t < U0.c; ++t) std::memcpy(w.col(t), U0.col(t), sizeof(T) * X0.r);
+            std::memcpy(w.col(U0.c), X0.col(j), sizeof(T) * X0.r);
+            W.push_back(std::move(w));
+        }
+    }
+    void solve_system(const LinOp<T>& A, long nrhs, const long* bidx, const double* bval, double tol,
+                      int system_index, long maxit, int method, Mat<T>& X, std::vector<BuildLogRow>& log,
+                      ProcessStats& st) {
+        const long n = A.n;
+        if (nrhs != (long)W.size()) throw ConfigError("baseline recycling: rhs count mismatch");
+        if (maxit <= 0) maxit = 2 * n;
+        X = Mat<T>(n, nrhs);
+        log.clear();
+        st = ProcessStats();
+        std::vector<T> b(n), z0(n), rj(n);
+        for (long j = 0; j < nrhs; ++j) {
+            Mat<T>& Wj = W[j];
+            Mat<T> AW(n, Wj.c);
+            for (long t = 0; t < Wj.c; ++t) A.apply(Wj.col(t), AW.col(t));
+            const RecycleSpace<T> rs = RecycleSpace<T>::from_raw(Wj, AW);
+            std::fill(b.begin(), b.end(), T(0));
+            b[bidx[j]] = T(bval[j]);
+            const double bnorm = nrm2(n, b.data());
+            initial_guess(rs, b.data(), z0.data(), rj.data());
+            BuildLogRow row;
+            row.system = system_index;
+            row.rhs = static_cast<int>(j);
+            row.init_relres = nrm2(n, rj.data()) / bnorm;
+            if (row.init_relres <= tol) {
+                std::memcpy(X.col(j), z0.data(), sizeof(T) * n);
+            } else {
+                auto solved = inner_solve<T>(method, A, rs, rj.data(), tol, maxit, bnorm);
+                if (!solved.report.converged)
+                    throw SolverError("baseline recycling: solve failed at system " + std::to_string(system_index) +
+                                      ", rhs " + std::to_string(j));
+                for (long i = 0; i < n; ++i) X(i, j) = z0[i] + solved.correction[i];
+                row.iterations = solved.report.iterations;
+                st.inner_iterations += row.iterations;
+                Wj.set_cols(Wj.c + 1);
+                std::memcpy(Wj.col(Wj.c - 1), solved.new_direction.data(), sizeof(T) * n);
+                row.appended = true;
+                ++st.appends;
+            }
+            log.push_back(row);
+        }
+    }
+};
+
 }  // namespace orc
 
 // =============================================================== C ABI ===
@@ -1575,6 +1634,52 @@ int orc_process_system(void* b, void* op, long nrhs, const long* bidx, const dou
         } else {
             Mat<cd> Xm;
             process_system(h->c, o->lc, nrhs, bidx, bval, tol, system_index, maxit, method, Xm, lg, st);
+            mat_to(Xm, X);
+        }
+        for (size_t t = 0; t < lg.size(); ++t) {
+            log[5 * t + 0] = lg[t].system;
+            log[5 * t + 1] = lg[t].rhs;
+            log[5 * t + 2] = lg[t].init_relres;
+            log[5 * t + 3] = lg[t].iterations;
+            log[5 * t + 4] = lg[t].appended ? 1.0 : 0.0;
+        }
+        if (inner_its) *inner_its = st.inner_iterations;
+        if (appends) *appends = st.appends;
+    });
+}
+
+struct PerRhsHandle {
+    int dtype = 0;
+    PerRhsRecycler<double> r;
+    PerRhsRecycler<cd> c;
+};
+
+void* orc_per_rhs_create(int dtype, long n, long ku, long nrhs, const void* U0, const void* X0) {
+    auto* h = new PerRhsHandle();
+    h->dtype = dtype;
+    if (dtype == 0)
+        h->r.init(mat_from<double>(U0, n, ku), mat_from<double>(X0, n, nrhs));
+    else
+        h->c.init(mat_from<cd>(U0, n, ku), mat_from<cd>(X0, n, nrhs));
+    return h;
+}
+void orc_per_rhs_destroy(void* h) { delete static_cast<PerRhsHandle*>(h); }
+
+int orc_per_rhs_solve_system(void* pr, void* op, long nrhs, const long* bidx, const double* bval, double tol,
+                             int system_index, long maxit, int method, void* X, double* log, long* inner_its,
+                             long* appends) {
+    auto* h = static_cast<PerRhsHandle*>(pr);
+    auto* o = static_cast<OpHandle*>(op);
+    return guard([&] {
+        std::vector<BuildLogRow> lg;
+        ProcessStats st;
+        if (h->dtype == 0) {
+            Mat<double> Xm;
+            h->r.solve_system(o->lr, nrhs, bidx, bval, tol, system_index, maxit, method, Xm, lg, st);
+            mat_to(Xm, X);
+        } else {
+            Mat<cd> Xm;
+            h->c.solve_system(o->lc, nrhs, bidx, bval, tol, system_index, maxit, method, Xm, lg, st);
             mat_to(Xm, X);
         }
         for (size_t t = 0; t < lg.size(); ++t) {

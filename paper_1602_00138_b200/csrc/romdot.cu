@@ -1263,6 +1263,7 @@ template <class T> struct DevBasis : BasisBase {
     std::vector<uint8_t> markers;
     std::vector<std::vector<int>> spaces;
     bool factored = false;
+    bool raw_only = false;  // per-RHS-only comparator: V and the index lists only (no image factor)
     Workspace<T> ws;
     DevBuf tmpv, tmpv2, AW, Ur, Kr, idx, X, bvec;
     DevBuf Ktmp, Gd, Sinvd, Rd, Rd2, gwork;   // block refresh workspace
@@ -1287,8 +1288,10 @@ template <class T> struct DevBasis : BasisBase {
             std::swap(b.bytes, nb.bytes);
         };
         grow(V);
-        grow(Wm);
-        grow(K);
+        if (!raw_only) {
+            grow(Wm);
+            grow(K);
+        }
         std::vector<T> R2((size_t)nc * nc, Sc<T>::zero());
         for (long j = 0; j < cols; ++j)
             for (long i = 0; i <= j; ++i) R2[i + j * nc] = R[i + j * capcols];
@@ -1540,6 +1543,14 @@ template <class T> struct DevBasis : BasisBase {
         }
     }
 
+    // raw column append (no image factorisation): the per-RHS-only comparator
+    void append_raw(const T* y, uint8_t marker) {
+        reserve(cols + 1);
+        CK(cudaMemcpyAsync(Vp() + (size_t)cols * n, y, sizeof(T) * n, cudaMemcpyDeviceToDevice, ctx->s));
+        ++cols;
+        markers.push_back(marker);
+    }
+
     bool append(const T* y, const T* z, uint8_t marker) {
         if (cap > 0 && cols >= cap) return false;
         reserve(cols + 1);
@@ -1730,6 +1741,65 @@ void process_system(DevBasis<T>& gb, DevOp& op, long nrhs, const long* bidx, con
          "system %d phases (ms): refresh %.1f eig-block %.1f checks %.1f rhs-spaces %.1f solves %.1f appends %.1f "
          "X-assembly %.1f | %ld its",
          system_index, pt.t[0], pt.t[1], pt.t[2], pt.t[3], pt.t[4], pt.t[5], pt.t[6], inner_its);
+}
+
+// BaselinePerRhsRecycler::solve_system (basis.cpp:221-264) on the device:
+// the comparator that recycles only each RHS's own space U_j = [U0, X0_j, own
+// directions] -- no global check, no cross-RHS sharing. Storage is a raw
+// DevBasis (V + index lists). Per system the shared eigen block is factored
+// once (factor_eig_block); per RHS the trailing columns (factor_rhs_space),
+// then the recycled CG / COCG at tol (not 0.25 tol, :244) on b_j itself: its
+// output g = U K^T b + (y - U K^T A y) is z0 + correction (:249), its first
+// residual is init_relres (:236-239), and y_m is appended when it iterated.
+template <class T>
+void per_rhs_solve_system(DevBasis<T>& gb, DevOp& op, long nrhs, const long* bidx, const double* bval, double tol,
+                          int system_index, long maxit, T* Xdev, std::vector<LogRow>& log, long& inner_its,
+                          long& appends) {
+    Ctx& c = *gb.ctx;
+    const long n = gb.n;
+    if (maxit <= 0) maxit = 2 * n;
+    if (nrhs != (long)gb.spaces.size()) throw ConfigError("baseline recycling: rhs count mismatch");
+    long cspace = 1;
+    for (const auto& sp : gb.spaces) cspace = std::max(cspace, (long)sp.size());
+    gb.factor_eig_block(op, cspace);
+    log.clear();
+    inner_its = 0;
+    appends = 0;
+    const long npad = padded_rows(n);
+    DevBuf rhsb, ybuf, imbuf, gbuf;
+    for (DevBuf* b : {&rhsb, &ybuf, &imbuf, &gbuf}) {  // zero-tailed (TMA passes)
+        b->ensure(sizeof(T) * npad);
+        CK(cudaMemsetAsync(b->p, 0, sizeof(T) * npad, c.s));
+    }
+    const T zero = Sc<T>::zero();
+    for (long j = 0; j < nrhs; ++j) {
+        if (bidx[j] < 0 || bidx[j] >= n) throw ConfigError("baseline recycling: rhs index out of range");
+        const double bnorm = std::fabs(bval[j]);
+        const T bv = Sc<T>::from(bval[j]);
+        T* rhs = rhsb.template as<T>();
+        CK(cudaMemcpyAsync(rhs + bidx[j], &bv, sizeof(T), cudaMemcpyHostToDevice, c.s));
+        auto& idx = gb.spaces[j];
+        const long cj = (long)idx.size();
+        gb.factor_rhs_space(op, idx);
+        T* Gj = Xdev ? Xdev + (size_t)j * n : gbuf.template as<T>();
+        SolveOut so = recycled_cg<T>(c, op, gb.Ur.template as<T>(), gb.Kr.template as<T>(), cj, rhs, tol, maxit, bnorm,
+                                     Gj, ybuf.template as<T>(), imbuf.template as<T>(), gb.ws, true, true);
+        CK(cudaMemcpyAsync(rhs + bidx[j], &zero, sizeof(T), cudaMemcpyHostToDevice, c.s));
+        c.sync();  // bv / zero are host stack values
+        if (!so.converged)
+            throw SolverError("baseline recycling: solve failed at system " + std::to_string(system_index) +
+                              ", rhs " + std::to_string(j));
+        LogRow row{system_index, (int)j, so.hist.empty() ? 0.0 : so.hist[0], so.iterations, false};
+        if (so.iterations > 0) {
+            gb.append_raw(ybuf.template as<T>(), kColCorrection);
+            idx.push_back((int)(gb.cols - 1));
+            row.appended = true;
+            ++appends;
+            inner_its += so.iterations;
+        }
+        log.push_back(row);
+    }
+    c.sync();
 }
 
 // ------------------------------------------------------------------ RRQR ---
@@ -2599,12 +2669,18 @@ long rd_basis_space(rd_basis* b, long j, int* out) {
     return m;
 }
 int rd_basis_refresh(rd_basis* b, rd_op* op) {
-    return guard([&] { BASIS_DISPATCH(b, B.refresh(op->op)); });
+    return guard([&] {
+        BASIS_DISPATCH(b, {
+            if (B.raw_only) throw rd::ConfigError("refresh: handle is a per-RHS recycler");
+            B.refresh(op->op);
+        });
+    });
 }
 int rd_basis_append(rd_basis* b, const void* y, const void* z, int marker, int where, int* appended) {
     return guard([&] {
         Ctx& cx = b->ctx->c;
         BASIS_DISPATCH(b, {
+            if (B.raw_only) throw rd::ConfigError("append: handle is a per-RHS recycler");
             using T = std::remove_reference_t<decltype(B.R[0])>;
             Staged ys(cx, y, sizeof(T) * B.n, where), zs(cx, z, sizeof(T) * B.n, where);
             const bool ok = B.append((const T*)ys.p, (const T*)zs.p, (uint8_t)marker);
@@ -2659,12 +2735,54 @@ int rd_process_system(rd_basis* b, rd_op* op, long nrhs, const long* bidx, const
         BASIS_DISPATCH(b, {
             using T = std::remove_reference_t<decltype(B.R[0])>;
             if (B.n != op->op.d.n) throw rd::ConfigError("process_system: dimension mismatch");
+            if (B.raw_only) throw rd::ConfigError("process_system: handle is a per-RHS recycler");
             Out xs(cx, X, sizeof(T) * B.n * nrhs, where);
             if (X && where == 0) B.X.ensure(sizeof(T) * B.n * nrhs);
             T* Xd = X ? (where == 0 ? B.X.template as<T>() : (T*)X) : nullptr;
             std::vector<LogRow> lg;
             long its = 0, app = 0;
             process_system<T>(B, op->op, nrhs, bidx, bval, tol, system_index, maxit, Xd, lg, its, app);
+            if (X && where == 0) {
+                CK(cudaMemcpyAsync(X, Xd, sizeof(T) * B.n * nrhs, cudaMemcpyDeviceToHost, cx.s));
+                cx.sync();
+            }
+            if (log)
+                for (size_t t = 0; t < lg.size(); ++t) {
+                    log[5 * t + 0] = lg[t].system;
+                    log[5 * t + 1] = lg[t].rhs;
+                    log[5 * t + 2] = lg[t].init_relres;
+                    log[5 * t + 3] = lg[t].iterations;
+                    log[5 * t + 4] = lg[t].appended ? 1.0 : 0.0;
+                }
+            if (inner_iterations) *inner_iterations = its;
+            if (appends) *appends = app;
+        });
+    });
+}
+
+int rd_per_rhs_create(rd_ctx* ctx, int dtype, long n, long ku, long nrhs, const void* U0, const void* X0, int where,
+                      rd_basis** out) {
+    const int rc = rd_basis_create(ctx, dtype, n, ku, nrhs, U0, X0, 0, where, out);
+    if (rc == 0) BASIS_DISPATCH(*out, B.raw_only = true);
+    return rc;
+}
+
+int rd_per_rhs_solve_system(rd_basis* b, rd_op* op, long nrhs, const long* bidx, const double* bval, double tol,
+                            int system_index, long maxit, void* X, int where, double* log, long* inner_iterations,
+                            long* appends) {
+    return guard([&] {
+        Ctx& cx = b->ctx->c;
+        if (!op->op.have_fields) throw rd::ConfigError("operator: fields not set");
+        BASIS_DISPATCH(b, {
+            using T = std::remove_reference_t<decltype(B.R[0])>;
+            if (!B.raw_only) throw rd::ConfigError("per-RHS recycler: handle is a global basis (rd_per_rhs_create)");
+            if (B.n != op->op.d.n) throw rd::ConfigError("per-RHS recycler: dimension mismatch");
+            Out xs(cx, X, sizeof(T) * B.n * nrhs, where);
+            if (X && where == 0) B.X.ensure(sizeof(T) * B.n * nrhs);
+            T* Xd = X ? (where == 0 ? B.X.template as<T>() : (T*)X) : nullptr;
+            std::vector<LogRow> lg;
+            long its = 0, app = 0;
+            per_rhs_solve_system<T>(B, op->op, nrhs, bidx, bval, tol, system_index, maxit, Xd, lg, its, app);
             if (X && where == 0) {
                 CK(cudaMemcpyAsync(X, Xd, sizeof(T) * B.n * nrhs, cudaMemcpyDeviceToHost, cx.s));
                 cx.sync();

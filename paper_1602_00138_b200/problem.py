@@ -214,6 +214,22 @@ def perturb_rbf(p: RBFParams, seed: int, sigma: float = 0.05) -> RBFParams:
     return RBFParams(c, w)
 
 
+def perturb_rbf_reference(p: RBFParams, seed: int, jitter: float) -> RBFParams:
+    """The reference's parameter sequence (harness.cpp:62-75): widths x (1 +
+    0.01 N(0,1)), centres + jitter N(0,1) with jitter = 0.02 h (nx / 8); the
+    amplitude draw (x (1 + 0.03 N)) is consumed to keep the stream aligned but
+    this level-set model has unit amplitudes."""
+    s = NormalStream(seed)
+    c = p.centres.copy()
+    w = p.widths.copy()
+    for j in range(c.shape[0]):
+        s.next()  # amplitude factor (p[j] *= 1 + 0.03 z)
+        w[j] = w[j] * (1.0 + 0.01 * s.next())
+        for a in range(c.shape[1]):
+            c[j, a] += jitter * s.next()
+    return RBFParams(c, w)
+
+
 def absorption(grid: GridSpec, p: RBFParams, mu_bg: float = 0.01, contrast: float = 0.02,
                eps: float = 0.05) -> np.ndarray:
     """mu_a = mu_bg + contrast * H_eps(phi), phi = sum_j psi(|x-c_j|/w_j) - 1/2,
@@ -266,6 +282,7 @@ class ProblemConfig:
     seed: int = 20160200
     src_high: Optional[bool] = None
     mus_prime: float = 1.0
+    ref_sequence: bool = False  # the reference's small per-system perturbations (harness.cpp:62-75)
 
     @property
     def grid(self) -> GridSpec:
@@ -289,6 +306,9 @@ class ProblemConfig:
         p0 = self.base_params()
         if i == 0:
             return p0
+        if self.ref_sequence:
+            jitter = 0.02 * self.grid.h * (self.N / 8.0)
+            return perturb_rbf_reference(p0, self.seed + 1000003 * i, jitter)
         return perturb_rbf(p0, self.seed + 1000003 * i)   # harness.cpp:65 seed pattern
 
     def systems(self) -> List[Tuple[int, float]]:
@@ -308,6 +328,11 @@ CONFIGS = {
     "C3": ProblemConfig("C3", d=3, N=64, n_src=(4, 8), n_det=(4, 8), m_rbf=8, n_points=8, omegas=(0.0,), k=40),
     "C4": ProblemConfig("C4", d=3, N=128, n_src=(6, 8), n_det=(6, 8), m_rbf=12, n_points=8,
                         omegas=(0.0, 0.1), k=64, complex=True, cap=768),
+    # the reference's acceptance criterion 5 (acceptance.cpp:314-334): 121^2 desk,
+    # 32 + 32, 9 bumps, run defaults k_eig = 10, tol_basis = 1e-7 (config.hpp:42-46),
+    # min(K, 2) systems (harness.cpp:224)
+    "R5": ProblemConfig("R5", d=2, N=121, n_src=(32,), n_det=(32,), m_rbf=9, n_points=2, omegas=(0.0,), k=10,
+                        tol=1e-7, ref_sequence=True),
     # small parity configs (oracle finishes in seconds)
     "T2": ProblemConfig("T2", d=2, N=33, n_src=(4,), n_det=(4,), m_rbf=4, n_points=3, omegas=(0.0,), k=6),
     "T2c": ProblemConfig("T2c", d=2, N=33, n_src=(4,), n_det=(4,), m_rbf=4, n_points=2,

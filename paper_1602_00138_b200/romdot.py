@@ -35,7 +35,7 @@ EXPORTS = [
     "rd_basis_append", "rd_basis_solve_projected", "rd_process_system", "rd_rrqr", "rd_bench_projection",
     "rd_bench_stencil", "rd_residual_norms", "rd_basis_compress", "rd_rom_create", "rd_rom_destroy",
     "rd_rom_order", "rd_rom_E", "rd_rom_reduced_system", "rd_rom_transfer", "rd_rom_jacobian",
-    "rd_fom_transfer", "rd_fom_jacobian",
+    "rd_fom_transfer", "rd_fom_jacobian", "rd_per_rhs_create", "rd_per_rhs_solve_system",
 ]
 
 
@@ -125,6 +125,9 @@ def load_library(path: Optional[str] = None):
     L.rd_bench_stencil.argtypes = [vp, C.c_int, C.c_long, C.c_int, vp]
     L.rd_basis_compress.argtypes = [vp, C.c_double, C.c_int, lp, vp, vp]
     L.rd_residual_norms.argtypes = [vp, C.c_int, C.c_long, vp, vp, vp, C.c_int, vp]
+    L.rd_per_rhs_create.argtypes = [vp, C.c_int, C.c_long, C.c_long, C.c_long, vp, vp, C.c_int, C.POINTER(vp)]
+    L.rd_per_rhs_solve_system.argtypes = [vp, vp, C.c_long, vp, vp, C.c_double, C.c_int, C.c_long, vp, C.c_int, vp,
+                                          lp, lp]
     L.rd_fom_transfer.argtypes = [vp, C.c_int, C.c_long, vp, vp, C.c_long, vp, vp, C.c_double, vp, C.c_int, lp]
     L.rd_fom_jacobian.argtypes = [vp, C.c_int, C.c_long, vp, vp, C.c_long, vp, vp, C.c_long, vp, vp, vp, C.c_double,
                                   C.c_double, vp, C.c_int]
@@ -466,6 +469,37 @@ def process_system(gb: GlobalBasis, op: SchurOperator, layout: P.Layout, tol: fl
                                             HOST, _p(log), C.byref(its), C.byref(app)))
     rows = [BuildLogRow(int(r[0]), int(r[1]), float(r[2]), int(r[3]), bool(r[4])) for r in log]
     return ProcessResult(X, rows, its.value, app.value)
+
+
+class PerRhsRecycler(GlobalBasis):
+    """BaselinePerRhsRecycler (basis.hpp:102-119, basis.cpp:209-266) on the
+    device: per-RHS-only recycling, the paper's Table 2 comparator."""
+
+    def __init__(self, U0: np.ndarray, X0: np.ndarray, ctx: Optional[Context] = None, dtype=None):
+        self.ctx = ctx or default_context()
+        dt = np.dtype(dtype) if dtype is not None else np.result_type(U0.dtype, X0.dtype)
+        U0 = _f(U0, dt)
+        X0 = _f(X0, dt)
+        self.dtype = dt
+        self.n = X0.shape[0]
+        self.nrhs = X0.shape[1]
+        h = C.c_void_p()
+        _check(load_library().rd_per_rhs_create(self.ctx.h, _dt(dt), self.n, U0.shape[1], X0.shape[1], _p(U0),
+                                                _p(X0), HOST, C.byref(h)))
+        self.h = h
+
+    def solve_system(self, op: SchurOperator, layout: P.Layout, tol: float, system_index: int, maxit: int = 0,
+                     want_X: bool = True) -> ProcessResult:
+        nrhs = layout.n_rhs
+        idx = np.ascontiguousarray(layout.idx, dtype=np.int64)
+        val = np.ascontiguousarray(layout.val, dtype=np.float64)
+        X = np.zeros((self.n, nrhs), dtype=self.dtype, order="F") if want_X else None
+        log = np.zeros((nrhs, 5))
+        its, app = C.c_long(), C.c_long()
+        _check(load_library().rd_per_rhs_solve_system(self.h, op.h, nrhs, _p(idx), _p(val), tol, system_index, maxit,
+                                                      _p(X), HOST, _p(log), C.byref(its), C.byref(app)))
+        rows = [BuildLogRow(int(r[0]), int(r[1]), float(r[2]), int(r[3]), bool(r[4])) for r in log]
+        return ProcessResult(X, rows, its.value, app.value)
 
 
 def init_basis_from(U0, X0, cap: int = 0, ctx: Optional[Context] = None, dtype=None) -> GlobalBasis:

@@ -320,3 +320,53 @@ def test_basis_compress_in_place(rd):
     Ut = Un[:, sn >= 1e-6 * sn[0]]
     s = np.linalg.svd(Q.T @ Ut, compute_uv=False)
     assert np.sqrt(max(0.0, 1 - s.min() ** 2)) <= 1e-6
+
+
+@pytest.mark.parametrize("cfg", ["T2", "T3c"])
+def test_per_rhs_recycler_lockstep_parity(rd, cfg):
+    """BaselinePerRhsRecycler (basis.cpp:209-266) on the device vs the CPU
+    checker from identical U0/X0: every log row (±2 iterations, same append
+    decisions, init_relres), explicit residual <= tol (test_basis.cpp:225-240)."""
+    c = P.CONFIGS[cfg]
+    g, lay = c.grid, c.layout()
+    U0, X0 = _shared_seed(c, g, lay)
+    po_ = orc.PerRhsRecycler(U0, X0)
+    pg_ = rd.PerRhsRecycler(U0, X0)
+    B = lay.dense(g.n, c.dtype)
+    appends = 0
+    for s, (pt, w) in enumerate(c.systems(), start=1):
+        f = c.fields(pt, w)
+        op_o = orc.Operator.grid(g, f, c.dtype)
+        po = po_.solve_system(op_o, lay, c.tol, s)
+        pg = pg_.solve_system(rd.SchurOperator(g, f, c.dtype), lay, c.tol, s)
+        R = op_o.apply(pg.X) - B
+        assert (np.linalg.norm(R, axis=0) <= c.tol * np.linalg.norm(B, axis=0)).all()
+        for ro, rg in zip(po.log, pg.log):
+            assert ro.appended == rg.appended, (s, ro, rg)
+            assert abs(ro.iterations - rg.iterations) <= 2, (s, ro, rg)
+            assert ro.init_relres == pytest.approx(rg.init_relres, rel=1e-6, abs=1e-13)
+        appends += pg.appends
+    # V = [U0, X0, every RHS's own directions]; U_j = [U0, X0_j, own directions]
+    assert pg_.cols == c.k + lay.n_rhs + appends
+    assert sum(len(pg_.space(j)) for j in range(lay.n_rhs)) == lay.n_rhs * (c.k + 1) + appends
+
+
+def test_global_basis_beats_per_rhs_recycling(rd):
+    """Acceptance criterion 5 (acceptance.cpp:314-334, cmd_compare_recycling
+    harness.cpp:209-252) on R5, its 121^2 / 32+32 / k_eig 10 / tol 1e-7 mirror
+    with the reference's parameter sequence: the shared-basis build needs
+    about half the inner iterations of per-RHS-only recycling. The reference
+    asserts <= 0.5 on its PaLS phantom; on this level-set phantom the CPU
+    checker gives 4941 / 9634 = 0.513 (CG), which the device must reproduce."""
+    c = P.CONFIGS["R5"]
+    g, lay = c.grid, c.layout()
+    U0, X0 = _shared_seed(c, g, lay)
+    gb = rd.GlobalBasis(U0, X0, c.cap)
+    pr = rd.PerRhsRecycler(U0, X0)
+    ours = base = 0
+    for s, (pt, w) in enumerate(c.systems()[:2], start=1):
+        f = c.fields(pt, w)
+        ours += rd.process_system(gb, rd.SchurOperator(g, f, c.dtype), lay, c.tol, s, want_X=False).inner_iterations
+        base += pr.solve_system(rd.SchurOperator(g, f, c.dtype), lay, c.tol, s, want_X=False).inner_iterations
+    assert ours / base <= 0.6, (ours, base)
+    assert abs(ours - 4941) <= 2 * 128 and abs(base - 9634) <= 2 * 128, (ours, base)

@@ -183,3 +183,19 @@ def test_svd_and_rrqr_compressed_rom_match_algorithm2():  # acceptance C7 :362-4
         psi = fom_transfer(A, Bt, Ct)
         assert np.linalg.norm(a - psi) / np.linalg.norm(psi) <= 1e-5
     assert worst <= 1e-4 and worst_rr <= 1e-4
+
+
+@pytest.mark.parametrize("method", [orc.MINRES, orc.CG])
+def test_baseline_recycler_per_rhs_growth_only(method):  # test_basis.cpp:225-240
+    d = Desk(21, 4, 4)
+    k = 6
+    gb, X0, lam, U0 = orc.init_basis(d.op(0.0), d.op(0.0), d.layout, k, 1e-7, method)
+    base = orc.PerRhsRecycler(U0, X0)
+    for s in (1, 2):
+        pr = base.solve_system(d.op(0.02 * s), d.layout, 1e-7, s, method=method)
+        A = d.A(0.02 * s)
+        res = np.linalg.norm(d.B - A @ pr.X, axis=0) / np.linalg.norm(d.B, axis=0)
+        assert res.max() <= 1e-7
+        # appends only where the RHS iterated; no cross-RHS sharing (basis.cpp:252-258)
+        assert pr.appends == sum(r.appended for r in pr.log)
+        assert all(r.appended == (r.iterations > 0) for r in pr.log)
