@@ -12,6 +12,8 @@
 //   MODE 1  x'  = x - K c1 ; c2 = op(K)^T x'         (fused second CGS pass)
 //   MODE 2  q   = w' - K c2 ; p = r + beta p ; s = q + beta s ;
 //           y  += alpha p ; r -= alpha s             (CG/COCG update)
+//           with G = K^T K given: q = w - K (2 c1 - G c1), the one-pass
+//           projection with the Gram-corrected second CGS coefficient
 //   MODE 3  x'  = x - K c                            (N pass, global basis)
 //
 // TMAP = true streams a column-major matrix (the global basis V/W/K_img,
@@ -83,7 +85,7 @@ __global__ void __launch_bounds__(TMA_THREADS, 1)
     ts_tma(const __grid_constant__ CUtensorMap tmap, int col0, const T* __restrict__ Krb, int C, long n, long ntile,
            TmaLayout L, const T* __restrict__ x,
            T* __restrict__ xo, const double* __restrict__ cin, GridRed red, double* out, T* __restrict__ r,
-           T* __restrict__ p, T* __restrict__ s, T* __restrict__ y, CGState* st) {
+           T* __restrict__ p, T* __restrict__ s, T* __restrict__ y, CGState* st, const T* __restrict__ G) {
     if (st && st->done) return;
     constexpr int W = Sc<T>::W;
     extern __shared__ __align__(128) unsigned char smem[];
@@ -103,8 +105,23 @@ __global__ void __launch_bounds__(TMA_THREADS, 1)
         }
         fence_mbar_init();
     }
-    if (MODE != 0)
+    if (MODE == 2 && G) {
+        // one-pass projection with the Gram correction: coef = c1 + (c1 - G c1),
+        // the second CGS coefficient K^T (w - K c1) = c1 - (K^T K) c1 formed from
+        // the solve's fixed Gram G = K^T K (symmetric: column t = row t) instead
+        // of a third stream over K. c1 is staged in the vals region (unused here).
+        T* c1s = reinterpret_cast<T*>(smem + L.off_vals);
+        for (int t = tid; t < C; t += blockDim.x) c1s[t] = Sc<T>::get(cin + (size_t)t * W);
+        __syncthreads();
+        for (int t = tid; t < C; t += blockDim.x) {
+            const T* gc = G + (size_t)t * C;
+            T acc = Sc<T>::zero();
+            for (int j = 0; j < C; ++j) acc = Sc<T>::fma(gc[j], c1s[j], acc);
+            cw[t] = Sc<T>::sub(Sc<T>::scale(c1s[t], 2.0), acc);
+        }
+    } else if (MODE != 0) {
         for (int t = tid; t < C; t += blockDim.x) cw[t] = Sc<T>::get(cin + (size_t)t * W);
+    }
     __syncthreads();
 
     if (wid == TMA_CONSUMERS / 32) {
