@@ -413,6 +413,26 @@ __global__ void __launch_bounds__(256) bcg_update(T* __restrict__ R, T* __restri
     }
 }
 
+// Symmetric Gram of a per-RHS recycle space K = [Q0 Kt] (c = ku + m columns):
+// G[:ku, :ku] = G00 (the system's eigen block, ld ku), G[:, ku:] = Gt (c x m,
+// ld c), G[ku:, :ku] = Gt[:ku, :]^T (bilinear: no conjugation).
+template <class T>
+__global__ void assemble_space_gram(const T* __restrict__ G00, int ku, const T* __restrict__ Gt, int c,
+                                    T* __restrict__ G) {
+    const long tot = (long)c * c;
+    for (long e = blockIdx.x * (long)blockDim.x + threadIdx.x; e < tot; e += (long)gridDim.x * blockDim.x) {
+        const int i = (int)(e % c), j = (int)(e / c);
+        T v;
+        if (j >= ku)
+            v = Gt[(size_t)(j - ku) * c + i];
+        else if (i >= ku)
+            v = Gt[(size_t)(i - ku) * c + j];
+        else
+            v = G00[(size_t)j * ku + i];
+        G[e] = v;
+    }
+}
+
 // R[idx[c] + c*ld] = val[c] (unit right-hand sides of the layout)
 template <class T>
 __global__ void scatter_unit_rhs(T* R, long ld, const long* __restrict__ idx, const double* __restrict__ val, int m) {

@@ -739,6 +739,18 @@ template <class T> struct Workspace {
     }
 };
 
+// One-pass inner projection with the Gram-corrected second CGS coefficient
+// (default; ROMDOT_CGS1G=0 selects the three-stream CGS2, ROMDOT_NO_TMA the
+// non-TMA kernels, which use CGS2).
+inline bool use_one_pass_projection() {
+    static const bool on = [] {
+        const char* e = std::getenv("ROMDOT_CGS1G");
+        const char* t = std::getenv("ROMDOT_NO_TMA");
+        return (e ? std::atoi(e) : 1) != 0 && (t ? std::atoi(t) : 0) == 0;
+    }();
+    return on;
+}
+
 // Recycled CG / COCG (the CPU checker under oracle/ restates the same recurrence).
 // rhs, U, K, g, y_out, image: device. g/y_out/image may alias workspace-free
 // buffers only.
@@ -747,7 +759,7 @@ template <class T> struct Workspace {
 template <class T>
 SolveOut recycled_cg(Ctx& c, DevOp& op, const T* U, const T* K, long ncol, const T* rhs, double tol, long maxit,
                      double rhs_scale, T* g, T* y_out, T* image, Workspace<T>& ws, bool want_hist,
-                     bool padded_io = false) {
+                     bool padded_io = false, const T* Gpre = nullptr) {
     constexpr int W = Sc<T>::W;
     const long n = op.n();
     const long npad = padded_rows(n);
@@ -815,18 +827,12 @@ SolveOut recycled_cg(Ctx& c, DevOp& op, const T* U, const T* K, long ncol, const
     // iteration counts and residuals as the three-stream CGS2 at C4 (29,206
     // iterations, max residual 9.98e-9 over three systems) in 24% less time.
     // ROMDOT_CGS1G=0 selects the three-stream CGS2 (MODE 0 / 1 / 2).
-    static const int cgs1g = [] {
-        const char* e = std::getenv("ROMDOT_CGS1G");
-        return e ? std::atoi(e) : 1;
-    }();
-    static const int no_tma_env = [] {
-        const char* e = std::getenv("ROMDOT_NO_TMA");
-        return e ? std::atoi(e) : 0;
-    }();
-    const bool gram_pass = cgs1g && ncol > 0 && ncol <= 128 && !no_tma_env;
-    if (gram_pass) {
+    const bool gram_pass = use_one_pass_projection() && ncol > 0 && ncol <= 128;
+    const T* Gk = Gpre;
+    if (gram_pass && !Gk) {
         ws.gk.ensure(sizeof(T) * ncol * ncol);
         gram<T, false>(c, K, n, ncol, K, n, ncol, n, ws.gk.template as<T>(), true, ws.gwork);
+        Gk = ws.gk.template as<T>();
     }
     const int batch = n < 200000 ? 16 : 8;
     long batches = 0;
@@ -855,8 +861,7 @@ SolveOut recycled_cg(Ctx& c, DevOp& op, const T* U, const T* K, long ncol, const
                                     st);
                 if (samp) c.prof_stop(e1, 1, n * es * (ncol + 1.0), iter);
                 cudaEvent_t e3 = samp ? c.prof_start() : nullptr;
-                ts_tma_launch<T, 2>(c, Kit, (int)ncol, n, w, nullptr, c1, nullptr, r, p, s, y, st,
-                                    ws.gk.template as<T>());
+                ts_tma_launch<T, 2>(c, Kit, (int)ncol, n, w, nullptr, c1, nullptr, r, p, s, y, st, Gk);
                 if (samp) c.prof_stop(e3, 3, n * es * (ncol + 9.0), iter);
             } else if (ncol > 0) {
                 static const int tma_mask = [] {
@@ -1296,6 +1301,7 @@ template <class T> struct DevBasis : BasisBase {
     Workspace<T> ws;
     DevBuf tmpv, tmpv2, AW, Ur, Kr, idx, X, bvec;
     DevBuf Ktmp, Gd, Sinvd, Rd, Rd2, gwork;   // block refresh workspace
+    DevBuf G00, Gt, Gsp;                     // bilinear Gram of the eigen block / of the current space
     long eig_ready_for = -1;                 // system tag whose eig-block factor sits in Ur/Kr
     long cmax_space = 0;
     long stats_block_refresh = 0, stats_seq_refresh = 0, stats_second_pass = 0;
@@ -1519,6 +1525,31 @@ template <class T> struct DevBasis : BasisBase {
             CK(cudaMemcpyAsync(Ub, S, sizeof(T) * n * ku, cudaMemcpyDeviceToDevice, c.s));
             if (ci.kappa1 <= 20.0) break;
         }
+        // G00 = Q0^T Q0 of the final eigen-block factor (shared by every RHS's
+        // space Gram, used by the one-pass inner projection)
+        G00.ensure(sizeof(T) * ku * ku);
+        gram<T, false>(c, Kb, n, ku, Kb, n, ku, n, G00.template as<T>(), true, gwork);
+    }
+
+    // G = K^T K of the space factored last (ku + m columns): G00 plus the thin
+    // block [Q0 Kt]^T Kt in <= 8-column chunks. Returns the device pointer.
+    const T* space_gram(long cj) {
+        Ctx& c = *ctx;
+        const long m = cj - ku;
+        Gsp.ensure(sizeof(T) * std::max(1L, cj * cj));
+        if (m <= 0) return ku > 0 ? G00.template as<T>() : nullptr;
+        T* Kb = Kr.template as<T>();
+        const T* Kt = Kb + (size_t)ku * n;
+        Gt.ensure(sizeof(T) * cj * m);
+        for (long t0 = 0; t0 < m; t0 += 8) {
+            const long b = std::min(8L, m - t0);
+            gram<T, false>(c, Kb, n, cj, Kt + (size_t)t0 * n, n, b, n, Gt.template as<T>() + (size_t)t0 * cj, false,
+                           gwork);
+        }
+        assemble_space_gram<T><<<c.grid_for(cj * cj, 256, 1), 256, 0, c.s>>>(
+            ku > 0 ? G00.template as<T>() : nullptr, (int)ku, Gt.template as<T>(), (int)cj, Gsp.template as<T>());
+        c.check_launch();
+        return Gsp.template as<T>();
     }
 
     void factor_rhs_space(DevOp& op, const std::vector<int>& cidx) {
@@ -1732,9 +1763,10 @@ void process_system(DevBasis<T>& gb, DevOp& op, long nrhs, const long* bidx, con
             lap(3);
             dbg_sum("space K", gb.Kr.template as<T>(), n * cj, c.s);
             dbg_sum("space U", gb.Ur.template as<T>(), n * cj, c.s);
+            const T* Gsp = use_one_pass_projection() ? gb.space_gram(cj) : nullptr;
             SolveOut so = recycled_cg<T>(c, op, gb.Ur.template as<T>(), gb.Kr.template as<T>(), cj, rhs,
                                          kInnerSafety * tol, maxit, bnorm, Gj, ybuf.template as<T>(),
-                                         imbuf.template as<T>(), gb.ws, false, true);
+                                         imbuf.template as<T>(), gb.ws, false, true, Gsp);
             if (!so.converged)
                 throw SolverError("process_system: correction solve failed at system " +
                                   std::to_string(system_index) + ", rhs " + std::to_string(j));
@@ -1811,8 +1843,9 @@ void per_rhs_solve_system(DevBasis<T>& gb, DevOp& op, long nrhs, const long* bid
         const long cj = (long)idx.size();
         gb.factor_rhs_space(op, idx);
         T* Gj = Xdev ? Xdev + (size_t)j * n : gbuf.template as<T>();
+        const T* Gsp = use_one_pass_projection() ? gb.space_gram(cj) : nullptr;
         SolveOut so = recycled_cg<T>(c, op, gb.Ur.template as<T>(), gb.Kr.template as<T>(), cj, rhs, tol, maxit, bnorm,
-                                     Gj, ybuf.template as<T>(), imbuf.template as<T>(), gb.ws, true, true);
+                                     Gj, ybuf.template as<T>(), imbuf.template as<T>(), gb.ws, true, true, Gsp);
         CK(cudaMemcpyAsync(rhs + bidx[j], &zero, sizeof(T), cudaMemcpyHostToDevice, c.s));
         c.sync();  // bv / zero are host stack values
         if (!so.converged)
