@@ -152,8 +152,19 @@ __device__ inline void grid_finish(const GridRed& g, int nv, double* out /* shar
     for (int v0 = 0; v0 < nv; v0 += groups) {
         const int v = v0 + threadIdx.x / tpc;
         double s = 0.0;
-        if (v < nv)
-            for (unsigned b = sub; b < nb; b += tpc) s += __ldcg(g.partials + (size_t)b * nv + v);
+        if (v < nv) {
+            // eight independent accumulators keep eight L2 loads in flight (a
+            // single chain serialises nb / tpc round trips); fixed association
+            const double* pp = g.partials + v;
+            double a[8] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+            unsigned b = sub;
+            for (; b + 7u * tpc < nb; b += 8u * tpc) {
+#pragma unroll
+                for (int q = 0; q < 8; ++q) a[q] += __ldcg(pp + (size_t)(b + q * tpc) * nv);
+            }
+            for (int q = 0; b < nb; b += tpc, ++q) a[q & 7] += __ldcg(pp + (size_t)b * nv);
+            s = ((a[0] + a[1]) + (a[2] + a[3])) + ((a[4] + a[5]) + (a[6] + a[7]));
+        }
         // combine tpc lanes (tpc divides 32 and groups are lane-aligned)
         for (int o = tpc >> 1; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
         if (v < nv && sub == 0) out[v] = s;

@@ -493,9 +493,17 @@ __global__ void __launch_bounds__(256) gram_thin(const T* __restrict__ X, long l
     const int nyc = gridDim.y;
     for (int e = threadIdx.x; e < nyc * nv; e += blockDim.x) {
         const int yc = e / nv, vv = e % nv;
-        double sum = 0.0;
-        for (unsigned bx = 0; bx < gridDim.x; ++bx)
-            sum += __ldcg(red.partials + (size_t)(bx + gridDim.x * yc) * nv + vv);
+        // eight independent accumulators (eight L2 loads in flight), fixed order
+        const double* pp = red.partials + (size_t)gridDim.x * yc * nv + vv;
+        double acc8[8] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+        unsigned bx = 0;
+        for (; bx + 8 <= gridDim.x; bx += 8) {
+#pragma unroll
+            for (int q = 0; q < 8; ++q) acc8[q] += __ldcg(pp + (size_t)(bx + q) * nv);
+        }
+        for (int q = 0; bx < gridDim.x; ++bx, ++q) acc8[q] += __ldcg(pp + (size_t)bx * nv);
+        const double sum =
+            ((acc8[0] + acc8[1]) + (acc8[2] + acc8[3])) + ((acc8[4] + acc8[5]) + (acc8[6] + acc8[7]));
         const int colr = vv / (B * W), v = (vv / W) % B, w = vv % W;
         const int col = yc * 32 + colr;
         if (col < a && v < b) reinterpret_cast<double*>(G)[((size_t)v * a + col) * W + w] = sum;

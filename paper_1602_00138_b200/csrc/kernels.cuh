@@ -413,6 +413,27 @@ __global__ void __launch_bounds__(256) bcg_update(T* __restrict__ R, T* __restri
     }
 }
 
+// Selective reorthogonalisation (Kahan-Parlett "twice is enough"): after the
+// first CGS pass, ||q1||^2 = ||z||^2 - ||c1||^2; when that keeps at least half
+// of ||z||^2 the first pass is already accurate to O(eps) and the second is
+// skipped: flag->done = 1 (the second-pass kernels then exit at entry) and
+// c2 = 0. Otherwise flag->done = 0 and the second pass runs.
+__global__ void reorth_decide(const double* __restrict__ c1, int nv, const double* __restrict__ nrmz, double* c2,
+                              CGState* flag) {
+    __shared__ double s_red[32];
+    __shared__ int s_skip;
+    double a = 0.0;
+    for (int i = threadIdx.x; i < nv; i += blockDim.x) a += c1[i] * c1[i];
+    a = block_sum(a, s_red);
+    if (threadIdx.x == 0) {
+        s_skip = (a <= 0.5 * nrmz[0]) ? 1 : 0;
+        flag->done = s_skip;
+    }
+    __syncthreads();
+    if (s_skip)
+        for (int i = threadIdx.x; i < nv; i += blockDim.x) c2[i] = 0.0;
+}
+
 // Symmetric Gram of a per-RHS recycle space K = [Q0 Kt] (c = ku + m columns):
 // G[:ku, :ku] = G00 (the system's eigen block, ld ku), G[:, ku:] = Gt (c x m,
 // ld c), G[ku:, :ku] = Gt[:ku, :]^T (bilinear: no conjugation).

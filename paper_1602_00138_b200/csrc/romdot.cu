@@ -171,7 +171,7 @@ struct Ctx {
     int device = 0;
     int sms = 148;
     cudaStream_t s = nullptr;
-    DevBuf partials, counter, scal, cgst, hist;
+    DevBuf partials, counter, scal, cgst, hist, rflag;
     CGState* st_host = nullptr;  // pinned, 2 slots
     cudaEvent_t ev[2] = {nullptr, nullptr};
     cudaEvent_t mark[2] = {nullptr, nullptr};
@@ -637,7 +637,7 @@ template <class T, bool HERM> CholInfo chol_inv(Ctx& c, T* G, T* Sinv, long r, b
 // padded to padded_rows(n) (the TMA x tile of the last row block).
 template <class T, int MODE, bool HERM>
 void global_tma_chunk(Ctx& c, const T* K, long ld, long ncols, long col0, int cc, const T* x, T* xo, const double* cin,
-                      double* out, long n) {
+                      double* out, long n, CGState* st = nullptr) {
     constexpr int CPW = 16;
     const int es = sizeof(T);
     TmaLayout L = tma_layout<T>(cc, 32, 2, 1);
@@ -662,7 +662,7 @@ void global_tma_chunk(Ctx& c, const T* K, long ld, long ncols, long col0, int cc
     const int grid = (int)std::max(1L, std::min<long>(ntile, (long)c.sms));
     ts_tma<T, MODE, HERM, CPW, true><<<grid, TMA_THREADS, L.total, c.s>>>(
         tm, (int)col0, nullptr, cc, n, ntile, L, x, xo, cin ? cin + col0 * Sc<T>::W : nullptr, c.red(),
-        out ? out + col0 * Sc<T>::W : nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr);
+        out ? out + col0 * Sc<T>::W : nullptr, nullptr, nullptr, nullptr, nullptr, st, nullptr);
     c.check_launch();
     (void)es;
 }
@@ -677,25 +677,28 @@ template <class T> bool tma_ok(long ld) {
 
 // out = op(K)^T x   (x padded)
 template <class T, bool HERM>
-void global_T(Ctx& c, const T* K, long ld, long ncols, const T* x, long n, double* out) {
+void global_T(Ctx& c, const T* K, long ld, long ncols, const T* x, long n, double* out, CGState* st = nullptr) {
     if (!tma_ok<T>(ld)) {
-        ts_T_launch<T, HERM>(c, K, ld, ncols, x, n, out);
+        ts_T_launch<T, HERM>(c, K, ld, ncols, x, n, out, st);
         return;
     }
     for (long c0 = 0; c0 < ncols; c0 += 128)
-        global_tma_chunk<T, 0, HERM>(c, K, ld, ncols, c0, (int)std::min(128L, ncols - c0), x, nullptr, nullptr, out, n);
+        global_tma_chunk<T, 0, HERM>(c, K, ld, ncols, c0, (int)std::min(128L, ncols - c0), x, nullptr, nullptr, out, n,
+                                     st);
 }
 
 // xo = x - K cin  (x, xo padded; may alias)
 template <class T>
-void global_N(Ctx& c, const T* K, long ld, long ncols, const T* x, T* xo, long n, const double* cin) {
+void global_N(Ctx& c, const T* K, long ld, long ncols, const T* x, T* xo, long n, const double* cin,
+              CGState* st = nullptr) {
     if (!tma_ok<T>(ld) || ncols == 0) {
-        ts_N_launch<T>(c, K, ld, ncols, x, xo, n, cin);
+        ts_N_launch<T>(c, K, ld, ncols, x, xo, n, cin, 1.0, st);
         return;
     }
     const T* src = x;
     for (long c0 = 0; c0 < ncols; c0 += 128) {
-        global_tma_chunk<T, 3, false>(c, K, ld, ncols, c0, (int)std::min(128L, ncols - c0), src, xo, cin, nullptr, n);
+        global_tma_chunk<T, 3, false>(c, K, ld, ncols, c0, (int)std::min(128L, ncols - c0), src, xo, cin, nullptr, n,
+                                      st);
         src = xo;
     }
 }
@@ -713,6 +716,26 @@ void cgs2_global(Ctx& c, const T* Q, long ldq, long t, const T* z, T* q, long n,
     global_N<T>(c, Q, ldq, t, z, q, n, tmp1);
     global_T<T, HERM>(c, Q, ldq, t, q, n, tmp2);
     global_N<T>(c, Q, ldq, t, q, q, n, tmp2);
+    launch_addsub(c, (int)(t * W), tmp1, tmp2, 1.0, coef);
+}
+
+// CGS2 with the second pass run only when the first cancelled more than half
+// of ||z||^2 (reorth_decide; device-side, no host sync). nrmz[0] = ||z||^2 on
+// entry (launch_norms). flag is scratch device state.
+template <class T, bool HERM>
+void cgs2_global_selective(Ctx& c, const T* Q, long ldq, long t, const T* z, T* q, long n, double* coef,
+                           double* tmp1, double* tmp2, const double* nrmz, CGState* flag) {
+    constexpr int W = Sc<T>::W;
+    if (t == 0) {
+        if (q != z) CK(cudaMemcpyAsync(q, z, sizeof(T) * n, cudaMemcpyDeviceToDevice, c.s));
+        return;
+    }
+    global_T<T, HERM>(c, Q, ldq, t, z, n, tmp1);
+    global_N<T>(c, Q, ldq, t, z, q, n, tmp1);
+    reorth_decide<<<1, 256, 0, c.s>>>(tmp1, (int)(t * W), nrmz, tmp2, flag);
+    c.check_launch();
+    global_T<T, HERM>(c, Q, ldq, t, q, n, tmp2, flag);
+    global_N<T>(c, Q, ldq, t, q, q, n, tmp2, flag);
     launch_addsub(c, (int)(t * W), tmp1, tmp2, 1.0, coef);
 }
 
@@ -814,7 +837,7 @@ SolveOut recycled_cg(Ctx& c, DevOp& op, const T* U, const T* K, long ncol, const
     // row-blocked copy of K for the inner-iteration kernels (contiguous 32-row tiles)
     const T* Kit = K;
     if (ncol > 0) {
-        ws.krb.ensure(sizeof(T) * npad * ncol);
+        if (sizeof(T) * npad * ncol > ws.krb.bytes) ws.krb.ensure(sizeof(T) * npad * (ncol + 16));  // slack
         repack_rb<T><<<c.grid_for(npad * ncol, 256, 8), 256, 0, c.s>>>(K, n, (int)ncol, n, ws.krb.template as<T>(),
                                                                       npad);
         c.check_launch();
@@ -1302,6 +1325,13 @@ template <class T> struct DevBasis : BasisBase {
     DevBuf tmpv, tmpv2, AW, Ur, Kr, idx, X, bvec;
     DevBuf Ktmp, Gd, Sinvd, Rd, Rd2, gwork;   // block refresh workspace
     DevBuf G00, Gt, Gsp;                     // bilinear Gram of the eigen block / of the current space
+    // process_system temporaries, persistent across systems (a multi-GB
+    // free + malloc per system costs a device sync and up to ~1 s)
+    DevBuf ps_idx, ps_val, ps_Wc, ps_Rall, ps_Coef, ps_Cpk, ps_rj, ps_wn, ps_y, ps_g, ps_im;
+    // grow-only with 25% slack
+    static void grow_to(DevBuf& b, size_t bytes) {
+        if (bytes > b.bytes) b.ensure(bytes + bytes / 4);
+    }
     long eig_ready_for = -1;                 // system tag whose eig-block factor sits in Ur/Kr
     long cmax_space = 0;
     long stats_block_refresh = 0, stats_seq_refresh = 0, stats_second_pass = 0;
@@ -1384,9 +1414,11 @@ template <class T> struct DevBasis : BasisBase {
         if (zp != z) CK(cudaMemcpyAsync(zp, z, sizeof(T) * n, cudaMemcpyDeviceToDevice, c.s));
         double* coef = c.sc(4);
         double* nrm = c.sc(7);
-        cgs2_global<T, true>(c, Kp(), n, j, zp, qp, n, coef, c.sc(5), c.sc(6));
-        launch_norms<T>(c, qp, n, nrm);
         launch_norms<T>(c, zp, n, nrm + 8);
+        c.rflag.ensure(sizeof(CGState));
+        cgs2_global_selective<T, true>(c, Kp(), n, j, zp, qp, n, coef, c.sc(5), c.sc(6), nrm + 8,
+                                       c.rflag.template as<CGState>());
+        launch_norms<T>(c, qp, n, nrm);
         std::vector<double> hc(2 + (size_t)j * W);
         CK(cudaMemcpyAsync(hc.data(), nrm, sizeof(double), cudaMemcpyDeviceToHost, c.s));
         CK(cudaMemcpyAsync(hc.data() + 1, nrm + 8, sizeof(double), cudaMemcpyDeviceToHost, c.s));
@@ -1503,9 +1535,13 @@ template <class T> struct DevBasis : BasisBase {
     // Same span and projector as the reference's full per-RHS QR.
     void factor_eig_block(DevOp& op, long cspace) {
         Ctx& c = *ctx;
-        Ur.ensure(sizeof(T) * n * std::max(1L, cspace));
-        Kr.ensure(sizeof(T) * n * std::max(1L, cspace));
-        AW.ensure(sizeof(T) * n * std::max(1L, std::max(ku, cspace)));
+        // the widest space grows by about one column per system: allocate with
+        // 16 columns of slack so these multi-GB buffers are not re-allocated
+        // (device sync + free + malloc) every system
+        const long cs = std::max(1L, cspace) + 16;
+        if ((size_t)(sizeof(T) * n * std::max(1L, cspace)) > Ur.bytes) Ur.ensure(sizeof(T) * n * cs);
+        if ((size_t)(sizeof(T) * n * std::max(1L, cspace)) > Kr.bytes) Kr.ensure(sizeof(T) * n * cs);
+        if ((size_t)(sizeof(T) * n * std::max(ku, cspace)) > AW.bytes) AW.ensure(sizeof(T) * n * std::max(ku, cs));
         tmpv2.ensure(sizeof(T) * n);
         if (ku == 0) return;
         T* Kb = Kr.template as<T>();
@@ -1692,16 +1728,18 @@ void process_system(DevBasis<T>& gb, DevOp& op, long nrhs, const long* bidx, con
     // is one tall GEMM per system; per RHS only the columns appended during the
     // system are projected out of R_all[:, j].
     const long r0 = gb.cols;
-    DevBuf idxd, vald, Wc, Rall, Coef, Cpk, rjbuf, wn, ybuf, gbuf, imbuf;
-    idxd.ensure(sizeof(long) * nrhs);
-    vald.ensure(sizeof(double) * nrhs);
+    using DB = DevBasis<T>;
+    DevBuf &idxd = gb.ps_idx, &vald = gb.ps_val, &Wc = gb.ps_Wc, &Rall = gb.ps_Rall, &Coef = gb.ps_Coef,
+           &Cpk = gb.ps_Cpk, &rjbuf = gb.ps_rj, &wn = gb.ps_wn, &ybuf = gb.ps_y, &gbuf = gb.ps_g, &imbuf = gb.ps_im;
+    DB::grow_to(idxd, sizeof(long) * nrhs);
+    DB::grow_to(vald, sizeof(double) * nrhs);
     CK(cudaMemcpyAsync(idxd.p, bidx, sizeof(long) * nrhs, cudaMemcpyHostToDevice, c.s));
     CK(cudaMemcpyAsync(vald.p, bval, sizeof(double) * nrhs, cudaMemcpyHostToDevice, c.s));
     const long npad = padded_rows(n);
-    Rall.ensure(sizeof(T) * npad * nrhs);
+    DB::grow_to(Rall, sizeof(T) * npad * nrhs);
     CK(cudaMemsetAsync(Rall.p, 0, sizeof(T) * npad * nrhs, c.s));
     if (r0 > 0) {
-        Wc.ensure(sizeof(T) * r0 * nrhs);
+        DB::grow_to(Wc, sizeof(T) * r0 * nrhs);
         row_gather_multi<T, true><<<c.grid_for(r0 * nrhs, 256, 4), 256, 0, c.s>>>(
             gb.Kp(), n, 0, (int)r0, idxd.template as<long>(), vald.template as<double>(), (int)nrhs, -1.0,
             Wc.template as<T>(), r0);
@@ -1716,21 +1754,21 @@ void process_system(DevBasis<T>& gb, DevOp& op, long nrhs, const long* bidx, con
     // deferred solution assembly X = G + W Coef (solve_projected, basis.cpp:110-112)
     const long capc = std::max(gb.capcols, r0 + nrhs + 1);
     if (Xdev) {
-        Coef.ensure(sizeof(T) * capc * nrhs);
+        DB::grow_to(Coef, sizeof(T) * capc * nrhs);
         CK(cudaMemsetAsync(Coef.p, 0, sizeof(T) * capc * nrhs, c.s));
     }
     for (DevBuf* b : {&rjbuf, &ybuf, &gbuf, &imbuf}) {  // zero-tailed (TMA passes)
-        b->ensure(sizeof(T) * npad);
+        DB::grow_to(*b, sizeof(T) * npad);
         CK(cudaMemsetAsync(b->p, 0, sizeof(T) * npad, c.s));
     }
-    wn.ensure(sizeof(T) * (nrhs + 8));
+    DB::grow_to(wn, sizeof(T) * (nrhs + 8));
     lap(2);
     for (long j = 0; j < nrhs; ++j) {
         const double bnorm = std::fabs(bval[j]);
         const long rcur = gb.cols;
         const T* rhs = Rall.template as<T>() + (size_t)j * npad;
         if (rcur > r0) {  // project out this system's appended columns
-            wn.ensure(sizeof(T) * (rcur - r0));
+            DB::grow_to(wn, sizeof(T) * (rcur - r0));
             row_gather_multi<T, true><<<c.grid_for(rcur - r0, 256, 1), 256, 0, c.s>>>(
                 gb.Kp(), n, (int)r0, (int)(rcur - r0), idxd.template as<long>() + j, vald.template as<double>() + j, 1,
                 1.0, wn.template as<T>(), rcur - r0);
@@ -1790,7 +1828,7 @@ void process_system(DevBasis<T>& gb, DevOp& op, long nrhs, const long* bidx, con
     }
     if (Xdev && gb.cols > 0) {
         const long rf = gb.cols;
-        Cpk.ensure(sizeof(T) * rf * nrhs);
+        DB::grow_to(Cpk, sizeof(T) * rf * nrhs);
         CK(cudaMemcpy2DAsync(Cpk.p, sizeof(T) * rf, Coef.p, sizeof(T) * capc, sizeof(T) * rf, nrhs,
                              cudaMemcpyDeviceToDevice, c.s));
         gemm<T, true>(c, gb.Wp(), n, rf, Cpk.template as<T>(), nrhs, Xdev, n, Xdev, n, n, false);
