@@ -829,10 +829,18 @@ SolveOut recycled_cg(Ctx& c, DevOp& op, const T* U, const T* K, long ncol, const
     CK(cudaMemcpyAsync(st, &c.st_host[0], sizeof(CGState), cudaMemcpyHostToDevice, c.s));
     CK(cudaStreamSynchronize(c.s));  // st_host slot reused below
 
-    // stencil+dots: (32 x 8) x-y tiles marching over kz planes, ~8 blocks per SM
+    // stencil+dots: (32 x 8) x-y tiles marching over kz planes; the smallest kz
+    // whose grid fits ONE resident wave (a partial second wave left the SMs 35%
+    // idle at 128^3: ncu, 1.73 waves)
     dim3 grid_st = stencil_grid(op.d, 1);
+    static int occ = 0;
+    if (!occ) {
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, cg_stencil_dots<T>, 256, 0));
+        occ = std::max(1, occ);
+    }
+    const long wave = (long)occ * c.sms;
     int kz = 1;
-    while ((long)grid_st.x * grid_st.y * ((op.d.N2 + kz - 1) / kz) > 8L * c.sms && kz < op.d.N2) kz *= 2;
+    while ((long)grid_st.x * grid_st.y * ((op.d.N2 + kz - 1) / kz) > wave && kz < op.d.N2) ++kz;
     grid_st.z = (unsigned)((op.d.N2 + kz - 1) / kz);
     // row-blocked copy of K for the inner-iteration kernels (contiguous 32-row tiles)
     const T* Kit = K;
