@@ -201,6 +201,23 @@ int rd_fom_jacobian(rd_op* op, int dtype, long n_src, const long* src_idx, const
                     const long* det_idx, const double* det_val, long n_par, const long* sup_ptr, const long* sup_idx,
                     const double* sup_val, double scale, double tol, void* J, int where);
 
+/* ------------------------------------------------------------- ROMB I/O --- */
+/* Basis file (src/io.cpp:77-110, README.md:96-99): "ROMB", u32 version,
+ * u64 n, u64 r, column-major data, r marker bytes (little-endian). dtype 0
+ * writes the reference's version 1 bit-exactly; dtype 1 (complex128) writes
+ * version 2, which adds one dtype byte after r. Errors are IoError (status 4):
+ * cannot open, not a basis file, unsupported version, truncated, marker count
+ * != column count (io.cpp:80-81). where = 1: V is device memory (ctx needed). */
+int rd_romb_write(const char* path, int dtype, long n, long r, const void* V, const uint8_t* markers, int where,
+                  rd_ctx* ctx);
+/* Header only: dtype, n, r of a version 1 or 2 file.                       */
+int rd_romb_info(const char* path, int* dtype, long* n, long* r);
+/* read_basis (io.cpp:93-110) into V (n x r, host or device) and markers (r).
+ * The dtype / shape must match the header (rd_romb_info).                  */
+int rd_romb_read(const char* path, int dtype, long n, long r, void* V, uint8_t* markers, int where, rd_ctx* ctx);
+/* write_basis of a device basis: V and its markers (harness.cpp:194).      */
+int rd_basis_save(rd_basis* b, const char* path);
+
 /* ------------------------------------------------------- bench hooks --- */
 /* Mean device ms per launch of the three inner-iteration projection kernels
  * (ms_out[0] c = K^T x, [1] fused x' = x - K c1 ; c2 = K^T x', [2] update)

@@ -13,6 +13,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <cstdint>
 #include <memory>
 #include <new>
 #include <stdexcept>
@@ -35,6 +36,9 @@ struct SolverError : std::runtime_error {
 };
 struct CudaError : std::runtime_error {
     explicit CudaError(const std::string& m) : std::runtime_error(m) {}
+};
+struct IoError : std::runtime_error {  // types.hpp:28-30, exit code 4
+    explicit IoError(const std::string& m) : std::runtime_error(m) {}
 };
 
 static thread_local std::string g_err;
@@ -2257,6 +2261,9 @@ template <class F> int guard(F&& f) {
     } catch (const rd::CudaError& e) {
         g_err = e.what();
         return 5;
+    } catch (const rd::IoError& e) {
+        g_err = e.what();
+        return 4;
     } catch (const std::exception& e) {
         g_err = e.what();
         return 1;
@@ -3245,6 +3252,133 @@ int rd_rom_jacobian(rd_rom* rm, rd_op* op, long n_src, const long* src_idx, cons
                        scale, static_cast<T*>(js.p));
             js.finish();
             if (where == 1) rm->ctx->c.sync();
+        });
+    });
+}
+
+// ------------------------------------------------------------------ ROMB ---
+// Basis file (src/io.cpp:77-110): "ROMB", u32 version, u64 n, u64 r, the
+// column-major data, r marker bytes, host little-endian. Version 1 is the
+// reference's f64 layout, written bit-exactly; version 2 (complex bases)
+// inserts one dtype byte (0 f64, 1 c128) after r.
+namespace {
+struct RombHeader {
+    uint32_t version = 0;
+    uint64_t n = 0, r = 0;
+    int dtype = 0;
+    long data_off = 0;
+};
+
+RombHeader romb_header(std::FILE* f, const std::string& path) {
+    char magic[4];
+    RombHeader h;
+    if (std::fread(magic, 1, 4, f) != 4 || std::memcmp(magic, "ROMB", 4) != 0)
+        throw rd::IoError(path + ": not a basis file");
+    if (std::fread(&h.version, 4, 1, f) != 1) throw rd::IoError(path + ": truncated basis file");
+    if (h.version != 1 && h.version != 2) throw rd::IoError(path + ": unsupported basis file version");
+    if (std::fread(&h.n, 8, 1, f) != 1 || std::fread(&h.r, 8, 1, f) != 1)
+        throw rd::IoError(path + ": truncated basis file");
+    if (h.version == 2) {
+        uint8_t dt = 0;
+        if (std::fread(&dt, 1, 1, f) != 1) throw rd::IoError(path + ": truncated basis file");
+        if (dt > 1) throw rd::IoError(path + ": unknown dtype in basis file");
+        h.dtype = dt;
+    }
+    h.data_off = std::ftell(f);
+    return h;
+}
+
+struct File {
+    std::FILE* f = nullptr;
+    File(const char* path, const char* mode) : f(std::fopen(path, mode)) {}
+    ~File() {
+        if (f) std::fclose(f);
+    }
+};
+constexpr size_t kRombChunk = size_t(1) << 28;  // device <-> host staging, 256 MB
+}  // namespace
+
+int rd_romb_write(const char* path, int dtype, long n, long r, const void* V, const uint8_t* markers, int where,
+                  rd_ctx* ctx) {
+    return guard([&] {
+        if (dtype != 0 && dtype != 1) throw rd::ConfigError("romb: dtype must be 0 (f64) or 1 (c128)");
+        if (!markers && r > 0) throw rd::IoError("basis file: marker count must equal column count");
+        if (n < 0 || r < 0) throw rd::ConfigError("romb: negative dimensions");
+        if (where == 1 && !ctx) throw rd::ConfigError("romb: a context is needed for device data");
+        File out(path, "wb");
+        if (!out.f) throw rd::IoError(std::string("cannot open ") + path + " for writing");
+        const uint32_t version = dtype == 0 ? 1u : 2u;
+        const uint64_t nn = (uint64_t)n, rr = (uint64_t)r;
+        bool ok = std::fwrite("ROMB", 1, 4, out.f) == 4 && std::fwrite(&version, 4, 1, out.f) == 1 &&
+                  std::fwrite(&nn, 8, 1, out.f) == 1 && std::fwrite(&rr, 8, 1, out.f) == 1;
+        if (version == 2) {
+            const uint8_t dt = (uint8_t)dtype;
+            ok = ok && std::fwrite(&dt, 1, 1, out.f) == 1;
+        }
+        const size_t bytes = esize(dtype) * (size_t)n * (size_t)r;
+        if (where == 1) {
+            std::vector<char> h(std::min(bytes, kRombChunk));
+            for (size_t o = 0; ok && o < bytes; o += kRombChunk) {
+                const size_t b = std::min(kRombChunk, bytes - o);
+                CK(cudaMemcpyAsync(h.data(), (const char*)V + o, b, cudaMemcpyDeviceToHost, ctx->c.s));
+                ctx->c.sync();
+                ok = std::fwrite(h.data(), 1, b, out.f) == b;
+            }
+        } else if (bytes) {
+            ok = ok && std::fwrite(V, 1, bytes, out.f) == bytes;
+        }
+        if (r) ok = ok && std::fwrite(markers, 1, (size_t)r, out.f) == (size_t)r;
+        if (!ok || std::fflush(out.f) != 0) throw rd::IoError(std::string("write failed: ") + path);
+    });
+}
+
+int rd_romb_info(const char* path, int* dtype, long* n, long* r) {
+    return guard([&] {
+        File in(path, "rb");
+        if (!in.f) throw rd::IoError(std::string("cannot open ") + path);
+        const RombHeader h = romb_header(in.f, path);
+        if (dtype) *dtype = h.dtype;
+        if (n) *n = (long)h.n;
+        if (r) *r = (long)h.r;
+    });
+}
+
+int rd_romb_read(const char* path, int dtype, long n, long r, void* V, uint8_t* markers, int where, rd_ctx* ctx) {
+    return guard([&] {
+        if (where == 1 && !ctx) throw rd::ConfigError("romb: a context is needed for device data");
+        File in(path, "rb");
+        if (!in.f) throw rd::IoError(std::string("cannot open ") + path);
+        const RombHeader h = romb_header(in.f, path);
+        if (h.dtype != dtype || (long)h.n != n || (long)h.r != r)
+            throw rd::ConfigError(std::string(path) + ": header does not match the requested dtype / shape");
+        const size_t bytes = esize(dtype) * (size_t)n * (size_t)r;
+        bool ok = true;
+        if (where == 1) {
+            std::vector<char> hb(std::min(bytes, kRombChunk));
+            for (size_t o = 0; ok && o < bytes; o += kRombChunk) {
+                const size_t b = std::min(kRombChunk, bytes - o);
+                ok = std::fread(hb.data(), 1, b, in.f) == b;
+                if (ok) {
+                    CK(cudaMemcpyAsync((char*)V + o, hb.data(), b, cudaMemcpyHostToDevice, ctx->c.s));
+                    ctx->c.sync();
+                }
+            }
+        } else if (bytes) {
+            ok = std::fread(V, 1, bytes, in.f) == bytes;
+        }
+        std::vector<uint8_t> mk((size_t)r);
+        if (ok && r) ok = std::fread(mk.data(), 1, (size_t)r, in.f) == (size_t)r;
+        if (!ok) throw rd::IoError(std::string(path) + ": truncated basis file");
+        if (markers) std::memcpy(markers, mk.data(), (size_t)r);
+    });
+}
+
+int rd_basis_save(rd_basis* b, const char* path) {
+    return guard([&] {
+        BASIS_DISPATCH(b, {
+            const int rc = rd_romb_write(path, b->h.dtype, B.n, B.cols, B.Vp(), B.markers.data(), 1, b->ctx);
+            if (rc == 4) throw rd::IoError(g_err);
+            if (rc) throw std::runtime_error(g_err);
         });
     });
 }

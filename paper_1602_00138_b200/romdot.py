@@ -36,6 +36,7 @@ EXPORTS = [
     "rd_bench_stencil", "rd_residual_norms", "rd_basis_compress", "rd_rom_create", "rd_rom_destroy",
     "rd_rom_order", "rd_rom_E", "rd_rom_reduced_system", "rd_rom_transfer", "rd_rom_jacobian",
     "rd_fom_transfer", "rd_fom_jacobian", "rd_per_rhs_create", "rd_per_rhs_solve_system",
+    "rd_romb_write", "rd_romb_info", "rd_romb_read", "rd_basis_save",
 ]
 
 
@@ -55,6 +56,10 @@ class SolverError(RomdotError):
 
 class CudaError(RomdotError):
     pass
+
+
+class IoError(RomdotError):
+    """IoError (types.hpp:28-30): basis / manifest files."""
 
 
 class _Report(C.Structure):
@@ -125,6 +130,10 @@ def load_library(path: Optional[str] = None):
     L.rd_bench_stencil.argtypes = [vp, C.c_int, C.c_long, C.c_int, vp]
     L.rd_basis_compress.argtypes = [vp, C.c_double, C.c_int, lp, vp, vp]
     L.rd_residual_norms.argtypes = [vp, C.c_int, C.c_long, vp, vp, vp, C.c_int, vp]
+    L.rd_romb_write.argtypes = [C.c_char_p, C.c_int, C.c_long, C.c_long, vp, vp, C.c_int, vp]
+    L.rd_romb_info.argtypes = [C.c_char_p, C.POINTER(C.c_int), lp, lp]
+    L.rd_romb_read.argtypes = [C.c_char_p, C.c_int, C.c_long, C.c_long, vp, vp, C.c_int, vp]
+    L.rd_basis_save.argtypes = [vp, C.c_char_p]
     L.rd_per_rhs_create.argtypes = [vp, C.c_int, C.c_long, C.c_long, C.c_long, vp, vp, C.c_int, C.POINTER(vp)]
     L.rd_per_rhs_solve_system.argtypes = [vp, vp, C.c_long, vp, vp, C.c_double, C.c_int, C.c_long, vp, C.c_int, vp,
                                           lp, lp]
@@ -144,10 +153,18 @@ def load_library(path: Optional[str] = None):
     return L
 
 
+def _release(fn: str, h) -> None:
+    """Destructor helper: free a handle unless the interpreter is shutting
+    down (module globals already cleared)."""
+    lib = globals().get("_LIB")
+    if lib is not None and h:
+        getattr(lib, fn)(h)
+
+
 def _check(rc):
     if rc != 0:
         msg = load_library().rd_last_error().decode()
-        raise {2: ConfigError, 3: SolverError, 5: CudaError}.get(rc, RomdotError)(rc, msg)
+        raise {2: ConfigError, 3: SolverError, 4: IoError, 5: CudaError}.get(rc, RomdotError)(rc, msg)
 
 
 def _p(a):
@@ -176,7 +193,7 @@ class Context:
 
     def __del__(self):
         if getattr(self, "h", None):
-            load_library().rd_ctx_destroy(self.h)
+            _release("rd_ctx_destroy", self.h)
             self.h = None
 
     def sync(self):
@@ -240,7 +257,7 @@ class SchurOperator:
 
     def __del__(self):
         if getattr(self, "h", None):
-            load_library().rd_op_destroy(self.h)
+            _release("rd_op_destroy", self.h)
             self.h = None
 
     def set_fields(self, fields: P.Fields, where: int = HOST, D_ptr=None, mu_ptr=None):
@@ -366,7 +383,7 @@ class GlobalBasis:
 
     def __del__(self):
         if getattr(self, "h", None):
-            load_library().rd_basis_destroy(self.h)
+            _release("rd_basis_destroy", self.h)
             self.h = None
 
     @property
@@ -431,6 +448,10 @@ class GlobalBasis:
         rdiag = np.zeros(max(m, 1))
         _check(load_library().rd_basis_compress(self.h, tol, int(normalize), C.byref(rank), _p(perm), _p(rdiag)))
         return rank.value, perm[:m], rdiag[:m]
+
+    def save(self, path: str):
+        """write_basis of V and its markers (io.cpp:77-91; harness.cpp:194)."""
+        _check(load_library().rd_basis_save(self.h, str(path).encode()))
 
     def refresh(self, op: SchurOperator):
         _check(load_library().rd_basis_refresh(self.h, op.h))
@@ -626,7 +647,7 @@ class ReducedModel:
 
     def __del__(self):
         if getattr(self, "h", None):
-            load_library().rd_rom_destroy(self.h)
+            _release("rd_rom_destroy", self.h)
             self.h = None
 
     def order(self) -> int:
@@ -666,3 +687,33 @@ class ReducedModel:
                                               _p(dv), len(supports), _p(ptr), _p(sidx), _p(sval), float(scale),
                                               _p(out), HOST))
         return out[:, : len(supports)]
+
+
+# ------------------------------------------------------------------ ROMB I/O --
+
+def romb_write(path, V: np.ndarray, markers) -> None:
+    """write_basis (io.cpp:77-91): version 1 for float64 (the reference's
+    layout, bit-exact), version 2 with a dtype byte for complex128."""
+    V = np.asfortranarray(V)
+    if V.dtype not in (np.float64, np.complex128):
+        raise ConfigError(2, "romb: float64 or complex128 only")
+    mk = np.ascontiguousarray(np.asarray(markers, dtype=np.uint8))
+    if mk.size != V.shape[1]:
+        raise IoError(4, "basis file: marker count must equal column count")
+    _check(load_library().rd_romb_write(str(path).encode(), _dt(V.dtype), V.shape[0], V.shape[1], _p(V),
+                                        _p(mk) if mk.size else None, HOST, None))
+
+
+def romb_info(path):
+    dt, n, r = C.c_int(), C.c_long(), C.c_long()
+    _check(load_library().rd_romb_info(str(path).encode(), C.byref(dt), C.byref(n), C.byref(r)))
+    return (np.complex128 if dt.value == 1 else np.float64), n.value, r.value
+
+
+def romb_read(path):
+    """read_basis (io.cpp:93-110) -> (V, markers)."""
+    dt, n, r = romb_info(path)
+    V = np.zeros((n, r), dtype=dt, order="F")
+    mk = np.zeros(max(r, 1), dtype=np.uint8)
+    _check(load_library().rd_romb_read(str(path).encode(), _dt(dt), n, r, _p(V), _p(mk), HOST, None))
+    return V, mk[:r].copy()

@@ -190,3 +190,56 @@ def test_fom_errors(rd):
     opr.set_fields(c.fields(1, 0.2))
     with pytest.raises(rd.ConfigError):
         rd.fom_transfer(opr, lay, 1e-10)
+
+
+# ---------------------------------------------------------------------------
+# Offline seed cache and basis files
+
+def test_offline_seed_cached_by_config_hash(rd, tmp_path):  # test_harness.cpp:202-217
+    from paper_1602_00138_b200 import offline as O
+    c = P.CONFIGS["T3"]
+    d = str(tmp_path / "offline")
+    assert not O.offline_seed(c, d)   # computed
+    assert O.offline_seed(c, d)       # cached
+    m = O.read_manifest(d + "/offline_manifest.txt")
+    m["hash"] = "0000000000000000"    # tampering forces a recompute
+    O.write_manifest(d + "/offline_manifest.txt", m)
+    assert not O.offline_seed(c, d)
+    U0, X0 = O.load_seed(d)
+    assert U0.shape == (c.grid.n, c.k) and X0.shape == (c.grid.n, c.layout().n_rhs)
+    mk = rd.romb_read(d + "/u0.romb")[1]
+    assert np.all(mk == O.COL_EIGENVECTOR)
+
+
+@pytest.mark.parametrize("name", ["T3", "T3c"])
+def test_build_from_cached_seed_and_basis_file(rd, tmp_path, name):
+    """init_basis_from on the cached seed (basis.cpp:114-134) reproduces the
+    freshly seeded build bit for bit; write_basis of the device basis reads
+    back bit-exactly with its markers."""
+    from paper_1602_00138_b200 import offline as O
+    c = P.CONFIGS[name]
+    g, lay = c.grid, c.layout()
+    d = str(tmp_path / "seed")
+    O.offline_seed(c, d)
+    U0, X0 = O.load_seed(d)
+
+    def build(U0, X0):
+        gb = rd.GlobalBasis(U0.astype(c.dtype), X0, c.cap)
+        logs = []
+        for s, (pt, w) in enumerate(c.systems(), start=1):
+            pr = rd.process_system(gb, rd.SchurOperator(g, c.fields(pt, w), c.dtype), lay, c.tol, s, want_X=False)
+            logs += [(r.init_relres, r.iterations, r.appended) for r in pr.log]
+        return gb, logs
+
+    op0r = rd.SchurOperator(g, c.fields(0), np.float64)
+    op0 = rd.SchurOperator(g, c.fields(0), c.dtype)
+    _, U0f = rd.smallest_eigenpairs(op0r, c.k, min(c.tol, 1e-8))
+    X0f, _ = rd.initial_solutions(op0, lay, c.tol)
+    gb1, log1 = build(U0, X0)
+    gb2, log2 = build(U0f, X0f)
+    assert log1 == log2
+    path = str(tmp_path / "basis.romb")
+    gb1.save(path)
+    V, mk = rd.romb_read(path)
+    assert V.tobytes(order="F") == gb1.V.tobytes(order="F")
+    assert np.array_equal(mk, gb1.markers[: gb1.cols])
