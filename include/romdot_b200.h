@@ -224,6 +224,8 @@ int rd_basis_save(rd_basis* b, const char* path);
  * on a seeded random n x c basis, and of the multi-column stencil apply.    */
 int rd_bench_projection(rd_ctx* ctx, int dtype, long n, long c, int iters, double* ms_out);
 int rd_bench_stencil(rd_op* op, int dtype, long ncols, int iters, double* ms_out);
+/* Mean device ms of the tall Gram X^T X (sym) or X^T Y on seeded n x a / n x b data. */
+int rd_bench_gram(rd_ctx* ctx, int dtype, long n, long a, long b, int sym, int iters, double* ms_out);
 
 #ifdef __cplusplus
 }

@@ -18,11 +18,14 @@
 namespace rd {
 
 template <class T> struct GT;  // tile geometry per scalar type
+// 16 x 16 threads, each an RA x RB register tile of strided rows / columns
+// (thread (tx, ty) owns columns tx + j*16 and rows ty + i*16: conflict-free
+// shared-memory reads); KC rows per staged chunk.
 template <> struct GT<double> {
-    static constexpr int TA = 64, TB = 64, KC = 32, RA = 4, RB = 4;
+    static constexpr int TA = 128, TB = 128, KC = 16, RA = 8, RB = 8;
 };
 template <> struct GT<cplx> {
-    static constexpr int TA = 32, TB = 32, KC = 32, RA = 2, RB = 2;
+    static constexpr int TA = 64, TB = 64, KC = 16, RA = 4, RB = 4;
 };
 
 // G_partial[slice][i][j] (column-major a x b per slice) = sum_{rows in slice} op(X[r,i]) Y[r,j]
@@ -69,13 +72,13 @@ __global__ void __launch_bounds__(256) gram_kernel(const T* __restrict__ X, long
         for (int q = 0; q < NB; ++q) Ys[lr][lc + q * (256 / KC)] = pbv[q];
         __syncthreads();
         if (rc + KC < r1) fetch(rc + KC);
-#pragma unroll 8
+#pragma unroll 4
         for (int k = 0; k < KC; ++k) {
             T xa[RA], yb[RB];
 #pragma unroll
-            for (int i = 0; i < RA; ++i) xa[i] = Xs[k][ty * RA + i];
+            for (int i = 0; i < RA; ++i) xa[i] = Xs[k][ty + i * (TA / RA)];
 #pragma unroll
-            for (int j = 0; j < RB; ++j) yb[j] = Ys[k][tx * RB + j];
+            for (int j = 0; j < RB; ++j) yb[j] = Ys[k][tx + j * (TB / RB)];
 #pragma unroll
             for (int i = 0; i < RA; ++i)
 #pragma unroll
@@ -88,7 +91,7 @@ __global__ void __launch_bounds__(256) gram_kernel(const T* __restrict__ X, long
     for (int i = 0; i < RA; ++i)
 #pragma unroll
         for (int j = 0; j < RB; ++j) {
-            const int gi = col_a0 + ty * RA + i, gj = col_b0 + tx * RB + j;
+            const int gi = col_a0 + ty + i * (TA / RA), gj = col_b0 + tx + j * (TB / RB);
             if (gi < a && gj < b) P[(size_t)gj * a + gi] = acc[i][j];
         }
 }

@@ -3035,6 +3035,47 @@ int rd_bench_projection(rd_ctx* ctx, int dtype, long n, long c, int iters, doubl
     });
 }
 
+// Gram G = X^T X (sym != 0, upper tiles + mirror) or X^T Y timing on seeded
+// random n x a / n x b blocks: mean device ms per call.
+int rd_bench_gram(rd_ctx* ctx, int dtype, long n, long a, long b, int sym, int iters, double* ms_out) {
+    return guard([&] {
+        Ctx& cx = ctx->c;
+        auto run = [&](auto tag) {
+            using T = decltype(tag);
+            DevBuf x, y, g, work;
+            x.ensure(sizeof(T) * n * a);
+            y.ensure(sizeof(T) * n * b);
+            g.ensure(sizeof(T) * a * b);
+            vec_randn<<<cx.grid_for(n * a * Sc<T>::W, 256, 8), 256, 0, cx.s>>>(x.template as<double>(),
+                                                                               n * a * Sc<T>::W, 11);
+            vec_randn<<<cx.grid_for(n * b * Sc<T>::W, 256, 8), 256, 0, cx.s>>>(y.template as<double>(),
+                                                                               n * b * Sc<T>::W, 12);
+            cx.check_launch();
+            const T* Y = sym ? x.template as<T>() : y.template as<T>();
+            const long bb = sym ? a : b;
+            cudaEvent_t e0, e1;
+            CK(cudaEventCreate(&e0));
+            CK(cudaEventCreate(&e1));
+            for (int w = 0; w < 2; ++w)
+                gram<T, false>(cx, x.template as<T>(), n, a, Y, n, bb, n, g.template as<T>(), sym != 0, work);
+            CK(cudaEventRecord(e0, cx.s));
+            for (int t = 0; t < iters; ++t)
+                gram<T, false>(cx, x.template as<T>(), n, a, Y, n, bb, n, g.template as<T>(), sym != 0, work);
+            CK(cudaEventRecord(e1, cx.s));
+            CK(cudaEventSynchronize(e1));
+            float ms = 0.f;
+            CK(cudaEventElapsedTime(&ms, e0, e1));
+            *ms_out = ms / iters;
+            cudaEventDestroy(e0);
+            cudaEventDestroy(e1);
+        };
+        if (dtype == 0)
+            run(double{});
+        else
+            run(cplx{});
+    });
+}
+
 // Multi-column stencil apply timing on the operator's current fields.
 int rd_bench_stencil(rd_op* o, int dtype, long ncols, int iters, double* ms_out) {
     return guard([&] {

@@ -36,7 +36,7 @@ EXPORTS = [
     "rd_bench_stencil", "rd_residual_norms", "rd_basis_compress", "rd_rom_create", "rd_rom_destroy",
     "rd_rom_order", "rd_rom_E", "rd_rom_reduced_system", "rd_rom_transfer", "rd_rom_jacobian",
     "rd_fom_transfer", "rd_fom_jacobian", "rd_per_rhs_create", "rd_per_rhs_solve_system",
-    "rd_romb_write", "rd_romb_info", "rd_romb_read", "rd_basis_save",
+    "rd_romb_write", "rd_romb_info", "rd_romb_read", "rd_basis_save", "rd_bench_gram",
 ]
 
 
@@ -128,6 +128,7 @@ def load_library(path: Optional[str] = None):
     L.rd_rrqr.argtypes = [vp, C.c_int, C.c_long, C.c_long, vp, C.c_double, C.c_int, lp, vp, vp, vp, C.c_int]
     L.rd_bench_projection.argtypes = [vp, C.c_int, C.c_long, C.c_long, C.c_int, vp]
     L.rd_bench_stencil.argtypes = [vp, C.c_int, C.c_long, C.c_int, vp]
+    L.rd_bench_gram.argtypes = [vp, C.c_int, C.c_long, C.c_long, C.c_long, C.c_int, C.c_int, vp]
     L.rd_basis_compress.argtypes = [vp, C.c_double, C.c_int, lp, vp, vp]
     L.rd_residual_norms.argtypes = [vp, C.c_int, C.c_long, vp, vp, vp, C.c_int, vp]
     L.rd_romb_write.argtypes = [C.c_char_p, C.c_int, C.c_long, C.c_long, vp, vp, C.c_int, vp]
@@ -717,3 +718,11 @@ def romb_read(path):
     mk = np.zeros(max(r, 1), dtype=np.uint8)
     _check(load_library().rd_romb_read(str(path).encode(), _dt(dt), n, r, _p(V), _p(mk), HOST, None))
     return V, mk[:r].copy()
+
+
+def bench_gram(n: int, a: int, b: int, cplx: bool, sym: bool, iters: int = 5, ctx: Optional[Context] = None) -> float:
+    """Mean device ms of the tall Gram on seeded data (bench hook)."""
+    ctx = ctx or default_context()
+    ms = np.zeros(1)
+    _check(load_library().rd_bench_gram(ctx.h, 1 if cplx else 0, n, a, b, int(sym), iters, _p(ms)))
+    return float(ms[0])

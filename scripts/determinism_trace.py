@@ -1,6 +1,6 @@
 """Run interleaved T3c/T2c builds with ROMDOT_VERBOSE=4 (async device hash log);
 markers go to stderr so the log can be split per build. Compare with
-scripts/diag_race4_cmp.py <log>."""
+scripts/determinism_trace_cmp.py <log>."""
 import sys
 sys.path.insert(0,'.'); sys.path.insert(0,'oracle')
 import oracle as orc

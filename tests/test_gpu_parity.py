@@ -370,3 +370,18 @@ def test_global_basis_beats_per_rhs_recycling(rd):
         base += pr.solve_system(rd.SchurOperator(g, f, c.dtype), lay, c.tol, s, want_X=False).inner_iterations
     assert ours / base <= 0.6, (ours, base)
     assert abs(ours - 4941) <= 2 * 128 and abs(base - 9634) <= 2 * 128, (ours, base)
+
+
+def test_full_config_parity_C1(rd):
+    """BASELINE configs[0] (C1, 2D 129^2, 32 RHS, 4 systems) at full size
+    against the CPU checker with north_star's tolerances: lockstep BuildLog
+    (+/-2 iterations, same append decisions), residual <= tol per solve, same
+    RRQR rank, principal-angle sine <= 1e-6, ROM transfer / Jacobian <= 1e-8."""
+    import importlib.util
+    import os
+    spec = importlib.util.spec_from_file_location(
+        "parity_full", os.path.join(os.path.dirname(__file__), "..", "scripts", "parity_full.py"))
+    mod = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(mod)
+    out = mod.run("C1")
+    assert out["pass"], out
