@@ -162,7 +162,9 @@ __device__ inline void grid_finish(const GridRed& g, int nv, double* out /* shar
 #pragma unroll
                 for (int q = 0; q < 8; ++q) a[q] += __ldcg(pp + (size_t)(b + q * tpc) * nv);
             }
-            for (int q = 0; b < nb; b += tpc, ++q) a[q & 7] += __ldcg(pp + (size_t)b * nv);
+#pragma unroll
+            for (int q = 0; q < 7; ++q)  // < 8 remaining slots, compile-time indices (no local memory)
+                if (b + q * tpc < nb) a[q] += __ldcg(pp + (size_t)(b + q * tpc) * nv);
             s = ((a[0] + a[1]) + (a[2] + a[3])) + ((a[4] + a[5]) + (a[6] + a[7]));
         }
         // combine tpc lanes (tpc divides 32 and groups are lane-aligned)

@@ -504,7 +504,9 @@ __global__ void __launch_bounds__(256) gram_thin(const T* __restrict__ X, long l
 #pragma unroll
             for (int q = 0; q < 8; ++q) acc8[q] += __ldcg(pp + (size_t)(bx + q) * nv);
         }
-        for (int q = 0; bx < gridDim.x; ++bx, ++q) acc8[q] += __ldcg(pp + (size_t)bx * nv);
+#pragma unroll
+        for (int q = 0; q < 7; ++q)
+            if (bx + q < gridDim.x) acc8[q] += __ldcg(pp + (size_t)(bx + q) * nv);
         const double sum =
             ((acc8[0] + acc8[1]) + (acc8[2] + acc8[3])) + ((acc8[4] + acc8[5]) + (acc8[6] + acc8[7]));
         const int colr = vv / (B * W), v = (vv / W) % B, w = vv % W;
