@@ -183,71 +183,6 @@ __device__ __forceinline__ void zmarch(const OpDev& op, const T* __restrict__ x,
     }
 }
 
-// Software-pipelined z-march (same arithmetic and face order as zmarch). The
-// loads that miss to HBM -- x one plane ahead and the node's own diag / +x /
-// +y / +z coefficients -- are issued one plane early; the in-plane neighbours
-// and the -x / -y faces sit in lines this or a neighbouring warp of the block
-// loaded a plane earlier (L1). ncu on the unpipelined march: 70% of stalls
-// were long-scoreboard waits on the first FMAs of each plane.
-template <class T, class F>
-__device__ __forceinline__ void zmarch_pf(const OpDev& op, const T* __restrict__ x, int i, int j, int k0, int k1,
-                                          F&& f) {
-    const long n = op.n;
-    const long s1 = op.N0, s2 = (long)op.N0 * op.N1;
-    const double* __restrict__ Fd = op.F;
-    long p = i + s1 * (j + (long)op.N1 * k0);
-    const bool three = op.d == 3;
-    T xm = (three && k0 > 0) ? x[p - s2] : Sc<T>::zero();
-    double fzm = (three && k0 > 0) ? __ldg(Fd + 3 * n + p - s2) : 0.0;
-    T xc = x[p];
-    const bool hx_m = i > 0, hx_p = i < op.N0 - 1, hy_m = j > 0, hy_p = j < op.N1 - 1;
-    // prefetched set of the current plane
-    bool hz = three && k0 < op.N2 - 1;
-    T xp = hz ? x[p + s2] : Sc<T>::zero();
-    double fzp = hz ? __ldg(Fd + 3 * n + p) : 0.0;
-    double dg = __ldg(Fd + p);
-    double fxp = hx_p ? __ldg(Fd + n + p) : 0.0;
-    double fyp = hy_p ? __ldg(Fd + 2 * n + p) : 0.0;
-    for (int k = k0; k < k1; ++k) {
-        // next plane's HBM loads first
-        const long q = p + s2;
-        const bool more = k + 1 < k1;
-        const bool hz2 = three && k + 1 < op.N2 - 1;
-        const T xp_n = (more && hz2) ? x[q + s2] : Sc<T>::zero();
-        const double fzp_n = (more && hz2) ? __ldg(Fd + 3 * n + q) : 0.0;
-        const double dg_n = more ? __ldg(Fd + q) : 0.0;
-        const double fxp_n = (more && hx_p) ? __ldg(Fd + n + q) : 0.0;
-        const double fyp_n = (more && hy_p) ? __ldg(Fd + 2 * n + q) : 0.0;
-        // current plane: in-plane neighbours and -x / -y faces (L1)
-        const double fxm = hx_m ? __ldg(Fd + n + p - 1) : 0.0;
-        const double fym = hy_m ? __ldg(Fd + 2 * n + p - s1) : 0.0;
-        const T xim = hx_m ? x[p - 1] : Sc<T>::zero();
-        const T xip = hx_p ? x[p + 1] : Sc<T>::zero();
-        const T xjm = hy_m ? x[p - s1] : Sc<T>::zero();
-        const T xjp = hy_p ? x[p + s1] : Sc<T>::zero();
-        T acc = Sc<T>::zero();
-        acc = axpy_real(fxm, xim, acc);
-        acc = axpy_real(fxp, xip, acc);
-        acc = axpy_real(fym, xjm, acc);
-        acc = axpy_real(fyp, xjp, acc);
-        if (three) {
-            acc = axpy_real(fzm, xm, acc);
-            acc = axpy_real(fzp, xp, acc);
-        }
-        const T yv = Sc<T>::sub(diag_apply<T>(dg, op.shift, xc), acc);
-        f(p, xc, yv);
-        xm = xc;
-        xc = xp;
-        fzm = fzp;
-        xp = xp_n;
-        fzp = fzp_n;
-        dg = dg_n;
-        fxp = fxp_n;
-        fyp = fyp_n;
-        p = q;
-    }
-}
-
 // y[:, c] = A x[:, xcol ? xcol[c] : c]: blockIdx.z = (column, k chunk of kz planes)
 template <class T>
 __global__ void __launch_bounds__(256) stencil_kernel(OpDev op, const T* __restrict__ x, long ldx,
@@ -348,7 +283,7 @@ __device__ __noinline__ void cg_recurrence(CGState* st, const double* s_tot, dou
 // K2: w = A r ; partials of {r^T r (W), r^T w (W), r^H r (1)} ; last block runs
 // the scalar recurrence. One grid reduction per iteration.
 template <class T>
-__global__ void __launch_bounds__(256, 3) cg_stencil_dots(OpDev op, const T* __restrict__ r, T* __restrict__ w,
+__global__ void __launch_bounds__(256) cg_stencil_dots(OpDev op, const T* __restrict__ r, T* __restrict__ w,
                                                        CGState* st, double* hist, GridRed red, int kz) {
     if (st->done) return;
     constexpr int W = Sc<T>::W;
@@ -359,7 +294,7 @@ __global__ void __launch_bounds__(256, 3) cg_stencil_dots(OpDev op, const T* __r
     const int j = blockIdx.y * 8 + (threadIdx.x >> 5);
     const int k0 = blockIdx.z * kz, k1 = min(op.N2, k0 + kz);
     if (i < op.N0 && j < op.N1)
-        zmarch_pf<T>(op, r, i, j, k0, k1, [&](long p, const T& rp, const T& wp) {
+        zmarch<T>(op, r, i, j, k0, k1, [&](long p, const T& rp, const T& wp) {
             w[p] = wp;
             g = Sc<T>::fma(rp, rp, g);
             dl = Sc<T>::fma(rp, wp, dl);
@@ -398,7 +333,7 @@ __global__ void __launch_bounds__(256, 3) cg_stencil_dots(OpDev op, const T* __r
 // and the column's last block runs its scalar step. Converged columns return.
 // The assembled coefficients are re-read per column from L2 (64 MB at 128^3).
 template <class T>
-__global__ void __launch_bounds__(256, 3) bcg_stencil_dots(OpDev op, const T* __restrict__ R, T* __restrict__ Wv, long ld,
+__global__ void __launch_bounds__(256) bcg_stencil_dots(OpDev op, const T* __restrict__ R, T* __restrict__ Wv, long ld,
                                                         CGState* st, double* partials, unsigned* counters, int kz) {
     constexpr int W = Sc<T>::W;
     constexpr int NV = 2 * W + 1;
@@ -415,7 +350,7 @@ __global__ void __launch_bounds__(256, 3) bcg_stencil_dots(OpDev op, const T* __
     const int j = blockIdx.y * 8 + (threadIdx.x >> 5);
     const int k0 = kc * kz, k1 = min(op.N2, k0 + kz);
     if (i < op.N0 && j < op.N1)
-        zmarch_pf<T>(op, r, i, j, k0, k1, [&](long p, const T& rp, const T& wp) {
+        zmarch<T>(op, r, i, j, k0, k1, [&](long p, const T& rp, const T& wp) {
             w[p] = wp;
             g = Sc<T>::fma(rp, rp, g);
             dl = Sc<T>::fma(rp, wp, dl);
@@ -478,20 +413,17 @@ __global__ void __launch_bounds__(256) bcg_update(T* __restrict__ R, T* __restri
     }
 }
 
-// Selective reorthogonalisation (Kahan-Parlett "twice is enough"): after the
-// first CGS pass, ||q1||^2 = ||z||^2 - ||c1||^2; when that keeps at least half
-// of ||z||^2 the first pass is already accurate to O(eps) and the second is
+// Selective reorthogonalisation (Kahan-Parlett "twice is enough"): when the
+// first CGS pass keeps at least half of ||z||^2 (||q1||^2 >= ||z||^2 / 2,
+// both measured) it is already accurate to O(eps) and the second pass is
 // skipped: flag->done = 1 (the second-pass kernels then exit at entry) and
-// c2 = 0. Otherwise flag->done = 0 and the second pass runs.
-__global__ void reorth_decide(const double* __restrict__ c1, int nv, const double* __restrict__ nrmz, double* c2,
+// c2 = 0. Otherwise flag->done = 0 and the second pass runs. The measured
+// ||q1|| keeps the test valid for bilinear (complex K^T K = I) spaces too.
+__global__ void reorth_decide(const double* __restrict__ nrmq, const double* __restrict__ nrmz, int nv, double* c2,
                               CGState* flag) {
-    __shared__ double s_red[32];
     __shared__ int s_skip;
-    double a = 0.0;
-    for (int i = threadIdx.x; i < nv; i += blockDim.x) a += c1[i] * c1[i];
-    a = block_sum(a, s_red);
     if (threadIdx.x == 0) {
-        s_skip = (a <= 0.5 * nrmz[0]) ? 1 : 0;
+        s_skip = (nrmq[0] >= 0.5 * nrmz[0]) ? 1 : 0;
         flag->done = s_skip;
     }
     __syncthreads();

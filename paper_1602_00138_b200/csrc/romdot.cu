@@ -240,7 +240,7 @@ struct Ctx {
         partials.ensure(sizeof(double) * 1024 * 1024);
         counter.ensure(sizeof(unsigned) * 16);
         CK(cudaMemset(counter.p, 0, counter.bytes));
-        scal.ensure(sizeof(double) * 64 * 1024);
+        scal.ensure(sizeof(double) * 16 * 8192);  // 16 scratch slots (sc(k))
         cgst.ensure(sizeof(CGState));
         hist.ensure(sizeof(double) * hist_cap);
         CK(cudaMallocHost(&st_host, 2 * sizeof(CGState)));
@@ -736,7 +736,9 @@ void cgs2_global_selective(Ctx& c, const T* Q, long ldq, long t, const T* z, T* 
     }
     global_T<T, HERM>(c, Q, ldq, t, z, n, tmp1);
     global_N<T>(c, Q, ldq, t, z, q, n, tmp1);
-    reorth_decide<<<1, 256, 0, c.s>>>(tmp1, (int)(t * W), nrmz, tmp2, flag);
+    double* nrmq = c.sc(8);
+    launch_norms<T>(c, q, n, nrmq);
+    reorth_decide<<<1, 256, 0, c.s>>>(nrmq, nrmz, (int)(t * W), tmp2, flag);
     c.check_launch();
     global_T<T, HERM>(c, Q, ldq, t, q, n, tmp2, flag);
     global_N<T>(c, Q, ldq, t, q, q, n, tmp2, flag);
@@ -805,10 +807,16 @@ SolveOut recycled_cg(Ctx& c, DevOp& op, const T* U, const T* K, long ncol, const
     CK(cudaMemsetAsync(w, 0, sizeof(T) * npad, c.s));
     // r0 = P rhs (CGS2), e = K^T rhs
     if (ncol > 0) {
-        if (padded_io)
-            cgs2_global<T, false>(c, K, n, ncol, rhs, r, n, e, c1, c2);
-        else
+        if (padded_io) {
+            // selective second pass (Kahan-Parlett, device-side): 2 streams over K
+            // instead of 4 when the first pass keeps at least half of ||rhs||^2
+            launch_norms<T>(c, rhs, n, c.sc(3) + 8);
+            c.rflag.ensure(sizeof(CGState));
+            cgs2_global_selective<T, false>(c, K, n, ncol, rhs, r, n, e, c1, c2, c.sc(3) + 8,
+                                            c.rflag.template as<CGState>());
+        } else {
             cgs2<T, false>(c, K, n, ncol, rhs, r, n, e, c1, c2);
+        }
     } else {
         CK(cudaMemcpyAsync(r, rhs, sizeof(T) * n, cudaMemcpyDeviceToDevice, c.s));
     }

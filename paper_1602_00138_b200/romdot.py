@@ -157,9 +157,12 @@ def load_library(path: Optional[str] = None):
 def _release(fn: str, h) -> None:
     """Destructor helper: free a handle unless the interpreter is shutting
     down (module globals already cleared)."""
-    lib = globals().get("_LIB")
-    if lib is not None and h:
-        getattr(lib, fn)(h)
+    try:
+        lib = globals().get("_LIB")
+        if lib is not None and h:
+            getattr(lib, fn)(h)
+    except Exception:  # interpreter teardown
+        pass
 
 
 def _check(rc):
@@ -194,7 +197,10 @@ class Context:
 
     def __del__(self):
         if getattr(self, "h", None):
-            _release("rd_ctx_destroy", self.h)
+            try:
+                _release("rd_ctx_destroy", self.h)
+            except Exception:
+                pass
             self.h = None
 
     def sync(self):
@@ -258,7 +264,10 @@ class SchurOperator:
 
     def __del__(self):
         if getattr(self, "h", None):
-            _release("rd_op_destroy", self.h)
+            try:
+                _release("rd_op_destroy", self.h)
+            except Exception:
+                pass
             self.h = None
 
     def set_fields(self, fields: P.Fields, where: int = HOST, D_ptr=None, mu_ptr=None):
@@ -384,7 +393,10 @@ class GlobalBasis:
 
     def __del__(self):
         if getattr(self, "h", None):
-            _release("rd_basis_destroy", self.h)
+            try:
+                _release("rd_basis_destroy", self.h)
+            except Exception:
+                pass
             self.h = None
 
     @property
@@ -648,7 +660,10 @@ class ReducedModel:
 
     def __del__(self):
         if getattr(self, "h", None):
-            _release("rd_rom_destroy", self.h)
+            try:
+                _release("rd_rom_destroy", self.h)
+            except Exception:
+                pass
             self.h = None
 
     def order(self) -> int:
