@@ -18,82 +18,149 @@
 namespace rd {
 
 template <class T> struct GT;  // tile geometry per scalar type
-// 16 x 16 threads, each an RA x RB register tile of strided rows / columns
-// (thread (tx, ty) owns columns tx + j*16 and rows ty + i*16: conflict-free
-// shared-memory reads); KC rows per staged chunk.
+// Gram block tiles (DMMA kernel below); KC is the host's slice granularity.
 template <> struct GT<double> {
-    static constexpr int TA = 128, TB = 128, KC = 16, RA = 8, RB = 8;
+    static constexpr int TA = 128, TB = 128, KC = 16, WARPS_M = 4, WARPS_N = 4, THREADS = 512;
 };
 template <> struct GT<cplx> {
-    static constexpr int TA = 64, TB = 64, KC = 16, RA = 4, RB = 4;
+    static constexpr int TA = 64, TB = 64, KC = 16, WARPS_M = 2, WARPS_N = 4, THREADS = 256;
 };
 
 // G_partial[slice][i][j] (column-major a x b per slice) = sum_{rows in slice} op(X[r,i]) Y[r,j]
+//
+// FP64 tensor cores: DMMA m8n8k4 (mma.sync.aligned.m8n8k4.row.col.f64). The
+// Gram is a GEMM with M = a, N = b and the long reduction K = rows: A = X^T
+// (row-major in k = row, i.e. X's column-major storage), B = Y. Block tile
+// TA x TB (real 128 x 128 with 16 warps as 4 x 4, complex 64 x 64 with 8
+// warps as 2 x 4): per k-step of 4 rows a warp issues 16 (real) / 32
+// (complex) DMMA from 8 / 12 fragment loads. Complex
+// products are four real DMMA on separately staged real / imaginary planes.
+// Chunks of 16 rows are staged in shared memory as [column][row] with rows
+// padded to 20 (each half-warp's 16 fragment loads hit 32 distinct banks) and
+// register double buffered from global memory.
+__device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b) {
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+                 : "+d"(d0), "+d"(d1)
+                 : "d"(a), "d"(b));
+}
+
+constexpr int GM_KC = 16, GM_LD = 20;
+
 template <class T, bool HERM>
-__global__ void __launch_bounds__(256) gram_kernel(const T* __restrict__ X, long ldx, int a, const T* __restrict__ Y,
+__global__ void __launch_bounds__(GT<T>::THREADS) gram_kernel(const T* __restrict__ X, long ldx, int a, const T* __restrict__ Y,
                                                    long ldy, int b, long n, long rows_per_slice, T* __restrict__ part,
                                                    bool sym_upper) {
-    constexpr int TA = GT<T>::TA, TB = GT<T>::TB, KC = GT<T>::KC, RA = GT<T>::RA, RB = GT<T>::RB;
+    constexpr bool CPLX = Sc<T>::W == 2;
+    constexpr int TA = GT<T>::TA, TB = GT<T>::TB, KC = GM_KC, LD = GM_LD;
+    constexpr int PL = CPLX ? 2 : 1;                 // planes (re, im)
+    constexpr int NTH = GT<T>::THREADS, WNN = GT<T>::WARPS_N;
+    constexpr int WM = TA / GT<T>::WARPS_M, WN = TB / WNN;  // warp tile
+    constexpr int MT = WM / 8, NT = WN / 8;           // mma tiles per warp
+    static_assert(KC == 16, "chunk of 16 rows");
     const int ta = blockIdx.x, tb = blockIdx.y, sl = blockIdx.z;
     if (sym_upper && ta > tb) return;
-    __shared__ T Xs[KC][TA + 1];
-    __shared__ T Ys[KC][TB + 1];
-    const int tx = threadIdx.x % (TB / RB), ty = threadIdx.x / (TB / RB);  // 16 x 16 threads
-    T acc[RA][RB];
+    __shared__ __align__(16) double Xs[PL][TA][LD];
+    __shared__ __align__(16) double Ys[PL][TB][LD];
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    const int wm = wid / WNN, wn = wid % WNN;
+    double acc[PL][MT][NT][2];
 #pragma unroll
-    for (int i = 0; i < RA; ++i)
+    for (int p = 0; p < PL; ++p)
 #pragma unroll
-        for (int j = 0; j < RB; ++j) acc[i][j] = Sc<T>::zero();
+        for (int i = 0; i < MT; ++i)
+#pragma unroll
+            for (int j = 0; j < NT; ++j) acc[p][i][j][0] = acc[p][i][j][1] = 0.0;
     const long r0 = (long)sl * rows_per_slice;
     const long r1 = min(n, r0 + rows_per_slice);
     const int col_a0 = ta * TA, col_b0 = tb * TB;
-    // register double buffering: chunk c+1 is loaded while chunk c is consumed
-    const int lr = threadIdx.x % KC, lc = threadIdx.x / KC;  // 32 rows x 8 column groups
-    constexpr int NA = TA / (256 / KC), NB = TB / (256 / KC);
+    // global staging: 16 rows x (TA + TB) columns; thread -> (row = tid % 16, column group tid / 16)
+    constexpr int CG = NTH / 16;              // column groups
+    const int lr = tid & 15, lc = tid >> 4;
+    constexpr int NA = TA / CG, NB = TB / CG;
     T pa[NA], pbv[NB];
     auto fetch = [&](long rc) {
         const long row = rc + lr;
 #pragma unroll
         for (int q = 0; q < NA; ++q) {
-            const int col = col_a0 + lc + q * (256 / KC);
+            const int col = col_a0 + lc + q * CG;
             pa[q] = (row < r1 && col < a) ? X[(size_t)col * ldx + row] : Sc<T>::zero();
         }
 #pragma unroll
         for (int q = 0; q < NB; ++q) {
-            const int col = col_b0 + lc + q * (256 / KC);
+            const int col = col_b0 + lc + q * CG;
             pbv[q] = (row < r1 && col < b) ? Y[(size_t)col * ldy + row] : Sc<T>::zero();
         }
     };
+    auto stage = [&]() {
+#pragma unroll
+        for (int q = 0; q < NA; ++q) {
+            if constexpr (CPLX) {
+                Xs[0][lc + q * CG][lr] = ((cplx&)pa[q]).x;
+                Xs[1][lc + q * CG][lr] = ((cplx&)pa[q]).y;
+            } else {
+                Xs[0][lc + q * CG][lr] = (double&)pa[q];
+            }
+        }
+#pragma unroll
+        for (int q = 0; q < NB; ++q) {
+            if constexpr (CPLX) {
+                Ys[0][lc + q * CG][lr] = ((cplx&)pbv[q]).x;
+                Ys[1][lc + q * CG][lr] = ((cplx&)pbv[q]).y;
+            } else {
+                Ys[0][lc + q * CG][lr] = (double&)pbv[q];
+            }
+        }
+    };
+    const int fr = lane >> 2, fk = lane & 3;   // fragment row (m or n) and k within the step
     if (r0 < r1) fetch(r0);
     for (long rc = r0; rc < r1; rc += KC) {
-#pragma unroll
-        for (int q = 0; q < NA; ++q) Xs[lr][lc + q * (256 / KC)] = pa[q];
-#pragma unroll
-        for (int q = 0; q < NB; ++q) Ys[lr][lc + q * (256 / KC)] = pbv[q];
+        stage();
         __syncthreads();
         if (rc + KC < r1) fetch(rc + KC);
-#pragma unroll 4
-        for (int k = 0; k < KC; ++k) {
-            T xa[RA], yb[RB];
 #pragma unroll
-            for (int i = 0; i < RA; ++i) xa[i] = Xs[k][ty + i * (TA / RA)];
+        for (int kk = 0; kk < KC; kk += 4) {
+            double af[PL][MT], bf[PL][NT];
 #pragma unroll
-            for (int j = 0; j < RB; ++j) yb[j] = Ys[k][tx + j * (TB / RB)];
+            for (int p = 0; p < PL; ++p) {
 #pragma unroll
-            for (int i = 0; i < RA; ++i)
+                for (int i = 0; i < MT; ++i) af[p][i] = Xs[p][wm * WM + i * 8 + fr][kk + fk];
 #pragma unroll
-                for (int j = 0; j < RB; ++j) acc[i][j] = opfma<T, HERM>(xa[i], yb[j], acc[i][j]);
+                for (int j = 0; j < NT; ++j) bf[p][j] = Ys[p][wn * WN + j * 8 + fr][kk + fk];
+            }
+#pragma unroll
+            for (int i = 0; i < MT; ++i)
+#pragma unroll
+                for (int j = 0; j < NT; ++j) {
+                    if constexpr (CPLX) {
+                        // T:  re += ar br - ai bi ; im += ar bi + ai br
+                        // H:  re += ar br + ai bi ; im += ar bi - ai br
+                        dmma(acc[0][i][j][0], acc[0][i][j][1], af[0][i], bf[0][j]);
+                        dmma(acc[0][i][j][0], acc[0][i][j][1], HERM ? af[1][i] : -af[1][i], bf[1][j]);
+                        dmma(acc[1][i][j][0], acc[1][i][j][1], af[0][i], bf[1][j]);
+                        dmma(acc[1][i][j][0], acc[1][i][j][1], HERM ? -af[1][i] : af[1][i], bf[0][j]);
+                    } else {
+                        dmma(acc[0][i][j][0], acc[0][i][j][1], af[0][i], bf[0][j]);
+                    }
+                }
         }
         __syncthreads();
     }
     T* P = part + (size_t)sl * a * b;
 #pragma unroll
-    for (int i = 0; i < RA; ++i)
+    for (int i = 0; i < MT; ++i)
 #pragma unroll
-        for (int j = 0; j < RB; ++j) {
-            const int gi = col_a0 + ty + i * (TA / RA), gj = col_b0 + tx + j * (TB / RB);
-            if (gi < a && gj < b) P[(size_t)gj * a + gi] = acc[i][j];
-        }
+        for (int j = 0; j < NT; ++j)
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+                const int gi = col_a0 + wm * WM + i * 8 + fr;
+                const int gj = col_b0 + wn * WN + j * 8 + 2 * fk + e;
+                if (gi < a && gj < b) {
+                    if constexpr (CPLX)
+                        P[(size_t)gj * a + gi] = make_double2(acc[0][i][j][e], acc[1][i][j][e]);
+                    else
+                        P[(size_t)gj * a + gi] = acc[0][i][j][e];
+                }
+            }
 }
 
 // G = sum over slices in order; if sym, mirror the upper triangle (op(G)^T = G for

@@ -545,7 +545,8 @@ void gram(Ctx& c, const T* X, long ldx, long a, const T* Y, long ldy, long b, lo
     slices = (n + rps - 1) / rps;
     work.ensure(sizeof(T) * slices * a * b);
     dim3 grid((unsigned)ta, (unsigned)tb, (unsigned)slices);
-    gram_kernel<T, HERM><<<grid, 256, 0, c.s>>>(X, ldx, (int)a, Y, ldy, (int)b, n, rps, work.template as<T>(), sym);
+    gram_kernel<T, HERM><<<grid, GT<T>::THREADS, 0, c.s>>>(X, ldx, (int)a, Y, ldy, (int)b, n, rps,
+                                                            work.template as<T>(), sym);
     c.check_launch();
     gram_reduce<T, HERM><<<c.grid_for(a * b, 256, 4), 256, 0, c.s>>>(work.template as<T>(), (int)slices, (int)a,
                                                                       (int)b, G, sym);
