@@ -355,6 +355,19 @@ def main():
     value = solves_all / (t_max / 1e3) if t_max > 0 else 0.0
 
     # ---- roofline from the live samples ------------------------------------
+    def ncu_traffic(kernel, alg_bytes):
+        """DRAM read + write per launch for this kernel class from the committed
+        ncu --set full capture (profiles/ncu_traffic_r01c.json), scaled from that
+        capture's launch to this run's algorithmic bytes per launch."""
+        try:
+            ref = json.load(open(os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles",
+                                              "ncu_traffic_r01c.json")))
+            k = ref["kernels"][kernel]
+            ratio = (k["dram_read_bytes"] + k["dram_write_bytes"]) / k["algorithmic_bytes"]
+            return round(alg_bytes * ratio), round(ratio, 4), ref["source"]
+        except Exception:
+            return None, None, None
+
     peak, peak_kind = measured_peak_hbm()
     classes = {}
     for name, (ms, by, ns) in prof.items():
@@ -368,7 +381,12 @@ def main():
         ach = classes[dominant]["GBps"]
         roofline = {"bound": "hbm", "kernel": dominant, "achieved": round(ach, 1), "peak": peak,
                     "peak_kind": peak_kind, "unit": "GB/s", "frac": round(ach / peak, 4),
-                    "traffic": None, "per_class": classes}
+                    "per_class": classes}
+        tr, ratio, src = ncu_traffic(dominant, classes[dominant]["bytes_per_launch"])
+        roofline["traffic"] = tr
+        roofline["traffic_unit"] = "bytes per launch (DRAM read + write)"
+        roofline["traffic_over_algorithmic"] = ratio
+        roofline["traffic_source"] = src
         if proj:
             tot_ms = sum(prof[k][0] for k in proj)
             tot_b = sum(prof[k][1] for k in proj)
