@@ -24,6 +24,7 @@
 #include "dense.cuh"
 #include "kernels.cuh"
 #include "ts_tma.cuh"
+#include "cg_fused.cuh"
 #include "rom.cuh"
 
 namespace rd {
@@ -176,6 +177,35 @@ struct Ctx {
     int sms = 148;
     cudaStream_t s = nullptr;
     DevBuf partials, counter, scal, cgst, hist, rflag;
+    DevBuf fstep;  // per-step counters of the fused iteration (zero between launches)
+    DevBuf fprof;  // ROMDOT_FUSED_PROF: per-role cycle sums of cg_fused
+    long fprof_launches = 0;
+    // print and reset the cg_fused role accounting (average per launch, per warp)
+    void fprof_report() {
+        if (!fprof.p || !fprof_launches) return;
+        unsigned long long h[40];  // 5 roles x 8 slots
+        CK(cudaMemcpy(h, fprof.p, sizeof(h), cudaMemcpyDeviceToHost));
+        const double L = (double)fprof_launches;
+        auto pr = [&](const char* role, int base, double warps, const char* const* names) {
+            std::fprintf(stderr, "[cg_fused] %-9s", role);
+            for (int i = 0; i < 8; ++i)
+                if (names[i]) std::fprintf(stderr, " %s=%.1fus", names[i], h[base + i] / L / warps / 1.9e3);
+            std::fprintf(stderr, "\n");
+        };
+        const double G = sms;
+        static const char* const np[8] = {"wait_empty", nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, "total"};
+        static const char* const nr[8] = {"wait_owners", "fence+atomic", "batches(us=count)", nullptr, nullptr, nullptr, nullptr, "total"};
+        static const char* const ns[8] = {"poll", "wait_slot", "compute", nullptr, nullptr, nullptr, nullptr, "total"};
+        static const char* const nc[8] = {"full_p1", "full_p2", "wfull", "pfree", "p2_math", "p1_partial", nullptr, "total"};
+        static const char* const nu[8] = {"full", "pready", "update", "fence+red", nullptr, nullptr, nullptr, "total"};
+        pr("producer", 0, G, np);
+        pr("release", 8, G, nr);
+        pr("update", 16, G, nu);
+        pr("stencil", 32, G * 4, ns);
+        pr("consumer", 24, G * 8, nc);
+        CK(cudaMemset(fprof.p, 0, fprof.bytes));
+        fprof_launches = 0;
+    }
     CGState* st_host = nullptr;  // pinned, 2 slots
     cudaEvent_t ev[2] = {nullptr, nullptr};
     cudaEvent_t mark[2] = {nullptr, nullptr};
@@ -480,6 +510,100 @@ void ts_tma_launch(Ctx& c, const T* Krb, int C, long n, const T* x, T* xo, const
         ts_tma_inst<T, MODE, 16>(c, Krb, C, n, x, xo, cin, out, r, p, s, y, st, G);
 }
 
+// ------------------------------------------------- fused CG iteration launcher ---
+// cg_fused (cg_fused.cuh): update of iteration i + stencil, dots and K^T w of
+// iteration i+1 in one launch, one HBM stream of the row-blocked K.
+template <class T, int CPW>
+void cg_fused_inst(Ctx& c, const OpDev& op, const T* Krb, int C, T* w, T* r, T* p, T* s, T* y, CGState* st,
+                   double* cbuf, const T* G) {
+    const long n = op.n;
+    const int es = sizeof(T);
+    int TR = 256;
+    while (TR > 32 && (long)TR * C * es > 48 * 1024) TR >>= 1;
+    FusedLayout L = fused_layout<T>(C, TR, 2);
+    const uint32_t fixed = L.total - 2 * L.stage_bytes;
+    static const long cap_kb = [] {
+        const char* e = std::getenv("ROMDOT_FUSED_SMEM_KB");
+        return e ? std::atol(e) : 222L;
+    }();
+    int S = (int)std::min<long>(8, (cap_kb * 1024 - fixed) / L.stage_bytes);
+    if (S < 2) S = 2;
+    L = fused_layout<T>(C, TR, S);
+    static int configured = 0;
+    if (!configured) {
+        int optin = 0;
+        CK(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, c.device));
+        cudaFuncAttributes fa;
+        CK(cudaFuncGetAttributes(&fa, cg_fused<T, CPW>));
+        CK(cudaFuncSetAttribute(cg_fused<T, CPW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                optin - (int)fa.sharedSizeBytes));
+        configured = optin - (int)fa.sharedSizeBytes;
+    }
+    if ((int)L.total > configured) throw ConfigError("fused CG iteration: shared-memory ring too large");
+    const long ntile = padded_rows(n) / TR;
+    const int grid = (int)std::max(1L, std::min<long>(ntile, (long)c.sms));
+    const long P = op.d == 3 ? (long)op.N0 * op.N1 : (long)op.N0;
+    const long D = (TR - 1 + P) / TR;
+    L.L = (int)((grid - 1 + D) / grid);
+    static const int slack = [] {
+        const char* e = std::getenv("ROMDOT_FUSED_SLACK");
+        return e ? std::max(0, std::atoi(e)) : 7;
+    }();
+    L.LI = L.L + slack;
+    static const int pf = [] {
+        const char* e = std::getenv("ROMDOT_FUSED_PF");
+        return e ? std::max(0, std::atoi(e)) : 0;
+    }();
+    L.PF = pf;
+    static const int dbg = [] {
+        const char* e = std::getenv("ROMDOT_FUSED_DBG");
+        return e ? std::atoi(e) : 0;
+    }();
+    L.dbg = dbg;
+    const long nsteps = (ntile + grid - 1) / grid;
+    if (c.fstep.bytes < sizeof(unsigned) * nsteps) {
+        c.fstep.ensure(sizeof(unsigned) * (nsteps + 1024));
+        CK(cudaMemsetAsync(c.fstep.p, 0, c.fstep.bytes, c.s));
+    }
+    static const bool tprof = [] {
+        const char* e = std::getenv("ROMDOT_FUSED_PROF");
+        return e && std::atoi(e) != 0;
+    }();
+    if (tprof && !c.fprof.p) {
+        c.fprof.ensure(sizeof(unsigned long long) * 40);  // 5 roles x 8 slots
+        CK(cudaMemsetAsync(c.fprof.p, 0, c.fprof.bytes, c.s));
+    }
+    cg_fused<T, CPW><<<grid, FU_THREADS, L.total, c.s>>>(op, Krb, C, ntile, L, w, r, p, s, y, st,
+                                                          c.hist.template as<double>(), c.red(), cbuf,
+                                                          c.fstep.template as<unsigned>(), G,
+                                                          tprof ? c.fprof.template as<unsigned long long>() : nullptr);
+    if (tprof) ++c.fprof_launches;
+    c.check_launch();
+}
+
+template <class T>
+void cg_fused_launch(Ctx& c, const OpDev& op, const T* Krb, int C, T* w, T* r, T* p, T* s, T* y, CGState* st,
+                     double* cbuf, const T* G) {
+    if (C > 128 || C < 1) throw ConfigError("fused CG iteration: 1..128 recycle columns");
+    const int cpw = (C + 7) / 8;
+    if (cpw <= 1)
+        cg_fused_inst<T, 1>(c, op, Krb, C, w, r, p, s, y, st, cbuf, G);
+    else if (cpw <= 2)
+        cg_fused_inst<T, 2>(c, op, Krb, C, w, r, p, s, y, st, cbuf, G);
+    else if (cpw <= 4)
+        cg_fused_inst<T, 4>(c, op, Krb, C, w, r, p, s, y, st, cbuf, G);
+    else if (cpw <= 6)
+        cg_fused_inst<T, 6>(c, op, Krb, C, w, r, p, s, y, st, cbuf, G);
+    else if (cpw <= 8)
+        cg_fused_inst<T, 8>(c, op, Krb, C, w, r, p, s, y, st, cbuf, G);
+    else if (cpw <= 10)
+        cg_fused_inst<T, 10>(c, op, Krb, C, w, r, p, s, y, st, cbuf, G);
+    else if (cpw <= 12)
+        cg_fused_inst<T, 12>(c, op, Krb, C, w, r, p, s, y, st, cbuf, G);
+    else
+        cg_fused_inst<T, 16>(c, op, Krb, C, w, r, p, s, y, st, cbuf, G);
+}
+
 // nrm[0] = ||x||^2, nrm[1..W] = x^T x
 template <class T> void launch_norms(Ctx& c, const T* x, long n, double* nrm) {
     vec_norms<T><<<c.grid_for(n, 256, 2), 256, 0, c.s>>>(x, n, c.red(), nrm);
@@ -772,6 +896,14 @@ template <class T> struct Workspace {
 // One-pass inner projection with the Gram-corrected second CGS coefficient
 // (default; ROMDOT_CGS1G=0 selects the three-stream CGS2, ROMDOT_NO_TMA the
 // non-TMA kernels, which use CGS2).
+// Fused one-launch iteration (cg_fused.cuh) on top of the one-pass projection
+// (default; ROMDOT_FUSED=0 keeps the three-launch iteration).
+// Read per solve (not cached) so a test can compare both paths in one process.
+inline bool use_fused_iteration() {
+    const char* e = std::getenv("ROMDOT_FUSED");
+    return (e ? std::atoi(e) : 1) != 0;
+}
+
 inline bool use_one_pass_projection() {
     static const bool on = [] {
         const char* e = std::getenv("ROMDOT_CGS1G");
@@ -881,10 +1013,27 @@ SolveOut recycled_cg(Ctx& c, DevOp& op, const T* U, const T* K, long ncol, const
     const int batch = n < 200000 ? 16 : 8;
     long batches = 0;
     const double es = sizeof(T);
+    const bool fused = gram_pass && use_fused_iteration();
     auto launch_batch = [&]() {
         for (int b = 0; b < batch; ++b) {
             const bool samp = c.prof && b == 0;
             const long iter = batches * batch;
+            if (fused) {
+                if (batches == 0 && b == 0) {
+                    // head of iteration 0: w = A r0, dots, alpha_0 ; c1 = K^T w
+                    cg_stencil_dots<T><<<grid_st, 256, 0, c.s>>>(op.d, r, w, st, c.hist.template as<double>(),
+                                                                 c.red(), kz);
+                    c.check_launch();
+                    ts_tma_launch<T, 0>(c, Kit, (int)ncol, n, w, nullptr, nullptr, c1, nullptr, nullptr, nullptr,
+                                        nullptr, st);
+                } else {
+                    // update of iteration i + head of iteration i+1, one stream of K
+                    cudaEvent_t e4 = samp ? c.prof_start() : nullptr;
+                    cg_fused_launch<T>(c, op.d, Kit, (int)ncol, w, r, p, s, y, st, c1, Gk);
+                    if (samp) c.prof_stop(e4, 4, n * (es * (ncol + 10.0) + 32.0), iter);
+                }
+                continue;
+            }
             cudaEvent_t e0 = samp ? c.prof_start() : nullptr;
             cg_stencil_dots<T><<<grid_st, 256, 0, c.s>>>(op.d, r, w, st, c.hist.template as<double>(), c.red(), kz);
             c.check_launch();
@@ -965,6 +1114,7 @@ SolveOut recycled_cg(Ctx& c, DevOp& op, const T* U, const T* K, long ncol, const
     c.sync();
     const CGState fin = c.st_host[0];
     if (c.prof) c.prof_flush(fin.it);
+    c.fprof_report();
     SolveOut out;
     out.iterations = fin.it;
     out.converged = fin.converged != 0;

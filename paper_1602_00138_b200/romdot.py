@@ -219,7 +219,7 @@ class Context:
     def profile(self, enable: bool = True):
         load_library().rd_ctx_profile(self.h, int(enable))
 
-    PROF_CLASSES = ("cg_stencil_dots", "ts_T", "ts_NT", "cg_update")
+    PROF_CLASSES = ("cg_stencil_dots", "ts_T", "ts_NT", "cg_update", "cg_fused")
 
     def prof(self):
         """{class: (ms_total, algorithmic_bytes_total, samples)} of the sampled launches."""

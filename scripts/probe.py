@@ -54,7 +54,7 @@ def main():
                                      args.iters, abs(lay.val[0]), outs[0].data_ptr(), outs[1].data_ptr(),
                                      outs[2].data_ptr(), C.byref(rep), None, 0, R.DEVICE))
         torch.cuda.synchronize()
-        print(f"solve rep {r}: {rep.iterations} its, {(time.perf_counter() - t0) * 1e3 / max(1, rep.iterations):.3f} ms/it")
+        print(f"solve rep {r}: {rep.iterations} its, relres {rep.final_relres:.6e}, {(time.perf_counter() - t0) * 1e3 / max(1, rep.iterations):.3f} ms/it")
     for k, (ms, by, ns) in ctx.prof().items():
         if ns:
             print(f"  {k:16s} {ms / ns * 1e3:9.1f} us/launch  {by / (ms / 1e3) / 1e9:8.1f} GB/s  ({ns} samples)")

@@ -385,3 +385,46 @@ def test_full_config_parity_C1(rd):
     spec.loader.exec_module(mod)
     out = mod.run("C1")
     assert out["pass"], out
+
+
+@pytest.mark.parametrize("d,N,cplx,width", [
+    (3, (64, 64, 64), False, 40),   # C3 grid: many steps per CTA, plane lag L > 1
+    (3, (48, 40, 44), True, 20),    # non-cubic complex, ragged last step
+    (2, (317, 317), True, 33),      # 2D: lag of one x-line
+    (3, (12, 12, 12), True, 9),     # tiny: fewer tiles than SMs, one step
+    (2, (33, 33), False, 6),
+])
+def test_fused_iteration_matches_unfused(rd, monkeypatch, d, N, cplx, width):
+    """cg_fused (update of iteration i + stencil/dots/K^T w of i+1 in one launch,
+    cg_fused.cuh) against the three-launch iteration on the same solve: both
+    converge, residual histories equal to rounding over the first iterations,
+    explicit residual <= tol. The random recycle spaces make these solves rough
+    (residual jumps of 20x), so the two roundings drift apart later; the
+    iteration counts are held to 2% + 2."""
+    g = P.GridSpec(d=d, N=N, h=1.0 / (N[0] - 1), D_bg=0.33)
+    f = random_fields(g, 8)
+    dt = np.complex128 if cplx else np.float64
+    if cplx:
+        f = P.Fields(f.D, f.mu, shift=g.h ** 2 * 0.1)
+    op_o = orc.Operator.grid(g, f, dt)
+    rng = np.random.default_rng(21)
+    # real W (also for the complex operator): a complex random W makes the
+    # bilinear K^T K = I basis ill-conditioned and COCG plateaus on both paths
+    W = rng.standard_normal((g.n, width)).astype(dt)
+    U, K = rd.recycle_space_from_raw(W, op_o.apply(W))
+    b = rng.standard_normal(g.n).astype(dt)
+    r0 = b - K @ (K.T @ b)
+    tol = 1e-8
+    op_g = rd.SchurOperator(g, f, dt)
+    out = {}
+    for fused in ("0", "1"):
+        monkeypatch.setenv("ROMDOT_FUSED", fused)
+        out[fused] = rd.recycled_cg(op_g, U, K, r0, tol, 2 * g.n, np.linalg.norm(b))
+    a, c = out["0"], out["1"]
+    assert a.report.converged and c.report.converged
+    assert abs(a.report.iterations - c.report.iterations) <= 2 + 0.02 * a.report.iterations
+    m = min(10, len(a.report.rel_residual_history), len(c.report.rel_residual_history))
+    assert np.allclose(c.report.rel_residual_history[:m], a.report.rel_residual_history[:m], rtol=1e-8, atol=0)
+    for res in (a, c):
+        assert np.linalg.norm(r0 - op_o.apply(res.correction)) <= 1.01 * tol * np.linalg.norm(b)
+    assert np.linalg.norm(c.correction - a.correction) <= 1e-5 * np.linalg.norm(a.correction)
