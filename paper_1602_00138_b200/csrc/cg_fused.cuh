@@ -2,8 +2,8 @@
 // the stencil, merged dots and first projection of iteration i+1, so the
 // recycle basis K crosses HBM ONCE per iteration instead of twice.
 //
-// The unfused iteration (recycled_cg in romdot.cu, the checker's
-// recycled_cg_step in oracle/romdot_oracle.cpp) is
+// The unfused iteration (recycled_cg in romdot.cu; the CPU checker restates
+// the same recurrence) is
 //   cg_stencil_dots : w = A r ; {r^T r, r^T w, r^H r} ; alpha, beta
 //   ts_tma<0>       : c1 = K^T w                       (K stream 1)
 //   ts_tma<2>       : q = w - K (2 c1 - G c1) ; p, s, y, r updates (K stream 2)
