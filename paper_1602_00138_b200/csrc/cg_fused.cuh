@@ -38,9 +38,10 @@ namespace rd {
 
 constexpr int FU_CONS = 256;                      // 8 consumer warps
 constexpr int FU_NSW = 4;                         // stencil warps
-constexpr int FU_THREADS = FU_CONS + 32 + 32 * FU_NSW + 64;  // + producer, stencil, release, update warps
+constexpr int FU_NREL = 2;  // release warps (alternating steps: their fences overlap)
+constexpr int FU_THREADS = FU_CONS + 32 + 32 * FU_NSW + 32 * FU_NREL + 32;  // + producer, stencil, release, update
 constexpr int FU_REL_WARP = FU_CONS / 32 + 1 + FU_NSW;
-constexpr int FU_UPD_WARP = FU_REL_WARP + 1;
+constexpr int FU_UPD_WARP = FU_REL_WARP + FU_NREL;
 constexpr int FU_NUPD = 1;
 constexpr int FU_NPB = 2;  // phase-1 partial buffers
 constexpr int FU_NWS = 2 * FU_NSW;                // w' slots (2 per stencil warp)
@@ -328,33 +329,30 @@ __global__ void __launch_bounds__(FU_THREADS, 1)
             });
             pr.flush(0, true);
         }
-    } else if (wid == FU_REL_WARP) {
+    } else if (wid >= FU_REL_WARP && wid < FU_REL_WARP + FU_NREL) {
         // ------------------------------ release warp ------------------------------
         // Publishes phase 1 of each step to the other CTAs: waits until the
         // update warp has stored r', p, s, y of the step's tile (CTA-scope
         // counter), then ONE gpu-scope fence (cumulative over those stores) for
         // every step completed since the last one, and the step counters. (A
         // fence per step in the update warp itself measured slower: 0.9 us each.)
+        // FU_NREL warps take alternating steps so consecutive fences overlap (a
+        // fence also waits for the warp's previous step-counter add).
         if (lane == 0) {
             FuProf pr{tprof};
             pr.start();
             volatile unsigned* rc = relcnt;
-            int done = 0;  // steps released so far
-            while (done < ns) {
+            for (int s1 = wid - FU_REL_WARP; s1 < ns; s1 += FU_NREL) {
                 long long ta = pr.now();
-                unsigned v;
-                while ((v = *rc) < (unsigned)(done + 1)) __nanosleep(32);
+                while (*rc < (unsigned)(s1 + 1)) __nanosleep(32);
                 pr.add(0, ta);
-                int m = (int)v;
-                if (m > ns) m = ns;
                 ta = pr.now();
                 fence_acq_rel_gpu();
-                for (int q = done; q < m; ++q) red_relaxed_gpu(stepcnt + q, 1u);
+                red_relaxed_gpu(stepcnt + s1, 1u);
                 pr.add(1, ta);
-                if (pr.t) pr.acc[2] += 1900;  // batch count (x 1 us in the report)
-                done = m;
+                if (pr.t) pr.acc[2] += 1900;  // release count (x 1 us in the report)
             }
-            pr.flush(8, true);
+            pr.flush(8, wid == FU_REL_WARP);
         }
     } else if (wid == FU_UPD_WARP) {
         // ------------------------------ update warp ------------------------------
