@@ -218,6 +218,18 @@ __global__ void __launch_bounds__(FU_THREADS, 1)
              CGState* st, double* hist, GridRed red, double* cbuf, unsigned* stepcnt, const T* __restrict__ G,
              unsigned long long* tprof) {
     if (st->done) return;
+    // ROMDOT_FUSED_PROF: launch-phase timestamps (ns) min/max over CTAs in
+    // tprof[40..47], folded into per-launch sums in tprof[48..55] by the last CTA
+    auto gtime = [] {
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+        return t;
+    };
+    if (tprof && threadIdx.x == 0) {
+        const unsigned long long t = gtime();
+        atomicMin(tprof + 40, t);
+        atomicMax(tprof + 41, t);
+    }
     constexpr int W = Sc<T>::W;
     extern __shared__ __align__(128) unsigned char smem[];
     const int TR = FL.TR, S = FL.S, RBN = FL.RBN;
@@ -257,17 +269,31 @@ __global__ void __launch_bounds__(FU_THREADS, 1)
         fence_mbar_init();
         relcnt[0] = 0u;
     }
-    // coef = 2 c1 - G c1 (the one-pass projection's Gram-corrected coefficient;
-    // G = K^T K symmetric), c1 = K^T w of the previous launch / the prologue
     for (int t = tid; t < C; t += blockDim.x) c1s[t] = Sc<T>::get(cbuf + (size_t)t * W);
-    __syncthreads();
-    for (int t = tid; t < C; t += blockDim.x) {
-        const T* gc = G + (size_t)t * C;
-        T acc = Sc<T>::zero();
-        for (int j = 0; j < C; ++j) acc = Sc<T>::fma(gc[j], c1s[j], acc);
-        cw[t] = Sc<T>::sub(Sc<T>::scale(c1s[t], 2.0), acc);
+    __syncthreads();  // barriers initialised, c1 staged
+    if (wid != FU_CONS / 32) {
+        // coef = 2 c1 - G c1 (the one-pass projection's Gram-corrected
+        // coefficient; G = K^T K symmetric), c1 = K^T w of the previous launch /
+        // the prologue. One warp per row of G (coalesced, fixed order); the
+        // producer warp is already issuing its first TMA loads meanwhile.
+        constexpr int NW = FU_THREADS / 32 - 1;
+        const int q = wid < FU_CONS / 32 ? wid : wid - 1;
+        for (int t = q; t < C; t += NW) {
+            const T* gc = G + (size_t)t * C;
+            T acc = Sc<T>::zero();
+            for (int j = lane; j < C; j += 32) acc = Sc<T>::fma(__ldg(gc + j), c1s[j], acc);
+            if constexpr (W == 1) {
+                acc = warp_sum(acc);
+            } else {
+                ((cplx&)acc).x = warp_sum(((cplx&)acc).x);
+                ((cplx&)acc).y = warp_sum(((cplx&)acc).y);
+            }
+            if (lane == 0) cw[t] = Sc<T>::sub(Sc<T>::scale(c1s[t], 2.0), acc);
+        }
+        // named barrier 1 over every warp but the producer
+        asm volatile("bar.sync 1, %0;" ::"r"(FU_THREADS - 32) : "memory");
     }
-    __syncthreads();
+    if (tprof && tid == 0) atomicMax(tprof + 42, gtime());
 
     if (wid == FU_CONS / 32) {
         // ------------------------------ producer ------------------------------
@@ -590,6 +616,11 @@ __global__ void __launch_bounds__(FU_THREADS, 1)
         }
     }
     __syncthreads();
+    if (tprof && tid == 0) {
+        const unsigned long long t = gtime();
+        atomicMin(tprof + 43, t);
+        atomicMax(tprof + 44, t);
+    }
     const int nv = C * W + 2 * W + 1;
     if (tid < 2 * W + 1) {
         double a = dsc[tid];
@@ -608,6 +639,27 @@ __global__ void __launch_bounds__(FU_THREADS, 1)
         st->alpha_prev = st->alpha;
         st->it = st->it + 1;
         cg_recurrence<T>(st, cbuf + C * W, hist);
+        if (tprof) {
+            // per launch: entry spread, prologue, roles (first/last CTA), commit+finish
+            const unsigned long long t = gtime(), a = tprof[40], b = tprof[41], c = tprof[42], d = tprof[43],
+                                     e = tprof[44];
+            tprof[48] += b - a;
+            tprof[49] += c - a;
+            tprof[50] += d - c;
+            tprof[51] += e - c;
+            tprof[52] += t - e;
+            tprof[53] += t - a;
+            if (tprof[45]) {  // previous launch end -> this entry
+                tprof[54] += a - tprof[45];
+                tprof[55] += 1;
+            }
+            tprof[45] = t;
+            tprof[40] = ~0ull;
+            tprof[41] = 0;
+            tprof[42] = 0;
+            tprof[43] = ~0ull;
+            tprof[44] = 0;
+        }
     }
 }
 

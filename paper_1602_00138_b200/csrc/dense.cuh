@@ -510,34 +510,38 @@ __global__ void scale_columns(T* X, long ld, int c, long n, const double* nrm2) 
 namespace rd {
 
 // Thin Gram G (a x b, b <= 8) = op(X)^T Y: a multi-vector T pass. Block y-index
-// selects 32 columns of X (4 per warp), lanes walk rows; per-lane accumulators
-// acc[4][b] live across the block's rows; deterministic grid reduction.
-template <class T, bool HERM, int B>
+// selects 8 CPW columns of X (CPW per warp), lanes walk rows; per-lane
+// accumulators acc[CPW][b] live across the block's rows; deterministic grid
+// reduction. CPW is chosen so ONE block row covers all a columns whenever the
+// registers allow (a = k + 1 + appends ~ 64..81 at C4): Y is then read once,
+// not once per 32-column chunk (the 32-column version re-read Y and left most
+// warps of the last chunk idle: 2.9 TB/s at a = 69, b = 4).
+template <class T, bool HERM, int B, int CPW>
 __global__ void __launch_bounds__(256) gram_thin(const T* __restrict__ X, long ldx, int a, const T* __restrict__ Y,
                                                  long ldy, int b, long n, GridRed red, T* __restrict__ G) {
     constexpr int W = Sc<T>::W;
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    const int c0 = blockIdx.y * 32 + wid * 4;
-    T acc[4][B];
+    const int c0 = blockIdx.y * 8 * CPW + wid * CPW;
+    T acc[CPW][B];
 #pragma unroll
-    for (int q = 0; q < 4; ++q)
+    for (int q = 0; q < CPW; ++q)
 #pragma unroll
         for (int v = 0; v < B; ++v) acc[q][v] = Sc<T>::zero();
     for (long row = (long)blockIdx.x * 32 + lane; row < n; row += (long)gridDim.x * 32) {
-        T yv[B], xv[4];
+        T yv[B], xv[CPW];
 #pragma unroll
-        for (int v = 0; v < B; ++v) yv[v] = v < b ? Y[(size_t)v * ldy + row] : Sc<T>::zero();
+        for (int v = 0; v < B; ++v) yv[v] = v < b ? __ldg(Y + (size_t)v * ldy + row) : Sc<T>::zero();
 #pragma unroll
-        for (int q = 0; q < 4; ++q) xv[q] = (c0 + q < a) ? X[(size_t)(c0 + q) * ldx + row] : Sc<T>::zero();
+        for (int q = 0; q < CPW; ++q) xv[q] = (c0 + q < a) ? __ldg(X + (size_t)(c0 + q) * ldx + row) : Sc<T>::zero();
 #pragma unroll
-        for (int q = 0; q < 4; ++q)
+        for (int q = 0; q < CPW; ++q)
 #pragma unroll
             for (int v = 0; v < B; ++v) acc[q][v] = opfma<T, HERM>(xv[q], yv[v], acc[q][v]);
     }
-    // block values: 32 columns x B vectors, column-major per block chunk
-    __shared__ double s_vals[32 * B * W];
+    // block values: 8 CPW columns x B vectors, column-major per block chunk
+    __shared__ double s_vals[8 * CPW * B * W];
 #pragma unroll
-    for (int q = 0; q < 4; ++q)
+    for (int q = 0; q < CPW; ++q)
 #pragma unroll
         for (int v = 0; v < B; ++v) {
             double t[W];
@@ -550,13 +554,13 @@ __global__ void __launch_bounds__(256) gram_thin(const T* __restrict__ X, long l
 #pragma unroll
             for (int w = 0; w < W; ++w) {
                 const double sv = warp_sum(t[w]);
-                if (lane == 0) s_vals[((wid * 4 + q) * B + v) * W + w] = sv;
+                if (lane == 0) s_vals[((wid * CPW + q) * B + v) * W + w] = sv;
             }
         }
     __syncthreads();
     // grid reduction over blockIdx.x for each column chunk (blockIdx.y): reuse the
     // generic last-block sum over all blocks with a per-chunk value offset
-    const int nv = 32 * B * W;
+    const int nv = 8 * CPW * B * W;
     if (!grid_commit(red, s_vals, nv)) return;
     // last block of the whole grid: sum, per chunk y, the gridDim.x partials
     __threadfence();
@@ -577,7 +581,134 @@ __global__ void __launch_bounds__(256) gram_thin(const T* __restrict__ X, long l
         const double sum =
             ((acc8[0] + acc8[1]) + (acc8[2] + acc8[3])) + ((acc8[4] + acc8[5]) + (acc8[6] + acc8[7]));
         const int colr = vv / (B * W), v = (vv / W) % B, w = vv % W;
-        const int col = yc * 32 + colr;
+        const int col = yc * 8 * CPW + colr;
+        if (col < a && v < b) reinterpret_cast<double*>(G)[((size_t)v * a + col) * W + w] = sum;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) *red.counter = 0u;
+}
+
+// Pipelined thin Gram (same result layout and reduction as gram_thin): the
+// 32-row tiles of the block's 8 CPW columns of X and of the b vectors of Y are
+// copied to shared memory with cp.async (16 B per thread, zero fill past the
+// ends) NS stages ahead, so ~(NS-1) x 32 x (8 CPW + B) x es bytes per SM are in
+// flight without costing registers (the register-staged gram_thin is
+// latency-bound at ~50 KB in flight per SM). One CTA per SM; lane = row of the
+// tile, warp = CPW columns, all B vectors.
+template <int BYTES> __device__ __forceinline__ void cp_async_el(void* dst, const void* src, bool ok) {
+    if constexpr (BYTES == 16)
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(smem_u32(dst)), "l"(src), "r"(ok ? 16 : 0)
+                     : "memory");
+    else
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(smem_u32(dst)), "l"(src), "r"(ok ? 8 : 0)
+                     : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N> __device__ __forceinline__ void cp_async_wait() {
+    asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
+template <class T, bool HERM, int B, int CPW, int NS, int RT>
+__global__ void __launch_bounds__(256, 1) gram_thin_pipe(const T* __restrict__ X, long ldx, int a,
+                                                         const T* __restrict__ Y, long ldy, int b, long n, GridRed red,
+                                                         T* __restrict__ G) {
+    constexpr int W = Sc<T>::W;
+    constexpr int NC = 8 * CPW;       // X columns per block
+    constexpr int SE = (NC + B) * RT;  // elements per stage (RT rows per tile)
+    extern __shared__ __align__(128) unsigned char gt_smem[];
+    T* sm = reinterpret_cast<T*>(gt_smem);
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    const int c0b = blockIdx.y * NC;
+    const long nrb = (n + RT - 1) / RT;
+    const long rb0 = blockIdx.x, stride = gridDim.x;
+    const long nmine = rb0 < nrb ? (nrb - rb0 + stride - 1) / stride : 0;
+    auto issue = [&](long k, int stage) {
+        if (k < nmine) {
+            const long rb = rb0 + k * stride;
+            T* st = sm + (size_t)stage * SE;
+            for (int e = tid; e < SE; e += 256) {
+                const int col = e / RT, rr = e % RT;
+                const long row = rb * RT + rr;
+                const T* src = X;
+                bool ok = false;
+                if (col < NC) {
+                    ok = c0b + col < a && row < n;
+                    if (ok) src = X + (size_t)(c0b + col) * ldx + row;
+                } else {
+                    ok = col - NC < b && row < n;
+                    if (ok) src = Y + (size_t)(col - NC) * ldy + row;
+                }
+                cp_async_el<sizeof(T)>(st + e, src, ok);
+            }
+        }
+        cp_async_commit();  // (possibly empty) group per k keeps the wait count uniform
+    };
+#pragma unroll
+    for (int s0 = 0; s0 < NS - 1; ++s0) issue(s0, s0);
+    T acc[CPW][B];
+#pragma unroll
+    for (int q = 0; q < CPW; ++q)
+#pragma unroll
+        for (int v = 0; v < B; ++v) acc[q][v] = Sc<T>::zero();
+    for (long k = 0; k < nmine; ++k) {
+        cp_async_wait<NS - 2>();
+        __syncthreads();  // stage k landed for every thread; stage k-1 fully consumed
+        issue(k + NS - 1, (int)((k + NS - 1) % NS));
+        const T* st = sm + (size_t)(k % NS) * SE;
+#pragma unroll
+        for (int h = 0; h < RT / 32; ++h) {
+            T yv[B];
+#pragma unroll
+            for (int v = 0; v < B; ++v) yv[v] = st[(NC + v) * RT + h * 32 + lane];
+#pragma unroll
+            for (int q = 0; q < CPW; ++q) {
+                const T xv = st[(wid * CPW + q) * RT + h * 32 + lane];
+#pragma unroll
+                for (int v = 0; v < B; ++v) acc[q][v] = opfma<T, HERM>(xv, yv[v], acc[q][v]);
+            }
+        }
+    }
+    cp_async_wait<0>();
+    __syncthreads();
+    double* s_vals = reinterpret_cast<double*>(gt_smem);  // reuse the ring
+#pragma unroll
+    for (int q = 0; q < CPW; ++q)
+#pragma unroll
+        for (int v = 0; v < B; ++v) {
+            double t[W];
+            if constexpr (W == 1) {
+                t[0] = (double&)acc[q][v];
+            } else {
+                t[0] = ((cplx&)acc[q][v]).x;
+                t[1] = ((cplx&)acc[q][v]).y;
+            }
+#pragma unroll
+            for (int w = 0; w < W; ++w) {
+                const double sv = warp_sum(t[w]);
+                if (lane == 0) s_vals[((wid * CPW + q) * B + v) * W + w] = sv;
+            }
+        }
+    __syncthreads();
+    const int nv = NC * B * W;
+    if (!grid_commit(red, s_vals, nv)) return;
+    __threadfence();
+    const int nyc = gridDim.y;
+    for (int e = threadIdx.x; e < nyc * nv; e += blockDim.x) {
+        const int yc = e / nv, vv = e % nv;
+        const double* pp = red.partials + (size_t)gridDim.x * yc * nv + vv;
+        double acc8[8] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+        unsigned bx = 0;
+        for (; bx + 8 <= gridDim.x; bx += 8) {
+#pragma unroll
+            for (int q = 0; q < 8; ++q) acc8[q] += __ldcg(pp + (size_t)(bx + q) * nv);
+        }
+#pragma unroll
+        for (int q = 0; q < 7; ++q)
+            if (bx + q < gridDim.x) acc8[q] += __ldcg(pp + (size_t)(bx + q) * nv);
+        const double sum =
+            ((acc8[0] + acc8[1]) + (acc8[2] + acc8[3])) + ((acc8[4] + acc8[5]) + (acc8[6] + acc8[7]));
+        const int colr = vv / (B * W), v = (vv / W) % B, w = vv % W;
+        const int col = yc * NC + colr;
         if (col < a && v < b) reinterpret_cast<double*>(G)[((size_t)v * a + col) * W + w] = sum;
     }
     __syncthreads();

@@ -181,9 +181,14 @@ struct Ctx {
     DevBuf fprof;  // ROMDOT_FUSED_PROF: per-role cycle sums of cg_fused
     long fprof_launches = 0;
     // print and reset the cg_fused role accounting (average per launch, per warp)
+    void fprof_reset() {
+        unsigned long long h[56] = {};
+        h[40] = h[43] = ~0ull;
+        CK(cudaMemcpy(fprof.p, h, sizeof(h), cudaMemcpyHostToDevice));
+    }
     void fprof_report() {
         if (!fprof.p || !fprof_launches) return;
-        unsigned long long h[40];  // 5 roles x 8 slots
+        unsigned long long h[56];  // 5 roles x 8 slots + launch-phase timestamps
         CK(cudaMemcpy(h, fprof.p, sizeof(h), cudaMemcpyDeviceToHost));
         const double L = (double)fprof_launches;
         auto pr = [&](const char* role, int base, double warps, const char* const* names) {
@@ -203,7 +208,12 @@ struct Ctx {
         pr("update", 16, G, nu);
         pr("stencil", 32, G * 4, ns);
         pr("consumer", 24, G * 8, nc);
-        CK(cudaMemset(fprof.p, 0, fprof.bytes));
+        std::fprintf(stderr,
+                     "[cg_fused] launch    entry_spread=%.1fus prologue=%.1fus roles_first=%.1fus roles_last=%.1fus "
+                     "commit+finish=%.1fus span=%.1fus gap_prev_end=%.1fus\n",
+                     h[48] / L / 1e3, h[49] / L / 1e3, h[50] / L / 1e3, h[51] / L / 1e3, h[52] / L / 1e3,
+                     h[53] / L / 1e3, h[55] ? (double)h[54] / h[55] / 1e3 : 0.0);
+        fprof_reset();
         fprof_launches = 0;
     }
     CGState* st_host = nullptr;  // pinned, 2 slots
@@ -224,6 +234,7 @@ struct Ctx {
         double bytes;
         long iter;
         cudaEvent_t a, b;
+        long nl;  // launches in the sample (iterations iter .. iter + nl - 1)
     };
     bool prof = false;
     ProfClass pc[8];
@@ -243,20 +254,20 @@ struct Ctx {
         CK(cudaEventRecord(a, s));
         return a;
     }
-    void prof_stop(cudaEvent_t a, int cls, double bytes, long iter) {
+    void prof_stop(cudaEvent_t a, int cls, double bytes, long iter, long nl = 1) {
         cudaEvent_t b = next_event();
         CK(cudaEventRecord(b, s));
-        pend.push_back(Pending{cls, bytes, iter, a, b});
+        pend.push_back(Pending{cls, bytes * nl, iter, a, b, nl});
     }
     // after a sync: keep samples of iterations that really executed
     void prof_flush(long executed) {
         for (auto& q : pend) {
-            if (q.iter >= executed) continue;
+            if (q.iter + q.nl > executed) continue;
             float ms = 0.f;
             CK(cudaEventElapsedTime(&ms, q.a, q.b));
             pc[q.cls].ms += ms;
             pc[q.cls].bytes += q.bytes;
-            pc[q.cls].samples += 1;
+            pc[q.cls].samples += q.nl;
         }
         pend.clear();
         evnext = 0;
@@ -570,8 +581,8 @@ void cg_fused_inst(Ctx& c, const OpDev& op, const T* Krb, int C, T* w, T* r, T* 
         return e && std::atoi(e) != 0;
     }();
     if (tprof && !c.fprof.p) {
-        c.fprof.ensure(sizeof(unsigned long long) * 40);  // 5 roles x 8 slots
-        CK(cudaMemsetAsync(c.fprof.p, 0, c.fprof.bytes, c.s));
+        c.fprof.ensure(sizeof(unsigned long long) * 56);  // 5 roles x 8 slots + launch phases
+        c.fprof_reset();
     }
     cg_fused<T, CPW><<<grid, FU_THREADS, L.total, c.s>>>(op, Krb, C, ntile, L, w, r, p, s, y, st,
                                                           c.hist.template as<double>(), c.red(), cbuf,
@@ -640,12 +651,82 @@ void cgs2(Ctx& c, const T* Q, long ldq, long t, const T* z, T* q, long n, double
 
 // ------------------------------------------------------- block helpers ---
 // G (a x b, device, ld a) = op(X)^T Y over n rows. sym: X == Y, upper tiles only.
-template <class T, bool HERM, int B>
+template <class T, bool HERM, int B, int CPW>
 void gram_thin_launch(Ctx& c, const T* X, long ldx, long a, const T* Y, long ldy, long b, long n, T* G) {
-    const int gx = (int)std::max(1L, std::min<long>((n + 31) / 32, (long)c.sms * 4 / ((a + 31) / 32) + 1));
-    dim3 grid(gx, (unsigned)((a + 31) / 32));
-    gram_thin<T, HERM, B><<<grid, 256, 0, c.s>>>(X, ldx, (int)a, Y, ldy, (int)b, n, c.red(), G);
+    const long chunks = (a + 8 * CPW - 1) / (8 * CPW);
+    static int per_sm = 0;
+    if (!per_sm) {
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, gram_thin<T, HERM, B, CPW>, 256, 0));
+        per_sm = std::max(1, per_sm);
+    }
+    const long want = std::max(1L, (long)c.sms * std::max(1, per_sm) / chunks);
+    const int gx = (int)std::max(1L, std::min<long>((n + 31) / 32, want));
+    if ((long)gx * chunks * 8 * CPW * B * Sc<T>::W > 1024L * 1024) throw ConfigError("gram_thin: partials");
+    dim3 grid(gx, (unsigned)chunks);
+    gram_thin<T, HERM, B, CPW><<<grid, 256, 0, c.s>>>(X, ldx, (int)a, Y, ldy, (int)b, n, c.red(), G);
     c.check_launch();
+}
+
+// pipelined thin Gram: one CTA per SM, NS-stage cp.async ring of RT-row tiles
+template <class T, bool HERM, int B, int CPW, int RT>
+void gram_thin_pipe_launch(Ctx& c, const T* X, long ldx, long a, const T* Y, long ldy, long b, long n, T* G) {
+    constexpr int NC = 8 * CPW;
+    constexpr size_t stage = sizeof(T) * (NC + B) * RT;
+    constexpr int NS = stage * 6 <= 210 * 1024 ? 6 : (stage * 5 <= 210 * 1024 ? 5 : (stage * 4 <= 210 * 1024 ? 4 : 3));
+    constexpr size_t smem = stage * NS;
+    static_assert(smem <= 220 * 1024, "gram_thin_pipe: ring too large");
+    static bool configured = false;
+    if (!configured) {
+        CK(cudaFuncSetAttribute(gram_thin_pipe<T, HERM, B, CPW, NS, RT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)smem));
+        configured = true;
+    }
+    const long chunks = (a + NC - 1) / NC;
+    const int gx = (int)std::max(1L, std::min<long>((n + RT - 1) / RT, (long)c.sms));
+    if ((long)gx * chunks * NC * B * Sc<T>::W > 1024L * 1024) throw ConfigError("gram_thin: partials");
+    dim3 grid(gx, (unsigned)chunks);
+    gram_thin_pipe<T, HERM, B, CPW, NS, RT><<<grid, 256, smem, c.s>>>(X, ldx, (int)a, Y, ldy, (int)b, n, c.red(), G);
+    c.check_launch();
+}
+
+template <class T, bool HERM, int B, int CPW>
+void gram_thin_pipe_rt(Ctx& c, const T* X, long ldx, long a, const T* Y, long ldy, long b, long n, T* G) {
+    static const int rt = [] {
+        const char* e = std::getenv("ROMDOT_GRAM_THIN_RT");
+        return e ? std::atoi(e) : 64;
+    }();
+    if constexpr (CPW <= 8) {
+        if (rt == 64) {
+            gram_thin_pipe_launch<T, HERM, B, CPW, 64>(c, X, ldx, a, Y, ldy, b, n, G);
+            return;
+        }
+    }
+    gram_thin_pipe_launch<T, HERM, B, CPW, 32>(c, X, ldx, a, Y, ldy, b, n, G);
+}
+
+// columns per warp: one block row over all a columns when the accumulators fit
+// (ROMDOT_GRAM_THIN=0 keeps the register-staged kernel)
+template <class T, bool HERM, int B>
+void gram_thin_cpw(Ctx& c, const T* X, long ldx, long a, const T* Y, long ldy, long b, long n, T* G) {
+    static const int pipe = [] {
+        const char* e = std::getenv("ROMDOT_GRAM_THIN");
+        return e ? std::atoi(e) : 1;
+    }();
+    if constexpr (B <= 4) {
+        // measured at n = 2M complex (exp: a = 64 / 69 / 81, b = 4): 0.48 / 0.71 / 0.71
+        // ms against 0.60 / 0.88 / 0.89 for the register-staged kernel, which
+        // stays faster for small L2-resident real problems (C3: n = 262k)
+        if (pipe && a <= 96 && n >= (1L << 20)) {
+            if (a <= 32)
+                gram_thin_pipe_rt<T, HERM, B, 4>(c, X, ldx, a, Y, ldy, b, n, G);
+            else if (a <= 64)
+                gram_thin_pipe_rt<T, HERM, B, 8>(c, X, ldx, a, Y, ldy, b, n, G);
+            else
+                gram_thin_pipe_rt<T, HERM, B, 12>(c, X, ldx, a, Y, ldy, b, n, G);
+            return;
+        }
+    }
+    gram_thin_launch<T, HERM, B, 4>(c, X, ldx, a, Y, ldy, b, n, G);
 }
 
 template <class T, bool HERM>
@@ -653,11 +734,11 @@ void gram(Ctx& c, const T* X, long ldx, long a, const T* Y, long ldy, long b, lo
     if (a == 0 || b == 0) return;
     if (!sym && b <= 8 && a <= 256) {  // thin: multi-vector T pass (no wasted tile FLOPs)
         if (b <= 2)
-            gram_thin_launch<T, HERM, 2>(c, X, ldx, a, Y, ldy, b, n, G);
+            gram_thin_cpw<T, HERM, 2>(c, X, ldx, a, Y, ldy, b, n, G);
         else if (b <= 4)
-            gram_thin_launch<T, HERM, 4>(c, X, ldx, a, Y, ldy, b, n, G);
+            gram_thin_cpw<T, HERM, 4>(c, X, ldx, a, Y, ldy, b, n, G);
         else
-            gram_thin_launch<T, HERM, 8>(c, X, ldx, a, Y, ldy, b, n, G);
+            gram_thin_cpw<T, HERM, 8>(c, X, ldx, a, Y, ldy, b, n, G);
         return;
     }
     const long ta = (a + GT<T>::TA - 1) / GT<T>::TA, tb = (b + GT<T>::TB - 1) / GT<T>::TB;
@@ -1014,6 +1095,7 @@ SolveOut recycled_cg(Ctx& c, DevOp& op, const T* U, const T* K, long ncol, const
     long batches = 0;
     const double es = sizeof(T);
     const bool fused = gram_pass && use_fused_iteration();
+    cudaEvent_t fused_ev = nullptr;
     auto launch_batch = [&]() {
         for (int b = 0; b < batch; ++b) {
             const bool samp = c.prof && b == 0;
@@ -1027,10 +1109,15 @@ SolveOut recycled_cg(Ctx& c, DevOp& op, const T* U, const T* K, long ncol, const
                     ts_tma_launch<T, 0>(c, Kit, (int)ncol, n, w, nullptr, nullptr, c1, nullptr, nullptr, nullptr,
                                         nullptr, st);
                 } else {
-                    // update of iteration i + head of iteration i+1, one stream of K
-                    cudaEvent_t e4 = samp ? c.prof_start() : nullptr;
+                    // update of iteration i + head of iteration i+1, one stream of K.
+                    // Sampled as a whole batch of back-to-back launches (an event
+                    // pair around every launch adds ~20 us of front-end gap to it);
+                    // kept only if all of them executed (prof_flush)
+                    const bool bs = c.prof && batches > 0;
+                    cudaEvent_t e4 = bs && b == 0 ? c.prof_start() : nullptr;
+                    if (e4) fused_ev = e4;
                     cg_fused_launch<T>(c, op.d, Kit, (int)ncol, w, r, p, s, y, st, c1, Gk);
-                    if (samp) c.prof_stop(e4, 4, n * (es * (ncol + 10.0) + 32.0), iter);
+                    if (bs && b == batch - 1) c.prof_stop(fused_ev, 4, n * (es * (ncol + 10.0) + 32.0), iter + 1, batch);
                 }
                 continue;
             }

@@ -24,6 +24,7 @@ def main():
     ap.add_argument("--iters", type=int, default=20)
     ap.add_argument("--reps", type=int, default=3)
     ap.add_argument("--stencil-cols", type=int, default=8)
+    ap.add_argument("--no-events", action="store_true", help="no per-launch CUDA events (wall time per iteration only)")
     args = ap.parse_args()
     import torch
     build.build()
@@ -46,7 +47,7 @@ def main():
     outs = [torch.empty(n, dtype=tdt, device="cuda") for _ in range(3)]
     rep = R._Report()
     L = R.load_library()
-    ctx.profile(True)
+    ctx.profile(not args.no_events)
     for r in range(args.reps):
         torch.cuda.synchronize()
         t0 = time.perf_counter()
