@@ -48,6 +48,7 @@ constexpr int FU_NWS = 2 * FU_NSW;                // w' slots (2 per stencil war
 
 struct FusedLayout {
     int TR, S, RBN, L, LI, PF;  // PF: phase-1 L2 prefetch distance (steps)
+    int poll_ns;                // back-off of the stencil warps' step-counter polls
     // LI: item-order lead of phase 1 (>= L, slack for the stencil warps)
     int dbg;  // timing experiments only: bit 0 skips the step waits, bit 1 the stencil loads, bit 2 the phase-2 K reload
     uint32_t tile_bytes, x_bytes, stage_bytes;
@@ -473,7 +474,7 @@ __global__ void __launch_bounds__(FU_THREADS, 1)
                 if (__all_sync(0xffffffffu, good))
                     ok += nq;
                 else
-                    __nanosleep(64);
+                    __nanosleep(FL.poll_ns);
             }
             pr.add(0, ta);
             const int slot = FU_NSW * (k & 1) + sw;
@@ -649,10 +650,11 @@ __global__ void __launch_bounds__(FU_THREADS, 1)
             tprof[51] += e - c;
             tprof[52] += t - e;
             tprof[53] += t - a;
-            if (tprof[45]) {  // previous launch end -> this entry
+            if (tprof[45] && a - tprof[45] < 1000000ull) {  // previous launch end -> this entry (same solve)
                 tprof[54] += a - tprof[45];
                 tprof[55] += 1;
             }
+            tprof[46] += 1;  // launches that ran (not the no-ops after convergence)
             tprof[45] = t;
             tprof[40] = ~0ull;
             tprof[41] = 0;

@@ -190,7 +190,7 @@ struct Ctx {
         if (!fprof.p || !fprof_launches) return;
         unsigned long long h[56];  // 5 roles x 8 slots + launch-phase timestamps
         CK(cudaMemcpy(h, fprof.p, sizeof(h), cudaMemcpyDeviceToHost));
-        const double L = (double)fprof_launches;
+        const double L = h[46] ? (double)h[46] : (double)fprof_launches;  // launches that ran
         auto pr = [&](const char* role, int base, double warps, const char* const* names) {
             std::fprintf(stderr, "[cg_fused] %-9s", role);
             for (int i = 0; i < 8; ++i)
@@ -566,6 +566,11 @@ void cg_fused_inst(Ctx& c, const OpDev& op, const T* Krb, int C, T* w, T* r, T* 
         return e ? std::max(0, std::atoi(e)) : 0;
     }();
     L.PF = pf;
+    static const int poll_ns = [] {
+        const char* e = std::getenv("ROMDOT_FUSED_POLL_NS");
+        return e ? std::max(0, std::atoi(e)) : 2000;  // ns; 64 measured 10% slower (power: the polls keep the GPU at its 1000 W cap)
+    }();
+    L.poll_ns = poll_ns;
     static const int dbg = [] {
         const char* e = std::getenv("ROMDOT_FUSED_DBG");
         return e ? std::atoi(e) : 0;

@@ -12,6 +12,13 @@ oracle run finishes in minutes (default C1):
   relative.
 
 Prints one JSON line (saved under profiles/ by the caller).
+
+At the target config (C4, n = 2,097,152 complex) the CPU checker cannot run
+the whole build in a GPU call (~35 s per solve on 16 host cores), so
+``--rhs m --device-seed`` runs the same lockstep on the first m RHS of the
+first systems, seeded with the DEVICE U0 / X0 (checked here against the
+checker's operator: eigen-residuals and X0 explicit residuals), and the
+compression and observable checks on the resulting candidate bases.
 Free-running builds can diverge after an append-decision flip on a marginal
 RHS; the lockstep comparison reports the flips it sees.
 """
@@ -37,22 +44,42 @@ def principal_sines(Q1, Q2):
     return np.sqrt(np.maximum(0.0, 1.0 - s * s))
 
 
-def run(config: str, n_systems: int = 0) -> dict:
+def run(config: str, n_systems: int = 0, n_rhs: int = 0, device_seed: bool = False) -> dict:
     import oracle as orc
     from paper_1602_00138_b200 import romdot as R
     c = P.CONFIGS[config]
-    g, lay = c.grid, c.layout()
+    g, lay_full = c.grid, c.layout()
+    lay = lay_full
+    if n_rhs:  # first n_rhs right-hand sides of every system (the basis keeps all X0 columns)
+        lay = P.Layout(lay_full.idx[:n_rhs].copy(), lay_full.val[:n_rhs].copy(), min(n_rhs, lay_full.n_src),
+                       max(0, n_rhs - lay_full.n_src))
     t0 = time.perf_counter()
     f0 = c.fields(0)
-    lam, U0 = orc.smallest_eigenpairs(orc.Operator.grid(g, f0), c.k, min(c.tol, 1e-8))
-    X0, _ = orc.initial_solutions(orc.Operator.grid(g, f0, c.dtype), lay, c.tol)
+    seed_check = {}
+    if device_seed:
+        lam, U0 = R.smallest_eigenpairs(R.SchurOperator(g, f0, np.float64), c.k, min(c.tol, 1e-8))
+        X0, _ = R.initial_solutions(R.SchurOperator(g, f0, c.dtype), lay_full, c.tol)
+        # the device seed, checked with the checker's own operator
+        op_r = orc.Operator.grid(g, f0)
+        er = np.linalg.norm(op_r.apply(U0) - U0 * lam, axis=0)
+        seed_check["eig_residual_over_lammax"] = float(er.max() / op_r.lam_max)
+        op0 = orc.Operator.grid(g, f0, c.dtype)
+        B0 = lay_full.dense(g.n, c.dtype)
+        seed_check["X0_max_explicit_residual"] = float(
+            (np.linalg.norm(op0.apply(X0) - B0, axis=0) / np.linalg.norm(B0, axis=0)).max())
+        del B0
+    else:
+        lam, U0 = orc.smallest_eigenpairs(orc.Operator.grid(g, f0), c.k, min(c.tol, 1e-8))
+        X0, _ = orc.initial_solutions(orc.Operator.grid(g, f0, c.dtype), lay, c.tol)
     U0 = U0.astype(c.dtype)
     t_seed = time.perf_counter() - t0
     gb_o = orc.GlobalBasis(U0, X0, c.cap)
     gb_g = R.GlobalBasis(U0, X0, c.cap)
+    del U0, X0
     systems = c.systems()[: n_systems] if n_systems else c.systems()
     rows = flips = worst_its = 0
-    worst_relres = worst_res = 0.0
+    worst_relres = worst_res = worst_res_cpu = xdiff = 0.0
+    log_rows = []
     t_cpu = t_gpu = 0.0
     B = lay.dense(g.n, c.dtype)
     for s, (pt, w) in enumerate(systems, start=1):
@@ -66,6 +93,11 @@ def run(config: str, n_systems: int = 0) -> dict:
         t_gpu += time.perf_counter() - t0
         res = np.linalg.norm(op_o.apply(pg.X) - B, axis=0) / np.linalg.norm(B, axis=0)
         worst_res = max(worst_res, float(res.max()))
+        res_o = np.linalg.norm(op_o.apply(po.X) - B, axis=0) / np.linalg.norm(B, axis=0)
+        worst_res_cpu = max(worst_res_cpu, float(res_o.max()))
+        xdiff = max(xdiff, float((np.linalg.norm(pg.X - po.X, axis=0) / np.linalg.norm(po.X, axis=0)).max()))
+        log_rows += [[s, ro.rhs, ro.iterations, rg.iterations, ro.init_relres, rg.init_relres, int(ro.appended),
+                      int(rg.appended)] for ro, rg in zip(po.log, pg.log)]
         for ro, rg in zip(po.log, pg.log):
             rows += 1
             if ro.appended != rg.appended:
@@ -74,6 +106,7 @@ def run(config: str, n_systems: int = 0) -> dict:
             worst_its = max(worst_its, abs(ro.iterations - rg.iterations))
             if ro.init_relres > 0:
                 worst_relres = max(worst_relres, abs(ro.init_relres - rg.init_relres) / ro.init_relres)
+        del po, pg
         print(json.dumps({"system": s, "cols_cpu": gb_o.cols, "cols_gpu": gb_g.cols, "flips": flips}),
               file=sys.stderr, flush=True)
         if flips:
@@ -100,7 +133,10 @@ def run(config: str, n_systems: int = 0) -> dict:
     rel = lambda a, b: float(np.linalg.norm(a - b) / np.linalg.norm(b))  # noqa: E731
     out = {"config": config, "systems": len(systems), "rows": rows, "append_flips": flips,
            "max_iteration_diff": worst_its, "max_init_relres_reldiff": worst_relres,
-           "max_explicit_residual_gpu": worst_res, "tol": c.tol,
+           "max_explicit_residual_gpu": worst_res, "max_explicit_residual_cpu": worst_res_cpu,
+           "max_solution_reldiff": xdiff, "tol": c.tol, "rhs_per_system": lay.n_rhs,
+           "seed": "device (checked with the checker's operator)" if device_seed else "checker", **seed_check,
+           "log_cpu_vs_gpu": log_rows if n_rhs else None,
            "rank_cpu": int(rank_o), "rank_gpu": int(rank_g), "max_principal_sine": float(sines.max()),
            "rom_transfer_reldiff": rel(psi_g, psi_o), "rom_jacobian_reldiff": rel(J_g, J_o),
            "rom_vs_fom_offtraining": rel(psi_g, fom),
@@ -114,9 +150,11 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--config", default="C1")
     ap.add_argument("--systems", type=int, default=0)
+    ap.add_argument("--rhs", type=int, default=0, help="first m RHS per system (0 = all)")
+    ap.add_argument("--device-seed", action="store_true", help="U0 / X0 from the device (checked), not the checker")
     args = ap.parse_args()
     build.build()
-    print(json.dumps(run(args.config, args.systems)))
+    print(json.dumps(run(args.config, args.systems, args.rhs, args.device_seed)))
 
 
 if __name__ == "__main__":
