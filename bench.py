@@ -364,7 +364,7 @@ def main():
                                               "ncu_traffic_r01c.json")))
             k = ref["kernels"][kernel]
             ratio = (k["dram_read_bytes"] + k["dram_write_bytes"]) / k["algorithmic_bytes"]
-            return round(alg_bytes * ratio), round(ratio, 4), ref["source"]
+            return round(alg_bytes * ratio), round(ratio, 4), k.get("source", ref["source"])
         except Exception:
             return None, None, None
 

@@ -49,6 +49,7 @@ constexpr int FU_NWS = 2 * FU_NSW;                // w' slots (2 per stencil war
 struct FusedLayout {
     int TR, S, RBN, L, LI, PF;  // PF: phase-1 L2 prefetch distance (steps)
     int poll_ns;                // back-off of the stencil warps' step-counter polls
+    int rel_ns;                 // back-off of the release warps' wait for the update warp
     // LI: item-order lead of phase 1 (>= L, slack for the stencil warps)
     int dbg;  // timing experiments only: bit 0 skips the step waits, bit 1 the stencil loads, bit 2 the phase-2 K reload
     uint32_t tile_bytes, x_bytes, stage_bytes;
@@ -218,6 +219,14 @@ __global__ void __launch_bounds__(FU_THREADS, 1)
     cg_fused(OpDev op, const T* __restrict__ Krb, int C, long ntile, FusedLayout FL, T* w, T* r, T* p, T* s, T* y,
              CGState* st, double* hist, GridRed red, double* cbuf, unsigned* stepcnt, const T* __restrict__ G,
              unsigned long long* tprof) {
+    // Programmatic dependent launch (ROMDOT_FUSED_PDL, default on): the next
+    // iteration's launch may be scheduled as soon as every CTA of this one has
+    // started, so its CTAs take the SMs this grid's CTAs free while the last CTA
+    // reduces, and wait here until this grid has completed (memory visible).
+    // Nothing before the wait reads global memory. Without the launch
+    // attribute both instructions are no-ops.
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    asm volatile("griddepcontrol.wait;" ::: "memory");
     if (st->done) return;
     // ROMDOT_FUSED_PROF: launch-phase timestamps (ns) min/max over CTAs in
     // tprof[40..47], folded into per-launch sums in tprof[48..55] by the last CTA
@@ -371,7 +380,7 @@ __global__ void __launch_bounds__(FU_THREADS, 1)
             volatile unsigned* rc = relcnt;
             for (int s1 = wid - FU_REL_WARP; s1 < ns; s1 += FU_NREL) {
                 long long ta = pr.now();
-                while (*rc < (unsigned)(s1 + 1)) __nanosleep(32);
+                while (*rc < (unsigned)(s1 + 1)) __nanosleep(FL.rel_ns);
                 pr.add(0, ta);
                 ta = pr.now();
                 fence_acq_rel_gpu();

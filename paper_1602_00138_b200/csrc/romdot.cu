@@ -571,6 +571,11 @@ void cg_fused_inst(Ctx& c, const OpDev& op, const T* Krb, int C, T* w, T* r, T* 
         return e ? std::max(0, std::atoi(e)) : 2000;  // ns; 64 measured 10% slower (power: the polls keep the GPU at its 1000 W cap)
     }();
     L.poll_ns = poll_ns;
+    static const int rel_ns = [] {
+        const char* e = std::getenv("ROMDOT_FUSED_REL_NS");
+        return e ? std::max(0, std::atoi(e)) : 256;
+    }();
+    L.rel_ns = rel_ns;
     static const int dbg = [] {
         const char* e = std::getenv("ROMDOT_FUSED_DBG");
         return e ? std::atoi(e) : 0;
@@ -589,10 +594,23 @@ void cg_fused_inst(Ctx& c, const OpDev& op, const T* Krb, int C, T* w, T* r, T* 
         c.fprof.ensure(sizeof(unsigned long long) * 56);  // 5 roles x 8 slots + launch phases
         c.fprof_reset();
     }
-    cg_fused<T, CPW><<<grid, FU_THREADS, L.total, c.s>>>(op, Krb, C, ntile, L, w, r, p, s, y, st,
-                                                          c.hist.template as<double>(), c.red(), cbuf,
-                                                          c.fstep.template as<unsigned>(), G,
-                                                          tprof ? c.fprof.template as<unsigned long long>() : nullptr);
+    static const bool pdl = [] {
+        const char* e = std::getenv("ROMDOT_FUSED_PDL");
+        return e ? std::atoi(e) != 0 : true;
+    }();
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)grid);
+    cfg.blockDim = dim3(FU_THREADS);
+    cfg.dynamicSmemBytes = L.total;
+    cfg.stream = c.s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = pdl ? 1 : 0;
+    CK(cudaLaunchKernelEx(&cfg, cg_fused<T, CPW>, op, Krb, C, ntile, L, w, r, p, s, y, st,
+                          c.hist.template as<double>(), c.red(), cbuf, c.fstep.template as<unsigned>(), G,
+                          tprof ? c.fprof.template as<unsigned long long>() : (unsigned long long*)nullptr));
     if (tprof) ++c.fprof_launches;
     c.check_launch();
 }

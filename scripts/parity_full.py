@@ -111,6 +111,10 @@ def run(config: str, n_systems: int = 0, n_rhs: int = 0, device_seed: bool = Fal
               file=sys.stderr, flush=True)
         if flips:
             break
+    print(json.dumps({"lockstep_rows": rows, "append_flips": flips, "max_iteration_diff": worst_its,
+                      "max_init_relres_reldiff": worst_relres, "max_explicit_residual_gpu": worst_res,
+                      "max_explicit_residual_cpu": worst_res_cpu, "max_solution_reldiff": xdiff, **seed_check}),
+          file=sys.stderr, flush=True)
     # compression: RRQR of each candidate basis at 1e-10 (normalised columns)
     Vo = gb_o.V
     rank_o, _, _, Qo = orc.qrcp(Vo, 1e-10, True)
@@ -123,13 +127,13 @@ def run(config: str, n_systems: int = 0, n_rhs: int = 0, device_seed: bool = Fal
     op = R.SchurOperator(g, f, c.dtype)
     rom_o = R.ReducedModel(Qo[:, :rank_o])
     rom_g = R.ReducedModel(Qg[:, :rank_g])
-    psi_o, psi_g = rom_o.transfer(op, lay), rom_g.transfer(op, lay)
+    psi_o, psi_g = rom_o.transfer(op, lay_full), rom_g.transfer(op, lay_full)
     rng = np.random.default_rng(7)
     sup = [(np.sort(rng.choice(g.n, size=g.n // 20, replace=False)), rng.uniform(0.1, 1.0, g.n // 20))
            for _ in range(4)]
-    J_o = rom_o.jacobian(op, lay, sup, -g.h ** 2)
-    J_g = rom_g.jacobian(op, lay, sup, -g.h ** 2)
-    fom, _ = R.fom_transfer(op, lay, 1e-10)
+    J_o = rom_o.jacobian(op, lay_full, sup, -g.h ** 2)
+    J_g = rom_g.jacobian(op, lay_full, sup, -g.h ** 2)
+    fom, _ = R.fom_transfer(op, lay_full, 1e-10)
     rel = lambda a, b: float(np.linalg.norm(a - b) / np.linalg.norm(b))  # noqa: E731
     out = {"config": config, "systems": len(systems), "rows": rows, "append_flips": flips,
            "max_iteration_diff": worst_its, "max_init_relres_reldiff": worst_relres,

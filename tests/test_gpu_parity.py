@@ -387,6 +387,23 @@ def test_full_config_parity_C1(rd):
     assert out["pass"], out
 
 
+def test_partial_lockstep_device_seed_C2(rd):
+    """The target-config recipe (scripts/parity_full.py --rhs --device-seed, run
+    at C4 on the box) on the complex 2D config C2: device U0 / X0 checked with
+    the checker's operator, then the first 4 RHS of two systems (omega = 0 and
+    0.05) in lockstep with north_star's tolerances."""
+    import importlib.util
+    import os
+    spec = importlib.util.spec_from_file_location(
+        "parity_full", os.path.join(os.path.dirname(__file__), "..", "scripts", "parity_full.py"))
+    mod = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(mod)
+    out = mod.run("C2", n_systems=2, n_rhs=4, device_seed=True)
+    assert out["X0_max_explicit_residual"] <= out["tol"], out
+    assert out["eig_residual_over_lammax"] <= 1e-8, out
+    assert out["pass"], out
+
+
 @pytest.mark.parametrize("d,N,cplx,width", [
     (3, (64, 64, 64), False, 40),   # C3 grid: many steps per CTA, plane lag L > 1
     (3, (48, 40, 44), True, 20),    # non-cubic complex, ragged last step
