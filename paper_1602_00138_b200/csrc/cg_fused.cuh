@@ -219,7 +219,7 @@ __global__ void __launch_bounds__(FU_THREADS, 1)
     cg_fused(OpDev op, const T* __restrict__ Krb, int C, long ntile, FusedLayout FL, T* w, T* r, T* p, T* s, T* y,
              CGState* st, double* hist, GridRed red, double* cbuf, unsigned* stepcnt, const T* __restrict__ G,
              unsigned long long* tprof) {
-    // Programmatic dependent launch (ROMDOT_FUSED_PDL, default on): the next
+    // Programmatic dependent launch (ROMDOT_FUSED_PDL=1, opt-in): the next
     // iteration's launch may be scheduled as soon as every CTA of this one has
     // started, so its CTAs take the SMs this grid's CTAs free while the last CTA
     // reduces, and wait here until this grid has completed (memory visible).
