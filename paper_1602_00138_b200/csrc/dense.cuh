@@ -268,6 +268,141 @@ __global__ void __launch_bounds__(256) gemm_tall(const T* __restrict__ X, long l
     }
 }
 
+// Z[n x b] = (SUB ? Y : 0) -/+ X[n x a] M[a x b] on the FP64 tensor cores (DMMA
+// m8n8k4, as gram_kernel): the MMA's M dimension is the rows of X, N the
+// output columns, K the inner dimension a. Block tile 128 rows x 64 columns
+// (complex: 4 real DMMA per product on split re / im planes; real: 128 x 128),
+// 8 warps as 4 (rows) x 2 (columns), warp tile 32 x 32 (real 32 x 64). Chunks
+// of 16 inner indices are register double buffered from global memory and
+// staged as Xs[plane][k][row] (ld 136: the four k rows of an A fragment hit
+// disjoint bank octets) and Ms[plane][col][k] (ld 20). upper_tri: M is upper
+// triangular, so a column block stops at its last column.
+constexpr int GD_TR = 128, GD_KC = 16, GD_LDX = GD_TR + 8, GD_LDM = 20;
+template <class T> struct GDT;
+template <> struct GDT<double> { static constexpr int TC = 128; };
+template <> struct GDT<cplx> { static constexpr int TC = 64; };
+template <class T> constexpr size_t gemm_dmma_smem() {
+    return sizeof(double) * Sc<T>::W * (GD_KC * GD_LDX + GDT<T>::TC * GD_LDM);
+}
+
+template <class T, bool SUB>
+__global__ void __launch_bounds__(256) gemm_tall_dmma(const T* __restrict__ X, long ldx, int a,
+                                                      const T* __restrict__ M, int b, const T* __restrict__ Y,
+                                                      long ldy, T* __restrict__ Z, long ldz, long n, bool upper_tri) {
+    constexpr bool CPLX = Sc<T>::W == 2;
+    constexpr int PL = CPLX ? 2 : 1;
+    constexpr int TR = GD_TR, TC = GDT<T>::TC, KC = GD_KC;
+    constexpr int WM = TR / 4, WN = TC / 2;  // warp tile
+    constexpr int MT = WM / 8, NT = WN / 8;
+    extern __shared__ __align__(16) double gd_smem[];  // Xs[PL][KC][GD_LDX], Ms[PL][TC][GD_LDM]
+    auto Xs = reinterpret_cast<double (*)[KC][GD_LDX]>(gd_smem);
+    auto Ms = reinterpret_cast<double (*)[TC][GD_LDM]>(gd_smem + PL * KC * GD_LDX);
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    const int wm = wid >> 1, wn = wid & 1;
+    const long row0 = (long)blockIdx.y * TR;
+    const int col0 = blockIdx.x * TC;
+    const int kend = upper_tri ? min(a, col0 + TC) : a;
+    double acc[PL][MT][NT][2];
+#pragma unroll
+    for (int p = 0; p < PL; ++p)
+#pragma unroll
+        for (int i = 0; i < MT; ++i)
+#pragma unroll
+            for (int j = 0; j < NT; ++j) acc[p][i][j][0] = acc[p][i][j][1] = 0.0;
+    constexpr int NX = TR * KC / 256, NM = KC * TC / 256;
+    T px[NX], pm[NM];
+    auto fetch = [&](int k0) {
+#pragma unroll
+        for (int q = 0; q < NX; ++q) {
+            const int e = tid + q * 256;
+            const int r = e % TR, k = e / TR;
+            const long row = row0 + r;
+            px[q] = (row < n && k0 + k < kend) ? X[(size_t)(k0 + k) * ldx + row] : Sc<T>::zero();
+        }
+#pragma unroll
+        for (int q = 0; q < NM; ++q) {
+            const int e = tid + q * 256;
+            const int k = e % KC, cc = e / KC;
+            pm[q] = (k0 + k < kend && col0 + cc < b) ? M[(size_t)(col0 + cc) * a + k0 + k] : Sc<T>::zero();
+        }
+    };
+    auto stage = [&]() {
+#pragma unroll
+        for (int q = 0; q < NX; ++q) {
+            const int e = tid + q * 256;
+            const int r = e % TR, k = e / TR;
+            if constexpr (CPLX) {
+                Xs[0][k][r] = ((cplx&)px[q]).x;
+                Xs[1][k][r] = ((cplx&)px[q]).y;
+            } else {
+                Xs[0][k][r] = (double&)px[q];
+            }
+        }
+#pragma unroll
+        for (int q = 0; q < NM; ++q) {
+            const int e = tid + q * 256;
+            const int k = e % KC, cc = e / KC;
+            if constexpr (CPLX) {
+                Ms[0][cc][k] = ((cplx&)pm[q]).x;
+                Ms[1][cc][k] = ((cplx&)pm[q]).y;
+            } else {
+                Ms[0][cc][k] = (double&)pm[q];
+            }
+        }
+    };
+    const int fr = lane >> 2, fk = lane & 3;
+    if (kend > 0) fetch(0);
+    for (int k0 = 0; k0 < kend; k0 += KC) {
+        stage();
+        __syncthreads();
+        if (k0 + KC < kend) fetch(k0 + KC);
+#pragma unroll
+        for (int kk = 0; kk < KC; kk += 4) {
+            double af[PL][MT], bf[PL][NT];
+#pragma unroll
+            for (int p = 0; p < PL; ++p) {
+#pragma unroll
+                for (int i = 0; i < MT; ++i) af[p][i] = Xs[p][kk + fk][wm * WM + i * 8 + fr];
+#pragma unroll
+                for (int j = 0; j < NT; ++j) bf[p][j] = Ms[p][wn * WN + j * 8 + fr][kk + fk];
+            }
+#pragma unroll
+            for (int i = 0; i < MT; ++i)
+#pragma unroll
+                for (int j = 0; j < NT; ++j) {
+                    if constexpr (CPLX) {
+                        // re += xr mr - xi mi ; im += xr mi + xi mr
+                        dmma(acc[0][i][j][0], acc[0][i][j][1], af[0][i], bf[0][j]);
+                        dmma(acc[0][i][j][0], acc[0][i][j][1], -af[1][i], bf[1][j]);
+                        dmma(acc[1][i][j][0], acc[1][i][j][1], af[0][i], bf[1][j]);
+                        dmma(acc[1][i][j][0], acc[1][i][j][1], af[1][i], bf[0][j]);
+                    } else {
+                        dmma(acc[0][i][j][0], acc[0][i][j][1], af[0][i], bf[0][j]);
+                    }
+                }
+        }
+        __syncthreads();
+    }
+#pragma unroll
+    for (int i = 0; i < MT; ++i)
+#pragma unroll
+        for (int j = 0; j < NT; ++j)
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+                const long row = row0 + wm * WM + i * 8 + fr;
+                const int col = col0 + wn * WN + j * 8 + 2 * fk + e;
+                if (row < n && col < b) {
+                    T v;
+                    if constexpr (CPLX)
+                        v = make_double2(acc[0][i][j][e], acc[1][i][j][e]);
+                    else
+                        v = acc[0][i][j][e];
+                    if (SUB) v = Sc<T>::sub(Y[(size_t)col * ldy + row], v);
+                    Z[(size_t)col * ldz + row] = v;
+                }
+            }
+}
+
 // ------------------------------------------------------------ small dense ---
 // In-place upper Cholesky of the r x r matrix G (column-major, ld r):
 // HERM: G = S^H S ; bilinear: G = S^T S (complex symmetric). Lower part zeroed.

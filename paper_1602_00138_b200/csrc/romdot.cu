@@ -811,6 +811,29 @@ void gemm(Ctx& c, const T* X, long ldx, long a, const T* M, long b, const T* Y, 
                 CK(cudaMemcpyAsync(Z + j * ldz, Y + j * ldy, sizeof(T) * n, cudaMemcpyDeviceToDevice, c.s));
         return;
     }
+    static const int dmma_on = [] {
+        const char* e = std::getenv("ROMDOT_GEMM_DMMA");
+        return e ? std::atoi(e) : 1;
+    }();
+    if (dmma_on && a >= 32) {  // FP64 tensor cores (gemm_tall_dmma); DFMA kernel below otherwise
+        constexpr int TCD = GDT<T>::TC;
+        constexpr size_t smem = gemm_dmma_smem<T>();
+        static bool configured = false;
+        if (!configured) {
+            CK(cudaFuncSetAttribute(gemm_tall_dmma<T, SUB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+            configured = true;
+        }
+        const long rtd = (n + GD_TR - 1) / GD_TR;
+        for (long r0 = 0; r0 < rtd; r0 += 65535) {
+            const long nr = std::min(65535L, rtd - r0);
+            const long off = r0 * GD_TR;
+            dim3 grid((unsigned)((b + TCD - 1) / TCD), (unsigned)nr);
+            gemm_tall_dmma<T, SUB><<<grid, 256, smem, c.s>>>(X + off, ldx, (int)a, M, (int)b, SUB ? Y + off : nullptr,
+                                                          ldy, Z + off, ldz, std::min(n - off, nr * GD_TR), upper);
+            c.check_launch();
+        }
+        return;
+    }
     constexpr int TC = Sc<T>::W == 1 ? 64 : 32;
     const long rt = (n + 63) / 64;
     for (long r0 = 0; r0 < rt; r0 += 65535) {
@@ -984,6 +1007,16 @@ struct SolveOut {
     double correction_norm = 0.0;
     std::vector<double> hist;
 };
+
+// CholQR refresh: a second pass when the 1-norm condition estimate of the first
+// pass's factor exceeds this (default 20; ROMDOT_REFRESH_KAPPA)
+inline double refresh_kappa() {
+    static const double k = [] {
+        const char* e = std::getenv("ROMDOT_REFRESH_KAPPA");
+        return e ? std::atof(e) : 20.0;
+    }();
+    return k;
+}
 
 template <class T> struct Workspace {
     DevBuf r, w, p, s, y, tmp, vec, krb, gk, gwork;
@@ -1790,7 +1823,8 @@ template <class T> struct DevBasis : BasisBase {
             c.check_launch();
             std::swap(Rd.p, Rd2.p);
             std::swap(Rd.bytes, Rd2.bytes);
-            if (ci.kappa1 <= 20.0) break;
+            VLOG(1, "refresh pass %d: r %ld, kappa1(S) %.3e", pass, r, ci.kappa1);
+            if (ci.kappa1 <= refresh_kappa()) break;
             ++stats_second_pass;
         }
         CK(cudaMemcpyAsync(Rh.data(), Rd.p, sizeof(T) * r * r, cudaMemcpyDeviceToHost, c.s));
