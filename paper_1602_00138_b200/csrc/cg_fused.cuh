@@ -50,6 +50,7 @@ struct FusedLayout {
     int TR, S, RBN, L, LI, PF;  // PF: phase-1 L2 prefetch distance (steps)
     int poll_ns;                // back-off of the stencil warps' step-counter polls
     int rel_ns;                 // back-off of the release warps' wait for the update warp
+    int ahead;                  // stencil polls look past the step they need
     // LI: item-order lead of phase 1 (>= L, slack for the stencil warps)
     int dbg;  // timing experiments only: bit 0 skips the step waits, bit 1 the stencil loads, bit 2 the phase-2 K reload
     uint32_t tile_bytes, x_bytes, stage_bytes;
@@ -469,21 +470,24 @@ __global__ void __launch_bounds__(FU_THREADS, 1)
             const long row_first = t * TR + lane;
             StCoef cf = stencil_coef(op, row_first < n ? row_first : n - 1);
             long long ta = pr.now();
-            // the step counters ok+1 .. shi, one per lane, polled in parallel (one
+            // the step counters from ok+1 on, one per lane, polled in parallel (one
             // L2 round trip per check instead of one per step); acquire loads so
-            // the r' halo loads below are ordered after the releases they observe
+            // the r' halo loads below are ordered after the releases they observe.
+            // With ROMDOT_FUSED_AHEAD (default) a poll also looks past shi and
+            // advances ok over every consecutive complete step, so later tiles of
+            // this warp usually find their steps covered without another poll.
             while (ok < shi && !(FL.dbg & 1)) {
-                const long nq = shi - ok < 32 ? shi - ok : 32;
+                const long lim = FL.ahead ? nsteps - 1 : shi;
+                const int nq = (int)(lim - ok < 32 ? lim - ok : 32);
                 bool good = true;
                 if (lane < nq) {
                     const long sq = ok + 1 + lane;
                     const long tiles = ntile - sq * Gd < Gd ? ntile - sq * Gd : Gd;
                     good = ld_acquire_u32(stepcnt + sq) >= (unsigned)tiles;  // one release per CTA and step
                 }
-                if (__all_sync(0xffffffffu, good))
-                    ok += nq;
-                else
-                    __nanosleep(FL.poll_ns);
+                const unsigned bad = __ballot_sync(0xffffffffu, !good);
+                ok += bad ? __ffs(bad) - 1 : nq;
+                if (ok < shi) __nanosleep(FL.poll_ns);
             }
             pr.add(0, ta);
             const int slot = FU_NSW * (k & 1) + sw;

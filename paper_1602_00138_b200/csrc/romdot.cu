@@ -576,6 +576,11 @@ void cg_fused_inst(Ctx& c, const OpDev& op, const T* Krb, int C, T* w, T* r, T* 
         return e ? std::max(0, std::atoi(e)) : 256;
     }();
     L.rel_ns = rel_ns;
+    static const int ahead = [] {
+        const char* e = std::getenv("ROMDOT_FUSED_AHEAD");
+        return e ? std::atoi(e) : 1;
+    }();
+    L.ahead = ahead;
     static const int dbg = [] {
         const char* e = std::getenv("ROMDOT_FUSED_DBG");
         return e ? std::atoi(e) : 0;
