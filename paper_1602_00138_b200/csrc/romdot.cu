@@ -1686,6 +1686,61 @@ template <class T> struct DevBasis : BasisBase {
     }
     T& Rat(long i, long j) { return R[i + j * capcols]; }
 
+    // W = V R^-1 is only read by the refresh and the deferred X assembly, so the
+    // appends of a system leave their W columns unformed (one N pass over W per
+    // append saved) and materialize_W() forms them as a block:
+    //   W_new = (V_new - W_old R_on) R_nn^-1
+    // (one tall GEMM over W_old, then forward substitution inside the new block).
+    // wvalid = leading columns of W that are formed. ROMDOT_LAZY_W=0 forms each
+    // column at its append as before.
+    long wvalid = 0;
+    DevBuf wblk, wrho;
+    static bool lazy_w() {
+        static const bool on = [] {
+            const char* e = std::getenv("ROMDOT_LAZY_W");
+            return e ? std::atoi(e) != 0 : true;
+        }();
+        return on;
+    }
+    void materialize_W() {
+        if (raw_only || wvalid >= cols) return;
+        Ctx& c = *ctx;
+        constexpr int W = Sc<T>::W;
+        const long m0 = wvalid, m = cols - m0;
+        T* Wn = Wp() + (size_t)m0 * n;
+        CK(cudaMemcpy2DAsync(Wn, sizeof(T) * n, Vp() + (size_t)m0 * n, sizeof(T) * n, sizeof(T) * n, m,
+                             cudaMemcpyDeviceToDevice, c.s));
+        // R_on (m0 x m, ld m0) and R_nn (m x m, ld m) to the device, 1 / R_jj^2 as rho^2
+        std::vector<T> h((size_t)m0 * m + (size_t)m * m, Sc<T>::zero());
+        std::vector<double> r2(m);
+        for (long j = 0; j < m; ++j) {
+            for (long i = 0; i < m0; ++i) h[i + j * m0] = Rat(i, m0 + j);
+            for (long i = 0; i < j; ++i) h[(size_t)m0 * m + i + j * m] = Rat(m0 + i, m0 + j);
+            r2[j] = Sc<T>::abs2(Rat(m0 + j, m0 + j));
+        }
+        wblk.ensure(sizeof(T) * h.size());
+        wrho.ensure(sizeof(double) * m);
+        CK(cudaMemcpyAsync(wblk.p, h.data(), sizeof(T) * h.size(), cudaMemcpyHostToDevice, c.s));
+        CK(cudaMemcpyAsync(wrho.p, r2.data(), sizeof(double) * m, cudaMemcpyHostToDevice, c.s));
+        const T* Ron = wblk.template as<T>();
+        const T* Rnn = Ron + (size_t)m0 * m;
+        if (m0 > 0) gemm<T, true>(c, Wp(), n, m0, Ron, m, Wn, n, Wn, n, n, false);
+        T* vp = padded(vpad);
+        for (long j = 0; j < m; ++j) {
+            T* wj = Wn + (size_t)j * n;
+            if (j > 0) {
+                CK(cudaMemcpyAsync(vp, wj, sizeof(T) * n, cudaMemcpyDeviceToDevice, c.s));
+                global_N<T>(c, Wn, n, j, vp, vp, n, (const double*)(Rnn + (size_t)j * m));
+                launch_scale<T>(c, vp, wj, n, wrho.template as<double>() + j, 0);
+            } else {
+                launch_scale<T>(c, wj, wj, n, wrho.template as<double>(), 0);
+            }
+        }
+        c.sync();  // host copies above are stack-owned
+        wvalid = cols;
+        (void)W;
+    }
+
     void drop_column(long cidx) {
         // V columns shift left; per-RHS indices remapped (SURVEY §5 latent bug fixed)
         for (long k = cidx; k + 1 < cols; ++k)
@@ -1750,12 +1805,16 @@ template <class T> struct DevBasis : BasisBase {
         if (may_drop && rho <= 1e-12 * zn) return false;
         launch_scale<T>(c, qp, Kp() + (size_t)j * n, n, nrm, 0);  // K_img(:, j) = q / rho
         T* wj = Wp() + (size_t)j * n;
-        if (j > 0) {
+        if (lazy_w()) {
+            // W(:, j) formed later by materialize_W (needs W(:, :j) formed only then)
+        } else if (j > 0) {  // W(:, :j) formed: wvalid == j on this path
             CK(cudaMemcpyAsync(vp, vj, sizeof(T) * n, cudaMemcpyDeviceToDevice, c.s));
             global_N<T>(c, Wp(), n, j, vp, vp, n, coef);             // W(:, j) = (v_j - W c) / rho
             launch_scale<T>(c, vp, wj, n, nrm, 0);
+            wvalid = j + 1;
         } else {
             launch_scale<T>(c, vj, wj, n, nrm, 0);
+            wvalid = 1;
         }
         for (long i = 0; i < j; ++i) {
             if constexpr (W == 1)
@@ -1777,11 +1836,15 @@ template <class T> struct DevBasis : BasisBase {
     // sequential path (which drops columns like the reference).
     void refresh(DevOp& op) {
         eig_ready_for = -1;
-        if (factored && cols > 0 && refresh_block(op)) {
-            ++stats_block_refresh;
-            return;
+        if (factored && cols > 0) {
+            materialize_W();
+            if (refresh_block(op)) {
+                ++stats_block_refresh;
+                return;
+            }
         }
         ++stats_seq_refresh;
+        wvalid = 0;  // every column is refactored: W is formed again from V
         long j = 0;
         while (j < cols) {
             if (factor_column(op, j, j >= ku)) {
@@ -1791,6 +1854,7 @@ template <class T> struct DevBasis : BasisBase {
             }
         }
         factored = true;
+        materialize_W();
     }
 
     bool refresh_block(DevOp& op) {
@@ -2153,6 +2217,7 @@ void process_system(DevBasis<T>& gb, DevOp& op, long nrhs, const long* bidx, con
         DB::grow_to(Cpk, sizeof(T) * rf * nrhs);
         CK(cudaMemcpy2DAsync(Cpk.p, sizeof(T) * rf, Coef.p, sizeof(T) * capc, sizeof(T) * rf, nrhs,
                              cudaMemcpyDeviceToDevice, c.s));
+        gb.materialize_W();
         gemm<T, true>(c, gb.Wp(), n, rf, Cpk.template as<T>(), nrhs, Xdev, n, Xdev, n, n, false);
     }
     c.sync();
@@ -3060,7 +3125,10 @@ long rd_basis_eig_block(rd_basis* b) {
 }
 void* rd_basis_device_ptr(rd_basis* b, int which) {
     void* p = nullptr;
-    BASIS_DISPATCH(b, p = which == 0 ? (void*)B.Vp() : which == 1 ? (void*)B.Kp() : (void*)B.Wp());
+    BASIS_DISPATCH(b, {
+        if (which >= 2) B.materialize_W();
+        p = which == 0 ? (void*)B.Vp() : which == 1 ? (void*)B.Kp() : (void*)B.Wp();
+    });
     return p;
 }
 int rd_basis_get(rd_basis* b, int which, void* out) {
@@ -3073,6 +3141,7 @@ int rd_basis_get(rd_basis* b, int which, void* out) {
                 for (long j = 0; j < B.cols; ++j)
                     for (long i = 0; i < B.cols; ++i) o[i + j * B.cols] = i <= j ? B.Rat(i, j) : Sc<T>::zero();
             } else {
+                if (which == 3) B.materialize_W();
                 const T* src = which == 0 ? B.Vp() : which == 1 ? B.Kp() : B.Wp();
                 CK(cudaMemcpyAsync(out, src, sizeof(T) * B.n * B.cols, cudaMemcpyDeviceToHost, b->ctx->c.s));
                 b->ctx->c.sync();
@@ -3132,6 +3201,7 @@ int rd_basis_solve_projected(rd_basis* b, const void* rhs, void* x, void* coords
                 xt.ensure(sizeof(T) * n);
                 xp = xt.p;
             }
+            B.materialize_W();
             ts_N_launch<T>(cx, B.Wp(), n, r, zero.template as<T>(), (T*)xp, n, w.template as<double>(), -1.0);
             xs.finish();
             if (coords) {
