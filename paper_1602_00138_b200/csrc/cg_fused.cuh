@@ -289,17 +289,32 @@ __global__ void __launch_bounds__(FU_THREADS, 1)
         // producer warp is already issuing its first TMA loads meanwhile.
         constexpr int NW = FU_THREADS / 32 - 1;
         const int q = wid < FU_CONS / 32 ? wid : wid - 1;
-        for (int t = q; t < C; t += NW) {
-            const T* gc = G + (size_t)t * C;
-            T acc = Sc<T>::zero();
-            for (int j = lane; j < C; j += 32) acc = Sc<T>::fma(__ldg(gc + j), c1s[j], acc);
-            if constexpr (W == 1) {
-                acc = warp_sum(acc);
-            } else {
-                ((cplx&)acc).x = warp_sum(((cplx&)acc).x);
-                ((cplx&)acc).y = warp_sum(((cplx&)acc).y);
+        // three rows per pass with all their loads in flight (C <= 128: <= 4 per lane and row)
+        for (int t0 = q; t0 < C; t0 += 3 * NW) {
+            T acc[3] = {Sc<T>::zero(), Sc<T>::zero(), Sc<T>::zero()};
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int j = lane + 32 * u;
+                if (j < C) {
+                    const T cj = c1s[j];
+#pragma unroll
+                    for (int v = 0; v < 3; ++v) {
+                        const int t = t0 + v * NW;
+                        if (t < C) acc[v] = Sc<T>::fma(__ldg(G + (size_t)t * C + j), cj, acc[v]);
+                    }
+                }
             }
-            if (lane == 0) cw[t] = Sc<T>::sub(Sc<T>::scale(c1s[t], 2.0), acc);
+#pragma unroll
+            for (int v = 0; v < 3; ++v) {
+                const int t = t0 + v * NW;
+                if constexpr (W == 1) {
+                    acc[v] = warp_sum(acc[v]);
+                } else {
+                    ((cplx&)acc[v]).x = warp_sum(((cplx&)acc[v]).x);
+                    ((cplx&)acc[v]).y = warp_sum(((cplx&)acc[v]).y);
+                }
+                if (lane == 0 && t < C) cw[t] = Sc<T>::sub(Sc<T>::scale(c1s[t], 2.0), acc[v]);
+            }
         }
         // named barrier 1 over every warp but the producer
         asm volatile("bar.sync 1, %0;" ::"r"(FU_THREADS - 32) : "memory");
