@@ -200,6 +200,78 @@ __global__ void __launch_bounds__(256) stencil_kernel(OpDev op, const T* __restr
     zmarch<T>(op, xc, i, j, k0, k1, [&](long p, const T&, const T& v) { yc[p] = v; });
 }
 
+// Multi-column apply, NC columns per thread: the node's coefficients are loaded
+// once per plane and applied to all NC columns (the one-column kernel above
+// re-reads them per column: 0.36-0.55 of HBM peak at 8 columns in the C5 sweep).
+// Same loads and summation order per column as zmarch.
+template <class T, int NC>
+__global__ void __launch_bounds__(256) stencil_kernel_mc(OpDev op, const T* __restrict__ x, long ldx,
+                                                         const int* __restrict__ xcol, T* __restrict__ y, long ldy,
+                                                         int ncols, int kz) {
+    const int nkc = (op.N2 + kz - 1) / kz;
+    const int cg = blockIdx.z / nkc;
+    const int kc = blockIdx.z - cg * nkc;
+    const int i = blockIdx.x * 32 + (threadIdx.x & 31);
+    const int j = blockIdx.y * 8 + (threadIdx.x >> 5);
+    const int c0 = cg * NC;
+    if (c0 >= ncols || i >= op.N0 || j >= op.N1) return;
+    const int k0 = kc * kz, k1 = min(op.N2, k0 + kz);
+    const long n = op.n;
+    const long s1 = op.N0, s2 = (long)op.N0 * op.N1;
+    const double* __restrict__ Fd = op.F;
+    const bool three = op.d == 3;
+    const T* xs[NC];
+    T* ys[NC];
+#pragma unroll
+    for (int q = 0; q < NC; ++q) {
+        const int c = min(c0 + q, ncols - 1);
+        xs[q] = x + (size_t)(xcol ? xcol[c] : c) * ldx;
+        ys[q] = y + (size_t)(c0 + q) * ldy;
+    }
+    long p = i + s1 * (j + (long)op.N1 * k0);
+    T xm[NC], xc[NC];
+    double fzm = (three && k0 > 0) ? __ldg(Fd + 3 * n + p - s2) : 0.0;
+#pragma unroll
+    for (int q = 0; q < NC; ++q) {
+        xm[q] = (three && k0 > 0) ? xs[q][p - s2] : Sc<T>::zero();
+        xc[q] = xs[q][p];
+    }
+    const bool hx_m = i > 0, hx_p = i < op.N0 - 1, hy_m = j > 0, hy_p = j < op.N1 - 1;
+    for (int k = k0; k < k1; ++k) {
+        const bool hz_p = three && k < op.N2 - 1;
+        const double fzp = hz_p ? __ldg(Fd + 3 * n + p) : 0.0;
+        const double dg = __ldg(Fd + p);
+        const double fxm = hx_m ? __ldg(Fd + n + p - 1) : 0.0;
+        const double fxp = hx_p ? __ldg(Fd + n + p) : 0.0;
+        const double fym = hy_m ? __ldg(Fd + 2 * n + p - s1) : 0.0;
+        const double fyp = hy_p ? __ldg(Fd + 2 * n + p) : 0.0;
+#pragma unroll
+        for (int q = 0; q < NC; ++q) {
+            const T* xq = xs[q];
+            const T xp = hz_p ? xq[p + s2] : Sc<T>::zero();
+            const T xim = hx_m ? xq[p - 1] : Sc<T>::zero();
+            const T xip = hx_p ? xq[p + 1] : Sc<T>::zero();
+            const T xjm = hy_m ? xq[p - s1] : Sc<T>::zero();
+            const T xjp = hy_p ? xq[p + s1] : Sc<T>::zero();
+            T acc = Sc<T>::zero();
+            acc = axpy_real(fxm, xim, acc);
+            acc = axpy_real(fxp, xip, acc);
+            acc = axpy_real(fym, xjm, acc);
+            acc = axpy_real(fyp, xjp, acc);
+            if (three) {
+                acc = axpy_real(fzm, xm[q], acc);
+                acc = axpy_real(fzp, xp, acc);
+            }
+            const T yv = Sc<T>::sub(diag_apply<T>(dg, op.shift, xc[q]), acc);
+            if (c0 + q < ncols) ys[q][p] = yv;
+            xm[q] = xc[q];
+            xc[q] = xp;
+        }
+        fzm = fzp;
+        p += s2;
+    }
+}
+
 // ------------------------------------------------------------ CG state ---
 // Scalars of one recycled CG / COCG solve (Chronopoulos-Gear recurrence).
 struct CGState {
