@@ -523,6 +523,20 @@ __global__ void assemble_space_gram(const T* __restrict__ G00, int ku, const T* 
     }
 }
 
+// One-pass CGS coefficient against the eigen block (Gram-corrected, as the
+// inner iteration's): Co = 2 C1 - G00 C1, G00 = Kb^T Kb (ku x ku), C1 = Kb^T Kt
+// (ku x m, ld ku); Kt - Kb Co equals the two-pass CGS in exact arithmetic.
+template <class T>
+__global__ void onepass_coef(const T* __restrict__ G00, int ku, const T* __restrict__ C1, int m, T* __restrict__ Co) {
+    const long tot = (long)ku * m;
+    for (long e = blockIdx.x * (long)blockDim.x + threadIdx.x; e < tot; e += (long)gridDim.x * blockDim.x) {
+        const int i = (int)(e % ku), t = (int)(e / ku);
+        T acc = Sc<T>::zero();
+        for (int k = 0; k < ku; ++k) acc = Sc<T>::fma(G00[(size_t)k * ku + i], C1[(size_t)t * ku + k], acc);
+        Co[e] = Sc<T>::sub(Sc<T>::scale(C1[e], 2.0), acc);
+    }
+}
+
 // R[idx[c] + c*ld] = val[c] (unit right-hand sides of the layout)
 template <class T>
 __global__ void scatter_unit_rhs(T* R, long ld, const long* __restrict__ idx, const double* __restrict__ val, int m) {

@@ -2019,17 +2019,34 @@ template <class T> struct DevBasis : BasisBase {
             T* C1 = (T*)c.sc(4);
             T* C2 = (T*)c.sc(5);
             if (ku * m * W > 8192) throw ConfigError("recycle space: trailing block too wide");
-            gram<T, false>(c, Kb, n, ku, Kt, n, m, n, C1, false, gwork);
-            dbg_sum(" frs C1", C1, ku * m, c.s);
-            gemm<T, true>(c, Kb, n, ku, C1, m, Kt, n, Kt, n, n, false);
-            dbg_sum(" frs Kt1", Kt, n * m, c.s);
-            gram<T, false>(c, Kb, n, ku, Kt, n, m, n, C2, false, gwork);
-            dbg_sum(" frs C2", C2, ku * m, c.s);
-            gemm<T, true>(c, Kb, n, ku, C2, m, Kt, n, Kt, n, n, false);
-            dbg_sum(" frs Kt2", Kt, n * m, c.s);
-            launch_addsub(c, (int)(ku * m * W), (double*)C1, (double*)C2, 1.0, (double*)C1);
-            gemm<T, true>(c, Ub, n, ku, C1, m, Ut, n, Ut, n, n, false);
-            dbg_sum(" frs Ut", Ut, n * m, c.s);
+            static const int onepass = [] {
+                // default on: C4 per-RHS spaces 420 -> 300 ms per late system; GPU suite and
+                // the C4 partial lockstep (profiles/r01g_rhs_onepass.txt) unchanged
+                const char* e = std::getenv("ROMDOT_RHS_ONEPASS");
+                return e ? std::atoi(e) : 1;
+            }();
+            if (onepass) {
+                // one T and one N pass over the eigen block (Gram-corrected coefficient,
+                // G00 = Kb^T Kb formed with the eigen block) instead of two each
+                gram<T, false>(c, Kb, n, ku, Kt, n, m, n, C1, false, gwork);
+                onepass_coef<T><<<c.grid_for(ku * m, 256, 1), 256, 0, c.s>>>(G00.template as<T>(), (int)ku, C1,
+                                                                               (int)m, C2);
+                c.check_launch();
+                gemm<T, true>(c, Kb, n, ku, C2, m, Kt, n, Kt, n, n, false);
+                gemm<T, true>(c, Ub, n, ku, C2, m, Ut, n, Ut, n, n, false);
+            } else {
+                gram<T, false>(c, Kb, n, ku, Kt, n, m, n, C1, false, gwork);
+                dbg_sum(" frs C1", C1, ku * m, c.s);
+                gemm<T, true>(c, Kb, n, ku, C1, m, Kt, n, Kt, n, n, false);
+                dbg_sum(" frs Kt1", Kt, n * m, c.s);
+                gram<T, false>(c, Kb, n, ku, Kt, n, m, n, C2, false, gwork);
+                dbg_sum(" frs C2", C2, ku * m, c.s);
+                gemm<T, true>(c, Kb, n, ku, C2, m, Kt, n, Kt, n, n, false);
+                dbg_sum(" frs Kt2", Kt, n * m, c.s);
+                launch_addsub(c, (int)(ku * m * W), (double*)C1, (double*)C2, 1.0, (double*)C1);
+                gemm<T, true>(c, Ub, n, ku, C1, m, Ut, n, Ut, n, n, false);
+                dbg_sum(" frs Ut", Ut, n * m, c.s);
+            }
         }
         double* coef = c.sc(6);
         double* nrm = c.sc(7);
