@@ -107,7 +107,10 @@ int rd_basis_factored(rd_basis* b);
 /* which: 0 V, 1 K_img, 2 R (cols x cols), 3 W = V R^-1. Host output.
  * which != 0 before the first refresh: status 2 (no image factor yet). */
 int rd_basis_get(rd_basis* b, int which, void* out);
-/* Device pointer of V / K_img / W (valid until the next call that grows the basis). */
+/* Device pointer of V / K_img / W (valid until the next call that grows the basis).
+ * W = V R^-1 is formed lazily: the columns appended since the last refresh / X
+ * assembly are formed by this call (which >= 2) and by rd_basis_get(which = 3);
+ * a W pointer taken before later appends does not see their columns formed. */
 void* rd_basis_device_ptr(rd_basis* b, int which);
 int rd_basis_markers(rd_basis* b, uint8_t* out);
 long rd_basis_space(rd_basis* b, long j, int* out);
