@@ -50,7 +50,8 @@ double rd_ctx_elapsed_ms(rd_ctx* ctx);
 long rd_ctx_launches(rd_ctx* ctx);
 /* Sampled per-kernel-class device timing of the inner iteration (CUDA events on
  * the ctx stream, first iteration of each launch batch). enable resets the counters.
- * cls: 0 cg_stencil_dots, 1 ts_T, 2 ts_NT, 3 cg_update. bytes = algorithmic bytes. */
+ * cls: 0 cg_stencil_dots, 1 ts_T, 2 ts_NT, 3 cg_update, 4 cg_fused (one event
+ * pair around a batch of back-to-back launches). bytes = algorithmic bytes. */
 void rd_ctx_profile(rd_ctx* ctx, int enable);
 int rd_ctx_prof_get(rd_ctx* ctx, int cls, double* ms, double* bytes, long* samples);
 /* Raw stream handle (cudaStream_t) for interop. */
@@ -110,8 +111,17 @@ int rd_basis_get(rd_basis* b, int which, void* out);
 /* Device pointer of V / K_img / W (valid until the next call that grows the basis).
  * W = V R^-1 is formed lazily: the columns appended since the last refresh / X
  * assembly are formed by this call (which >= 2) and by rd_basis_get(which = 3);
- * a W pointer taken before later appends does not see their columns formed. */
+ * a W pointer taken before later appends does not see their columns formed.
+ * Returns NULL (rd_last_error set) for W before the first refresh or after
+ * rd_basis_compress, and on any CUDA failure while forming W.               */
 void* rd_basis_device_ptr(rd_basis* b, int which);
+/* Checkpoint hook (test / baseline instrumentation; no reference counterpart):
+ * rd_process_system calls fn(user, system_index, j) before RHS j, with the
+ * stream idle, so fn may read the state the reference's loop body
+ * (src/basis.cpp:168-205) starts RHS j from -- V, K_img, R (rd_basis_get) and
+ * U_j (rd_basis_space). A nonzero return aborts the system with status 3.
+ * fn = NULL removes the hook.                                                */
+int rd_basis_set_rhs_hook(rd_basis* b, int (*fn)(void* user, int system_index, long rhs), void* user);
 int rd_basis_markers(rd_basis* b, uint8_t* out);
 long rd_basis_space(rd_basis* b, long j, int* out);
 /* GlobalBasis::refresh (src/basis.cpp:37-76) for the operator's current fields. */
@@ -229,6 +239,9 @@ int rd_bench_projection(rd_ctx* ctx, int dtype, long n, long c, int iters, doubl
 int rd_bench_stencil(rd_op* op, int dtype, long ncols, int iters, double* ms_out);
 /* Mean device ms of the tall Gram X^T X (sym) or X^T Y on seeded n x a / n x b data. */
 int rd_bench_gram(rd_ctx* ctx, int dtype, long n, long a, long b, int sym, int iters, double* ms_out);
+/* Mean device ms of the tall GEMM Z = X M (n x a by a x b; upper: M upper
+ * triangular, the refresh's S^-1 products) on seeded data.                 */
+int rd_bench_gemm(rd_ctx* ctx, int dtype, long n, long a, long b, int upper, int iters, double* ms_out);
 
 #ifdef __cplusplus
 }

@@ -82,6 +82,8 @@ def lib():
         L.orc_thin_qr.argtypes = [C.c_int, C.c_long, C.c_long, vp, vp, vp]
         L.orc_qrcp.argtypes = [C.c_int, C.c_long, C.c_long, vp, C.c_double, C.c_int, c_long_p, vp, vp, vp]
         L.orc_normal_stream.argtypes = [C.c_uint64, C.c_long, vp]
+        L.orc_replay_rhs.argtypes = [vp, C.c_long, vp, vp, vp, vp, C.c_long, C.c_long, C.c_double, C.c_double,
+                                     C.c_long, C.c_long, C.c_int, vp, vp, vp]
         _LIB = L
     return _LIB
 
@@ -434,3 +436,40 @@ def normal_stream(seed: int, count: int) -> np.ndarray:
     out = np.zeros(count)
     lib().orc_normal_stream(seed, count, _p(out))
     return out
+
+
+@dataclass
+class ReplayResult:
+    """One process_system RHS replayed from a recorded state (replay_rhs)."""
+    init_relres: float
+    iterations: int
+    appended: bool
+    rho_over_znorm: float
+    converged: bool
+    room: bool
+    X: np.ndarray
+    y: Optional[np.ndarray]
+    times: dict
+
+
+def replay_rhs(op: Operator, V, K_img, R, space, bidx: int, bval: float, tol: float, cap: int = 0, maxit: int = 0,
+               method=CG, want_y: bool = False) -> ReplayResult:
+    """The loop body of process_system (basis.cpp:168-205) for one RHS, run on
+    a recorded basis state (V, K_img: n x r Fortran views, R: r x r) without
+    copying it: global check, recycle space from_raw(V[:, space], A V[:, space]),
+    recycled CG/COCG at 0.25 tol, X_j = correction + solve_projected(b_j), and
+    the append decision (not applied). Host-core wall times per phase."""
+    n, r = V.shape
+    for a in (V, K_img):
+        if a.dtype != op.dtype or not a.flags.f_contiguous or a.shape != (n, r):
+            raise ValueError("replay_rhs: V / K_img must be Fortran (n, r) arrays of the operator dtype")
+    Rf = _f(R, op.dtype)
+    sp = np.ascontiguousarray(space, dtype=np.int32)
+    X = np.zeros(n, dtype=op.dtype)
+    y = np.zeros(n, dtype=op.dtype) if want_y else None
+    info = np.zeros(12)
+    _check(lib().orc_replay_rhs(op.h, r, _p(V), _p(K_img), _p(Rf), _p(sp), sp.size, int(bidx), float(bval), tol,
+                                maxit, cap, method, _p(X), _p(y) if y is not None else None, _p(info)))
+    keys = ["check", "space", "solve", "projected", "append", "total"]
+    return ReplayResult(float(info[0]), int(info[1]), bool(info[2]), float(info[3]), bool(info[4]), bool(info[11]),
+                        X, y, dict(zip(keys, map(float, info[5:11]))))

@@ -32,6 +32,7 @@
 // (RRQR) compression at 1e-10 (acceptance.cpp:368-383 uses an SVD).
 // ============================================================================
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <complex>
 #include <cstdint>
@@ -301,7 +302,15 @@ struct BandChol {
 
 // ---------------------------------------------------------- dense kernels ---
 // y -= K c ; c = K^op w  with op = T (bilinear) or H (Hermitian)
-template <class T> void gemv_op(const Mat<T>& K, long cols, const T* w, T* c, bool herm) {
+// Read-only column-major view of caller-owned memory (replay of a recorded
+// device state without copying its multi-GB V / K_img; same col() interface).
+template <class T> struct View {
+    long r = 0, c = 0;
+    const T* p = nullptr;
+    const T* col(long j) const { return p + j * r; }
+};
+
+template <class M, class T> void gemv_op(const M& K, long cols, const T* w, T* c, bool herm) {
     if (cols >= 4) {
 #pragma omp parallel for schedule(dynamic, 1)
         for (long j = 0; j < cols; ++j) c[j] = herm ? dotH_seq(K.r, K.col(j), w) : dotT_seq(K.r, K.col(j), w);
@@ -309,7 +318,7 @@ template <class T> void gemv_op(const Mat<T>& K, long cols, const T* w, T* c, bo
         for (long j = 0; j < cols; ++j) c[j] = herm ? dotH(K.r, K.col(j), w) : dotT(K.r, K.col(j), w);
     }
 }
-template <class T> void sub_Kc(const Mat<T>& K, long cols, const T* c, T* y) {
+template <class M, class T> void sub_Kc(const M& K, long cols, const T* c, T* y) {
     const long n = K.r;
     const long nb = (n + kChunk - 1) / kChunk;
 #pragma omp parallel for schedule(static) if (nb >= 4)
@@ -1148,6 +1157,110 @@ void process_system(GlobalBasis<T>& gb, const LinOp<T>& A, long nrhs, const long
     }
 }
 
+// One RHS of process_system (the loop body of basis.cpp:168-205) replayed
+// from a recorded basis state: V, K_img (n x r) and R (r x r) as read from the
+// device build at the start of RHS j, plus U_j's column indices. Memory is
+// borrowed (no copy of the multi-GB V / K_img). A_i U_j is recomputed by the
+// operator (bitwise equal to the reference's cached K~ columns, which are
+// A_i v computed by the same apply). The append is decided but not applied
+// (the recorded state is not mutated): CGS2 of z = A_i y_m against K_img and
+// the drop rule rho <= 1e-12 ||z|| (basis.cpp:78-103).
+// info[0..11]: init_relres, iterations, appended, rho/||z||, converged,
+//   t_check, t_space, t_solve, t_projected, t_append, t_total (s), room.
+template <class T>
+void replay_rhs(const LinOp<T>& A, long n, long r, const T* Vp, const T* Kp, const T* Rp, const int* space, long cj,
+                long bidx, double bval, double tol, long maxit, long cap, int method, T* Xj, T* yout,
+                double* info) {
+    using clk = std::chrono::steady_clock;
+    auto secs = [](clk::time_point a, clk::time_point b) { return std::chrono::duration<double>(b - a).count(); };
+    if (bidx < 0 || bidx >= n) throw ConfigError("replay: rhs index out of range");
+    if (maxit <= 0) maxit = 2 * n;
+    const View<T> V{n, r, Vp}, K{n, r, Kp};
+    const auto t0 = clk::now();
+    std::vector<T> b(n, T(0)), rj(n);
+    b[bidx] = T(bval);
+    const double bnorm = nrm2(n, b.data());
+    // global check (basis.cpp:171-177): w = K_img^H b, r_j = b - K_img w
+    std::vector<T> w(r);
+    gemv_op(K, r, b.data(), w.data(), true);
+    rj = b;
+    sub_Kc(K, r, w.data(), rj.data());
+    const double init_relres = nrm2(n, rj.data()) / bnorm;
+    // solve_projected(b) (basis.cpp:105-112): c = R^-1 K_img^H b, x = V c
+    auto solve_projected = [&](std::vector<T>& x) {
+        std::vector<T> cc(r);
+        gemv_op(K, r, b.data(), cc.data(), true);
+        for (long i = r - 1; i >= 0; --i) {
+            T acc = cc[i];
+            for (long k = i + 1; k < r; ++k) acc -= Rp[i + k * r] * cc[k];
+            cc[i] = acc / Rp[i + i * r];
+        }
+        x.assign(n, T(0));
+        const long nb = (n + kChunk - 1) / kChunk;
+#pragma omp parallel for schedule(static) if (nb >= 4)
+        for (long bk = 0; bk < nb; ++bk) {
+            const long i0 = bk * kChunk, i1 = std::min(n, i0 + kChunk);
+            for (long j = 0; j < r; ++j) {
+                const T cv = cc[j];
+                const T* vc = V.col(j);
+                for (long i = i0; i < i1; ++i) x[i] += vc[i] * cv;
+            }
+        }
+    };
+    const auto t1 = clk::now();
+    double t_space = 0, t_solve = 0, t_proj = 0, t_app = 0;
+    int its = 0, appended = 0, converged = 1, room = 0;
+    double rho_rel = 0.0;
+    std::vector<T> xp;
+    if (init_relres <= tol) {
+        const auto a = clk::now();
+        solve_projected(xp);
+        std::memcpy(Xj, xp.data(), sizeof(T) * n);
+        t_proj = secs(a, clk::now());
+        if (yout) std::fill(yout, yout + n, T(0));
+    } else {
+        auto a = clk::now();
+        Mat<T> W(n, cj), AW(n, cj);
+        for (long t = 0; t < cj; ++t) {
+            if (space[t] < 0 || space[t] >= r) throw ConfigError("replay: space index out of range");
+            std::memcpy(W.col(t), V.col(space[t]), sizeof(T) * n);
+            A.apply(W.col(t), AW.col(t));
+        }
+        const RecycleSpace<T> rs = RecycleSpace<T>::from_raw(W, AW);
+        W = Mat<T>();
+        AW = Mat<T>();
+        auto b2 = clk::now();
+        t_space = secs(a, b2);
+        auto solved = inner_solve<T>(method, A, rs, rj.data(), kInnerSafety * tol, maxit, bnorm);
+        a = clk::now();
+        t_solve = secs(b2, a);
+        converged = solved.report.converged ? 1 : 0;
+        its = solved.report.iterations;
+        solve_projected(xp);
+        for (long i = 0; i < n; ++i) Xj[i] = solved.correction[i] + xp[i];
+        b2 = clk::now();
+        t_proj = secs(a, b2);
+        if (yout) std::memcpy(yout, solved.new_direction.data(), sizeof(T) * n);
+        room = (cap <= 0 || r < cap) ? 1 : 0;
+        if (room) {  // GlobalBasis::append decision (basis.cpp:78-86)
+            const T* z = solved.image.data();
+            std::vector<T> c1(r), c2(r), q(z, z + n);
+            gemv_op(K, r, q.data(), c1.data(), true);
+            sub_Kc(K, r, c1.data(), q.data());
+            gemv_op(K, r, q.data(), c2.data(), true);
+            sub_Kc(K, r, c2.data(), q.data());
+            const double rho = nrm2(n, q.data()), zn = nrm2(n, z);
+            rho_rel = zn > 0 ? rho / zn : 0.0;
+            appended = rho > 1e-12 * zn ? 1 : 0;
+        }
+        t_app = secs(b2, clk::now());
+    }
+    const double t_total = secs(t0, clk::now());
+    const double vals[12] = {init_relres, double(its), double(appended), rho_rel, double(converged), secs(t0, t1),
+                             t_space,     t_solve,     t_proj,          t_app,   t_total,           double(room)};
+    std::memcpy(info, vals, sizeof(vals));
+}
+
 // BaselinePerRhsRecycler (basis.cpp:209-266): per-RHS raw columns
 // W_j = [U0, X0_j, own new directions]; per system K~_j = A_i W_j (the
 // reference caches A~_* W_j and adds mu W_j, :229; with a variable D field the
@@ -1645,6 +1758,24 @@ int orc_process_system(void* b, void* op, long nrhs, const long* bidx, const dou
         }
         if (inner_its) *inner_its = st.inner_iterations;
         if (appends) *appends = st.appends;
+    });
+}
+
+// Replay one RHS of process_system from a recorded state (see replay_rhs).
+// R is r x r column-major (ld r); space holds cj column indices into V.
+int orc_replay_rhs(void* op, long r, const void* V, const void* Kimg, const void* R, const int* space, long cj,
+                   long bidx, double bval, double tol, long maxit, long cap, int method, void* Xj, void* y,
+                   double* info) {
+    auto* o = static_cast<OpHandle*>(op);
+    return guard([&] {
+        if (o->dtype == 0)
+            replay_rhs<double>(o->lr, o->n, r, static_cast<const double*>(V), static_cast<const double*>(Kimg),
+                               static_cast<const double*>(R), space, cj, bidx, bval, tol, maxit, cap, method,
+                               static_cast<double*>(Xj), static_cast<double*>(y), info);
+        else
+            replay_rhs<cd>(o->lc, o->n, r, static_cast<const cd*>(V), static_cast<const cd*>(Kimg),
+                           static_cast<const cd*>(R), space, cj, bidx, bval, tol, maxit, cap, method,
+                           static_cast<cd*>(Xj), static_cast<cd*>(y), info);
     });
 }
 

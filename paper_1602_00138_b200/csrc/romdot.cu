@@ -634,11 +634,17 @@ void cg_fused_inst(Ctx& c, const OpDev& op, const T* Krb, int C, T* w, T* r, T* 
     cfg.blockDim = dim3(FU_THREADS);
     cfg.dynamicSmemBytes = L.total;
     cfg.stream = c.s;
-    cudaLaunchAttribute at[1];
-    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    at[0].val.programmaticStreamSerializationAllowed = 1;
+    // Cooperative launch: the CTAs spin on one another's step counters, so they
+    // must all be resident at once. The attribute makes the driver guarantee
+    // that (or fail the launch with cudaErrorCooperativeLaunchTooLarge, e.g.
+    // when another kernel or MPS client holds SMs) instead of hanging.
+    cudaLaunchAttribute at[2];
+    at[0].id = cudaLaunchAttributeCooperative;
+    at[0].val.cooperative = 1;
+    at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[1].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = at;
-    cfg.numAttrs = pdl ? 1 : 0;
+    cfg.numAttrs = pdl ? 2 : 1;
     CK(cudaLaunchKernelEx(&cfg, cg_fused<T, CPW>, op, Krb, C, ntile, L, w, r, p, s, y, st,
                           c.hist.template as<double>(), c.red(), cbuf, c.fstep.template as<unsigned>(), G,
                           tprof ? c.fprof.template as<unsigned long long>() : (unsigned long long*)nullptr));
@@ -1652,8 +1658,16 @@ static void smallest_eigenpairs_dev(Ctx& c, DevOp& op, long k, double tol, std::
 constexpr uint8_t kColEigenvector = 0, kColInitialSolution = 1, kColCorrection = 2;
 constexpr double kInnerSafety = 0.25;  // basis.cpp:27
 
+// Host callback run by process_system before each RHS (checkpoint-replay
+// parity and CPU-baseline sampling): the basis state it sees through
+// rd_basis_get / rd_basis_space is the state the reference's loop body
+// (basis.cpp:168-205) starts RHS j from. Nonzero return aborts the system.
+typedef int (*RhsHook)(void* user, int system_index, long rhs);
+
 struct BasisBase {
     virtual ~BasisBase() = default;
+    RhsHook hook = nullptr;
+    void* hook_user = nullptr;
 };
 
 template <class T> struct DevBasis : BasisBase {
@@ -1679,7 +1693,7 @@ template <class T> struct DevBasis : BasisBase {
     }
     long eig_ready_for = -1;                 // system tag whose eig-block factor sits in Ur/Kr
     long cmax_space = 0;
-    long stats_block_refresh = 0, stats_seq_refresh = 0, stats_second_pass = 0;
+    long stats_block_refresh = 0, stats_seq_refresh = 0, stats_second_pass = 0, stats_rhs_second_pass = 0;
 
     T* Vp() const { return V.template as<T>(); }
     T* Wp() const { return Wm.template as<T>(); }
@@ -2027,13 +2041,37 @@ template <class T> struct DevBasis : BasisBase {
             }();
             if (onepass) {
                 // one T and one N pass over the eigen block (Gram-corrected coefficient,
-                // G00 = Kb^T Kb formed with the eigen block) instead of two each
+                // G00 = Kb^T Kb formed with the eigen block) instead of two each.
+                // The Gram correction equals CGS2 only in exact arithmetic, so the
+                // Kahan-Parlett guard of the global appends applies: when a column
+                // lost more than half of ||kt||^2 to the projection (cancellation),
+                // a second plain pass (C = Kb^T Kt ; Kt -= Kb C ; Ut -= Ub C) repairs
+                // the loss of orthogonality. The column norms are one extra read of
+                // the m trailing columns each side of the projection.
+                double* nb = c.sc(10);
+                double* na = c.sc(11);
+                col_norms<T><<<c.grid_for(n, 256, 2), 256, sizeof(double) * m, c.s>>>(Kt, n, (int)m, n, c.red(), nb);
+                c.check_launch();
                 gram<T, false>(c, Kb, n, ku, Kt, n, m, n, C1, false, gwork);
                 onepass_coef<T><<<c.grid_for(ku * m, 256, 1), 256, 0, c.s>>>(G00.template as<T>(), (int)ku, C1,
                                                                                (int)m, C2);
                 c.check_launch();
                 gemm<T, true>(c, Kb, n, ku, C2, m, Kt, n, Kt, n, n, false);
                 gemm<T, true>(c, Ub, n, ku, C2, m, Ut, n, Ut, n, n, false);
+                col_norms<T><<<c.grid_for(n, 256, 2), 256, sizeof(double) * m, c.s>>>(Kt, n, (int)m, n, c.red(), na);
+                c.check_launch();
+                std::vector<double> hn(2 * m);
+                CK(cudaMemcpyAsync(hn.data(), nb, sizeof(double) * m, cudaMemcpyDeviceToHost, c.s));
+                CK(cudaMemcpyAsync(hn.data() + m, na, sizeof(double) * m, cudaMemcpyDeviceToHost, c.s));
+                c.sync();
+                bool cancel = false;
+                for (long t = 0; t < m; ++t) cancel |= hn[m + t] < 0.5 * hn[t];
+                if (cancel) {
+                    ++stats_rhs_second_pass;
+                    gram<T, false>(c, Kb, n, ku, Kt, n, m, n, C1, false, gwork);
+                    gemm<T, true>(c, Kb, n, ku, C1, m, Kt, n, Kt, n, n, false);
+                    gemm<T, true>(c, Ub, n, ku, C1, m, Ut, n, Ut, n, n, false);
+                }
             } else {
                 gram<T, false>(c, Kb, n, ku, Kt, n, m, n, C1, false, gwork);
                 dbg_sum(" frs C1", C1, ku * m, c.s);
@@ -2137,8 +2175,9 @@ void process_system(DevBasis<T>& gb, DevOp& op, long nrhs, const long* bidx, con
     };
     gb.refresh(op);
     lap(0);
-    VLOG(1, "system %d: refresh done (cols %ld, block %ld seq %ld second-pass %ld)", system_index, gb.cols,
-         gb.stats_block_refresh, gb.stats_seq_refresh, gb.stats_second_pass);
+    VLOG(1, "system %d: refresh done (cols %ld, block %ld seq %ld second-pass %ld, rhs-space second passes %ld)",
+         system_index, gb.cols, gb.stats_block_refresh, gb.stats_seq_refresh, gb.stats_second_pass,
+         gb.stats_rhs_second_pass);
     long cspace = 1;
     for (const auto& sp : gb.spaces) cspace = std::max(cspace, (long)sp.size() + 1);
     dbg_sum("refresh K", gb.Kp(), gb.n * gb.cols, c.s);
@@ -2191,6 +2230,12 @@ void process_system(DevBasis<T>& gb, DevOp& op, long nrhs, const long* bidx, con
     DB::grow_to(wn, sizeof(T) * (nrhs + 8));
     lap(2);
     for (long j = 0; j < nrhs; ++j) {
+        if (gb.hook) {
+            c.sync();
+            if (gb.hook(gb.hook_user, system_index, j) != 0)
+                throw SolverError("process_system: rhs hook aborted at system " + std::to_string(system_index) +
+                                  ", rhs " + std::to_string(j));
+        }
         const double bnorm = std::fabs(bval[j]);
         const long rcur = gb.cols;
         const T* rhs = Rall.template as<T>() + (size_t)j * npad;
@@ -2245,7 +2290,8 @@ void process_system(DevBasis<T>& gb, DevOp& op, long nrhs, const long* bidx, con
                 row.appended = true;
                 ++appends;
                 dbg_sum("appended K col", gb.Kp() + (size_t)(gb.cols - 1) * n, n, c.s);
-                dbg_sum("appended W col", gb.Wp() + (size_t)(gb.cols - 1) * n, n, c.s);
+                if (!DevBasis<T>::lazy_w())  // lazy W: the column is formed later (materialize_W)
+                    dbg_sum("appended W col", gb.Wp() + (size_t)(gb.cols - 1) * n, n, c.s);
             }
             lap(5);
         }
@@ -3166,11 +3212,24 @@ long rd_basis_eig_block(rd_basis* b) {
 }
 void* rd_basis_device_ptr(rd_basis* b, int which) {
     void* p = nullptr;
-    BASIS_DISPATCH(b, {
-        if (which >= 2) B.materialize_W();
-        p = which == 0 ? (void*)B.Vp() : which == 1 ? (void*)B.Kp() : (void*)B.Wp();
+    const int rc = guard([&] {
+        BASIS_DISPATCH(b, {
+            if (which >= 2) {
+                if (!B.factored || !B.Wm.p) throw ConfigError("basis has no W = V R^-1 (refresh first)");
+                B.materialize_W();
+            }
+            p = which == 0 ? (void*)B.Vp() : which == 1 ? (void*)B.Kp() : (void*)B.Wp();
+        });
     });
-    return p;
+    return rc == 0 ? p : nullptr;
+}
+int rd_basis_set_rhs_hook(rd_basis* b, int (*fn)(void*, int, long), void* user) {
+    return guard([&] {
+        BASIS_DISPATCH(b, {
+            B.hook = fn;
+            B.hook_user = user;
+        });
+    });
 }
 int rd_basis_get(rd_basis* b, int which, void* out) {
     return guard([&] {
@@ -3497,6 +3556,47 @@ int rd_bench_gram(rd_ctx* ctx, int dtype, long n, long a, long b, int sym, int i
     });
 }
 
+// Mean device ms of the tall GEMM Z = X M (n x a times a x b, the refresh's
+// K = Y S^-1 / W S^-1 products; upper = M upper triangular) on seeded data.
+int rd_bench_gemm(rd_ctx* ctx, int dtype, long n, long a, long b, int upper, int iters, double* ms_out) {
+    return guard([&] {
+        Ctx& cx = ctx->c;
+        auto run = [&](auto tag) {
+            using T = decltype(tag);
+            DevBuf x, m, z;
+            x.ensure(sizeof(T) * n * a);
+            m.ensure(sizeof(T) * a * b);
+            z.ensure(sizeof(T) * n * b);
+            vec_randn<<<cx.grid_for(n * a * Sc<T>::W, 256, 8), 256, 0, cx.s>>>(x.template as<double>(),
+                                                                               n * a * Sc<T>::W, 21);
+            vec_randn<<<cx.grid_for(a * b * Sc<T>::W, 256, 8), 256, 0, cx.s>>>(m.template as<double>(),
+                                                                               a * b * Sc<T>::W, 22);
+            cx.check_launch();
+            cudaEvent_t e0, e1;
+            CK(cudaEventCreate(&e0));
+            CK(cudaEventCreate(&e1));
+            for (int w = 0; w < 2; ++w)
+                gemm<T, false>(cx, x.template as<T>(), n, a, m.template as<T>(), b, nullptr, 0, z.template as<T>(), n,
+                               n, upper != 0);
+            CK(cudaEventRecord(e0, cx.s));
+            for (int t = 0; t < iters; ++t)
+                gemm<T, false>(cx, x.template as<T>(), n, a, m.template as<T>(), b, nullptr, 0, z.template as<T>(), n,
+                               n, upper != 0);
+            CK(cudaEventRecord(e1, cx.s));
+            CK(cudaEventSynchronize(e1));
+            float ms = 0.f;
+            CK(cudaEventElapsedTime(&ms, e0, e1));
+            *ms_out = ms / iters;
+            cudaEventDestroy(e0);
+            cudaEventDestroy(e1);
+        };
+        if (dtype == 0)
+            run(double{});
+        else
+            run(cplx{});
+    });
+}
+
 // Multi-column stencil apply timing on the operator's current fields.
 int rd_bench_stencil(rd_op* o, int dtype, long ncols, int iters, double* ms_out) {
     return guard([&] {
@@ -3605,6 +3705,7 @@ int rd_basis_compress(rd_basis* b, double tol, int normalize, long* rank, long* 
             cx.sync();
             B.cols = rk;
             B.factored = false;
+            B.wvalid = 0;  // W (freed above) must be re-formed after a new refresh
             B.markers.assign(rk, kColCorrection);
             *rank = rk;
             for (long j = 0; j < m; ++j) perm[j] = pv[j];

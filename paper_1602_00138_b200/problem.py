@@ -234,10 +234,20 @@ def absorption(grid: GridSpec, p: RBFParams, mu_bg: float = 0.01, contrast: floa
                eps: float = 0.05) -> np.ndarray:
     """mu_a = mu_bg + contrast * H_eps(phi), phi = sum_j psi(|x-c_j|/w_j) - 1/2,
     psi(r) = exp(-r^2/2) 1[r < 3] (compactly supported Gaussian RBF)."""
-    x = grid.coordinates()
+    # separable squared distances broadcast over the (N_{d-1}, ..., N_0) node
+    # array (C order = node order p = i0 + N0 (i1 + N1 i2)); summed axis 0
+    # first, the same association as sum(axis=1) over (n, d) coordinates, so
+    # the values are bit-identical to the coordinate-list form
+    axes = [np.arange(Na) * grid.h for Na in grid.N]
     phi = np.full(grid.n, -0.5)
     for c, w in zip(p.centres, p.widths):
-        r = np.sqrt(((x - c) ** 2).sum(axis=1)) / w
+        r2 = None
+        for a in range(grid.d):
+            shape = [1] * grid.d
+            shape[grid.d - 1 - a] = grid.N[a]
+            da = ((axes[a] - c[a]) ** 2).reshape(shape)
+            r2 = da if r2 is None else r2 + da
+        r = np.sqrt(r2.reshape(-1)) / w
         phi += np.where(r < 3.0, np.exp(-0.5 * r * r), 0.0)
     return mu_bg + contrast * smooth_heaviside(phi, eps)
 

@@ -36,7 +36,7 @@ EXPORTS = [
     "rd_bench_stencil", "rd_residual_norms", "rd_basis_compress", "rd_rom_create", "rd_rom_destroy",
     "rd_rom_order", "rd_rom_E", "rd_rom_reduced_system", "rd_rom_transfer", "rd_rom_jacobian",
     "rd_fom_transfer", "rd_fom_jacobian", "rd_per_rhs_create", "rd_per_rhs_solve_system",
-    "rd_romb_write", "rd_romb_info", "rd_romb_read", "rd_basis_save", "rd_bench_gram",
+    "rd_romb_write", "rd_romb_info", "rd_romb_read", "rd_basis_save", "rd_bench_gram", "rd_basis_set_rhs_hook", "rd_bench_gemm",
 ]
 
 
@@ -68,6 +68,9 @@ class _Report(C.Structure):
 
 
 _LIB = None
+
+# int (*)(void* user, int system_index, long rhs): rd_basis_set_rhs_hook
+RHS_HOOK = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_int, C.c_long)
 
 
 def load_library(path: Optional[str] = None):
@@ -129,6 +132,7 @@ def load_library(path: Optional[str] = None):
     L.rd_bench_projection.argtypes = [vp, C.c_int, C.c_long, C.c_long, C.c_int, vp]
     L.rd_bench_stencil.argtypes = [vp, C.c_int, C.c_long, C.c_int, vp]
     L.rd_bench_gram.argtypes = [vp, C.c_int, C.c_long, C.c_long, C.c_long, C.c_int, C.c_int, vp]
+    L.rd_bench_gemm.argtypes = [vp, C.c_int, C.c_long, C.c_long, C.c_long, C.c_int, C.c_int, vp]
     L.rd_basis_compress.argtypes = [vp, C.c_double, C.c_int, lp, vp, vp]
     L.rd_residual_norms.argtypes = [vp, C.c_int, C.c_long, vp, vp, vp, C.c_int, vp]
     L.rd_romb_write.argtypes = [C.c_char_p, C.c_int, C.c_long, C.c_long, vp, vp, C.c_int, vp]
@@ -141,6 +145,7 @@ def load_library(path: Optional[str] = None):
     L.rd_fom_transfer.argtypes = [vp, C.c_int, C.c_long, vp, vp, C.c_long, vp, vp, C.c_double, vp, C.c_int, lp]
     L.rd_fom_jacobian.argtypes = [vp, C.c_int, C.c_long, vp, vp, C.c_long, vp, vp, C.c_long, vp, vp, vp, C.c_double,
                                   C.c_double, vp, C.c_int]
+    L.rd_basis_set_rhs_hook.argtypes = [vp, RHS_HOOK, vp]
     L.rd_rom_create.argtypes = [vp, C.c_int, C.c_long, C.c_long, vp, C.c_int, C.POINTER(vp)]
     L.rd_rom_destroy.argtypes = [vp]
     L.rd_rom_order.argtypes = [vp]
@@ -391,6 +396,27 @@ class GlobalBasis:
                                               cap, HOST, C.byref(h)))
         self.h = h
 
+    @classmethod
+    def from_device(cls, U0_ptr: int, X0_ptr: int, n: int, ku: int, nrhs: int, dtype, cap: int = 0,
+                    ctx: Optional[Context] = None) -> "GlobalBasis":
+        """init_basis_from (basis.cpp:114-134) on device-resident U0 (n x ku) and
+        X0 (n x nrhs), column-major, already in the basis dtype (no host copy)."""
+        self = cls.__new__(cls)
+        self.ctx = ctx or default_context()
+        self.dtype = np.dtype(dtype)
+        self.n, self.nrhs = n, nrhs
+        h = C.c_void_p()
+        _check(load_library().rd_basis_create(self.ctx.h, _dt(self.dtype), n, ku, nrhs, C.c_void_p(U0_ptr),
+                                              C.c_void_p(X0_ptr), cap, DEVICE, C.byref(h)))
+        self.h = h
+        return self
+
+    def destroy(self):
+        """Free the device buffers now (instead of at garbage collection)."""
+        if getattr(self, "h", None):
+            load_library().rd_basis_destroy(self.h)
+            self.h = None
+
     def __del__(self):
         if getattr(self, "h", None):
             try:
@@ -452,6 +478,40 @@ class GlobalBasis:
         load_library().rd_basis_space(self.h, j, _p(out))
         return out[:m].tolist()
 
+    def get_into(self, which: int, out: np.ndarray) -> np.ndarray:
+        """rd_basis_get into a caller-owned Fortran buffer with >= cols columns
+        (0 V, 1 K_img, 3 W: n x cols; 2 R: cols x cols); returns the filled view."""
+        r = self.cols
+        shape = (r, r) if which == 2 else (self.n, r)
+        if out.dtype != self.dtype or not out.flags.f_contiguous or out.shape[0] != shape[0] or out.shape[1] < r:
+            raise ValueError("get_into: buffer must be Fortran-ordered, dtype %s, %d rows, >= %d cols"
+                             % (self.dtype, shape[0], r))
+        view = out[:, :r]
+        _check(load_library().rd_basis_get(self.h, which, _p(view)))
+        return view
+
+    def set_rhs_hook(self, fn=None):
+        """Checkpoint hook: fn(system_index, j) runs before RHS j of every
+        process_system (the state it reads is the one the reference's loop body
+        starts from). An exception in fn aborts the system (SolverError) and is
+        re-raised from process_system's caller via ``hook_error``."""
+        self.hook_error = None
+        if fn is None:
+            self._hook = None
+            _check(load_library().rd_basis_set_rhs_hook(self.h, C.cast(None, RHS_HOOK), None))
+            return
+
+        def tramp(_user, system_index, j):
+            try:
+                fn(int(system_index), int(j))
+                return 0
+            except BaseException as e:  # noqa: BLE001 -- surfaced after the C call returns
+                self.hook_error = e
+                return 1
+
+        self._hook = RHS_HOOK(tramp)
+        _check(load_library().rd_basis_set_rhs_hook(self.h, self._hook, None))
+
     def compress(self, tol: float = 1e-10, normalize: bool = True):
         """Algorithm 1 compression in place (RRQR); V becomes the orthonormal
         retained basis. Returns (rank, perm, rdiag)."""
@@ -491,16 +551,33 @@ class GlobalBasis:
 
 
 def process_system(gb: GlobalBasis, op: SchurOperator, layout: P.Layout, tol: float, system_index: int,
-                   maxit: int = 0, want_X: bool = True) -> ProcessResult:
-    """Algorithm 2 main loop for one system (basis.cpp:157-207)."""
+                   maxit: int = 0, want_X: bool = True, X_out=None) -> ProcessResult:
+    """Algorithm 2 main loop for one system (basis.cpp:157-207).
+
+    X: a new host array when ``want_X``; ``X_out`` = a caller-owned host
+    Fortran (n x nrhs) array (e.g. pinned memory) filled in place, or an int
+    device pointer (n x nrhs, column-major) written on the device."""
     nrhs = layout.n_rhs
     idx = np.ascontiguousarray(layout.idx, dtype=np.int64)
     val = np.ascontiguousarray(layout.val, dtype=np.float64)
-    X = np.zeros((gb.n, nrhs), dtype=gb.dtype, order="F") if want_X else None
+    where = HOST
+    if X_out is None:
+        X = np.zeros((gb.n, nrhs), dtype=gb.dtype, order="F") if want_X else None
+        xp = _p(X)
+    elif isinstance(X_out, int):
+        X, xp, where = None, C.c_void_p(X_out), DEVICE
+    else:
+        if X_out.dtype != gb.dtype or X_out.shape != (gb.n, nrhs) or not X_out.flags.f_contiguous:
+            raise ValueError("process_system: X_out must be a Fortran (n, nrhs) array of the basis dtype")
+        X, xp = X_out, _p(X_out)
     log = np.zeros((nrhs, 5))
     its, app = C.c_long(), C.c_long()
-    _check(load_library().rd_process_system(gb.h, op.h, nrhs, _p(idx), _p(val), tol, system_index, maxit, _p(X),
-                                            HOST, _p(log), C.byref(its), C.byref(app)))
+    rc = load_library().rd_process_system(gb.h, op.h, nrhs, _p(idx), _p(val), tol, system_index, maxit, xp,
+                                          where, _p(log), C.byref(its), C.byref(app))
+    if rc != 0 and getattr(gb, "hook_error", None) is not None:
+        err, gb.hook_error = gb.hook_error, None
+        raise err
+    _check(rc)
     rows = [BuildLogRow(int(r[0]), int(r[1]), float(r[2]), int(r[3]), bool(r[4])) for r in log]
     return ProcessResult(X, rows, its.value, app.value)
 
@@ -740,4 +817,13 @@ def bench_gram(n: int, a: int, b: int, cplx: bool, sym: bool, iters: int = 5, ct
     ctx = ctx or default_context()
     ms = np.zeros(1)
     _check(load_library().rd_bench_gram(ctx.h, 1 if cplx else 0, n, a, b, int(sym), iters, _p(ms)))
+    return float(ms[0])
+
+
+def bench_gemm(n: int, a: int, b: int, cplx: bool, upper: bool = False, iters: int = 5,
+               ctx: Optional[Context] = None) -> float:
+    """Mean device ms of the tall GEMM X (n x a) M (a x b) on seeded data (bench hook)."""
+    ctx = ctx or default_context()
+    ms = np.zeros(1)
+    _check(load_library().rd_bench_gemm(ctx.h, 1 if cplx else 0, n, a, b, int(upper), iters, _p(ms)))
     return float(ms[0])
