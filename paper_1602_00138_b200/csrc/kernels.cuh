@@ -35,6 +35,8 @@ struct OpDev {
     const double* D;    // node fields (input)
     const double* mu;
     const double* F;    // assembled [4][n]: diag, fx, fy, fz
+    const double* Fp;   // the same fields with rows padded to ldF (TMA tensor maps need 16-byte row pitch)
+    long ldF;           // row pitch of Fp (N0, or N0 + 1 for odd N0)
 };
 
 __device__ __forceinline__ double hmean(double a, double b) { return 2.0 * (a * b) / (a + b); }
@@ -90,6 +92,19 @@ __global__ void __launch_bounds__(256) op_prepare(OpDev op, double* __restrict__
     F[op.n + p] = fx;
     F[2 * op.n + p] = fy;
     F[3 * op.n + p] = fz;
+}
+
+// Copy of the assembled fields with the row pitch rounded up to even (the
+// multi-column TMA stencil's tensor map needs 16-byte row strides).
+__global__ void pad_fields(const double* __restrict__ F, long n, int N0, long rows, long ldF,
+                           double* __restrict__ Fp) {
+    const long tot = 4 * rows * ldF;
+    for (long e = blockIdx.x * (long)blockDim.x + threadIdx.x; e < tot; e += (long)gridDim.x * blockDim.x) {
+        const long f = e / (rows * ldF), rem = e - f * rows * ldF;
+        const long row = rem / ldF;
+        const int i = (int)(rem - row * ldF);
+        Fp[e] = i < N0 ? F[f * n + row * N0 + i] : 0.0;
+    }
 }
 
 // Row p of A x from the assembled fields (same face order as the checker).

@@ -25,6 +25,7 @@
 #include "kernels.cuh"
 #include "ts_tma.cuh"
 #include "cg_fused.cuh"
+#include "stencil_tma.cuh"
 #include "rom.cuh"
 
 namespace rd {
@@ -316,11 +317,23 @@ struct Ctx {
 struct DevOp {
     Ctx* ctx = nullptr;
     OpDev d{};
-    DevBuf D, mu, F;
+    DevBuf D, mu, F, Fpad;
     bool have_fields = false;
     double lam_max = 0.0;
     long n() const { return d.n; }
 };
+
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda)
+inline PFN_cuTensorMapEncodeTiled_v12000 tmap_encode() {
+    static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
+    if (!encode) {
+        cudaDriverEntryPointQueryResult q;
+        CK(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", reinterpret_cast<void**>(&encode), cudaEnableDefault,
+                                   &q));
+        if (!encode) throw CudaError("cuTensorMapEncodeTiled unavailable");
+    }
+    return encode;
+}
 
 // ------------------------------------------------------ launch helpers ---
 inline dim3 stencil_grid(const OpDev& op, long zmult) {
@@ -335,9 +348,96 @@ inline int stencil_kz(const OpDev& op, long ncols, int sms) {
     return kz;
 }
 
+// ---- multi-column stencil through TMA-staged planes (stencil_tma.cuh) ----
+template <class T> CUtensorMap make_stencil_xmap(const OpDev& op, const T* x, long ldx, long xcols) {
+    constexpr int W = Sc<T>::W;
+    CUtensorMap m;
+    cuuint64_t gdim[4] = {(cuuint64_t)op.N0 * W, (cuuint64_t)op.N1, (cuuint64_t)op.N2, (cuuint64_t)xcols};
+    cuuint64_t gstride[3] = {(cuuint64_t)op.N0 * sizeof(T), (cuuint64_t)op.N0 * op.N1 * sizeof(T),
+                             (cuuint64_t)ldx * sizeof(T)};
+    cuuint32_t box[4] = {(cuuint32_t)(SXH * W), (cuuint32_t)SYH, 1, 1};
+    cuuint32_t es[4] = {1, 1, 1, 1};
+    CUresult r = tmap_encode()(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, const_cast<T*>(x), gdim, gstride, box, es,
+                               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                               CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) throw CudaError("stencil x tensor map: cuTensorMapEncodeTiled failed " + std::to_string((int)r));
+    return m;
+}
+inline CUtensorMap make_stencil_fmap(const OpDev& op) {
+    CUtensorMap m;
+    const cuuint64_t rows = (cuuint64_t)op.N1 * op.N2;
+    cuuint64_t gdim[4] = {(cuuint64_t)op.N0, (cuuint64_t)op.N1, (cuuint64_t)op.N2, 4};
+    cuuint64_t gstride[3] = {(cuuint64_t)op.ldF * 8, (cuuint64_t)op.ldF * op.N1 * 8, (cuuint64_t)op.ldF * rows * 8};
+    cuuint32_t box[4] = {(cuuint32_t)SXH, (cuuint32_t)SYH, 1, 4};
+    cuuint32_t es[4] = {1, 1, 1, 1};
+    CUresult r = tmap_encode()(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, const_cast<double*>(op.Fp), gdim, gstride,
+                               box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                               CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) throw CudaError("stencil field tensor map: cuTensorMapEncodeTiled failed " + std::to_string((int)r));
+    return m;
+}
+
+// TMA strides / base must be 16-byte aligned: always for complex128; for
+// float64 the x rows need an even N0 and an even column pitch.
+template <class T> bool stencil_tma_ok(const OpDev& op, const T* x, long ldx) {
+    static const int on = [] {
+        const char* e = std::getenv("ROMDOT_STENCIL_TMA");
+        return e ? std::atoi(e) : 1;
+    }();
+    if (!on || !op.Fp) return false;
+    if (((uintptr_t)x & 15u) != 0) return false;
+    if (sizeof(T) == 8 && (op.N0 % 2 != 0 || ldx % 2 != 0)) return false;
+    return true;
+}
+
+template <class T, int NC>
+void launch_stencil_tma(Ctx& c, const OpDev& op, const T* x, long ldx, const int* xcol, T* y, long ldy, long ncols) {
+    constexpr int S = 5;
+    const size_t smem = (size_t)S * StTma<T>::stage(NC);
+    static bool configured = false;
+    if (!configured) {
+        CK(cudaFuncSetAttribute(stencil_tma<T, NC>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        configured = true;
+    }
+    const CUtensorMap xm = make_stencil_xmap<T>(op, x, ldx, xcol ? (1L << 24) : ncols);
+    const CUtensorMap fm = make_stencil_fmap(op);
+    const long bxy = (long)((op.N0 + SX - 1) / SX) * ((op.N1 + SY - 1) / SY);
+    const long groups = (ncols + NC - 1) / NC;
+    // z chunk: as long as possible (plane re-loads at chunk seams cost 2 / kz)
+    // while the grid still covers every SM a few times
+    int kz = op.N2;
+    while (kz > 8 && bxy * groups * ((op.N2 + kz - 1) / kz) < 4L * c.sms) kz = (kz + 1) / 2;
+    const long nkc = (op.N2 + kz - 1) / kz;
+    const long maxg = std::max(1L, 65535L / nkc);
+    for (long g0 = 0; g0 < groups; g0 += maxg) {
+        const long ng = std::min(maxg, groups - g0);
+        const long cc0 = g0 * NC;
+        const long nc = std::min(ng * NC, ncols - cc0);
+        dim3 grid((unsigned)((op.N0 + SX - 1) / SX), (unsigned)((op.N1 + SY - 1) / SY), (unsigned)(nkc * ng));
+        // column offsets go through the tensor-map coordinate (base stays aligned);
+        // gathered columns through xcol
+        if (xcol) {
+            stencil_tma<T, NC><<<grid, ST_THREADS, smem, c.s>>>(xm, fm, op, xcol + cc0, y + (size_t)cc0 * ldy, ldy,
+                                                                 (int)nc, kz, S);
+        } else {
+            const CUtensorMap xo = cc0 ? make_stencil_xmap<T>(op, x + (size_t)cc0 * ldx, ldx, nc) : xm;
+            stencil_tma<T, NC><<<grid, ST_THREADS, smem, c.s>>>(xo, fm, op, nullptr, y + (size_t)cc0 * ldy, ldy,
+                                                                 (int)nc, kz, S);
+        }
+        c.check_launch();
+    }
+}
+
 template <class T> void launch_stencil(Ctx& c, const OpDev& op, const T* x, long ldx, const int* xcol, T* y,
                                        long ldy, long ncols) {
     if (ncols <= 0) return;
+    if (ncols >= 2 && stencil_tma_ok<T>(op, x, ldx)) {
+        if constexpr (Sc<T>::W == 2)
+            launch_stencil_tma<T, 4>(c, op, x, ldx, xcol, y, ldy, ncols);
+        else
+            launch_stencil_tma<T, 8>(c, op, x, ldx, xcol, y, ldy, ncols);
+        return;
+    }
     static const int mc = [] {
         // opt-in: C5 sweep at 8 columns 2D f64 0.38 -> 0.62 of peak, but 3D c128
         // 0.50 -> 0.41 (fewer z-march blocks in flight); C4 refresh unchanged
@@ -470,13 +570,7 @@ static CUtensorMap g_null_tmap;  // unused map passed to the 1D (row-blocked) va
 // Encode a 2D tensor map over a column-major n x ncols matrix (ld = n) viewed
 // as doubles, box = 32 rows x bc columns (driver entry point, no -lcuda).
 template <class T> CUtensorMap make_colmajor_tmap(const T* base, long n, long ld, long ncols, int bc) {
-    static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
-    if (!encode) {
-        cudaDriverEntryPointQueryResult q;
-        CK(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", reinterpret_cast<void**>(&encode), cudaEnableDefault,
-                                   &q));
-        if (!encode) throw CudaError("cuTensorMapEncodeTiled unavailable");
-    }
+    auto encode = tmap_encode();
     constexpr int W = Sc<T>::W;
     CUtensorMap m;
     cuuint64_t gdim[2] = {(cuuint64_t)n * W, (cuuint64_t)ncols};
@@ -2423,10 +2517,20 @@ long rrqr_dev(Ctx& c, long n, long m, const T* A, double tol, bool normalize, st
     long rank = 0;
     bool done = false;
     int level = 0;
+    PhaseTimer pt;  // ROMDOT_VERBOSE >= 1: per-phase wall time (adds syncs)
+    const bool timing = verbose() >= 1;
+    auto lap = [&](int k) {
+        if (timing) {
+            c.sync();
+            pt.lap(k);
+        }
+    };
+    lap(7);
     while (!done && !remaining.empty()) {
         const long mr = (long)remaining.size();
         G.ensure(sizeof(T) * mr * mr);
         gram<T, true>(c, Zp, ld, mr, Zp, ld, mr, n, G.template as<T>(), true, work);
+        lap(0);
         Rrow.ensure(sizeof(T) * mr * mr);
         pivd.ensure(sizeof(int) * mr);
         rdg.ensure(sizeof(double) * mr);
@@ -2450,6 +2554,7 @@ long rrqr_dev(Ctx& c, long n, long m, const T* A, double tol, bool normalize, st
             CK(cudaMemcpy(rdl.data(), rdg.p, sizeof(double) * nsel, cudaMemcpyDeviceToHost));
         }
         if (r00 < 0.0) r00 = nsel ? rdl[0] : 0.0;
+        lap(1);
         // accept pivots above the rank threshold
         long keep = 0;
         while (keep < nsel && rdl[keep] > tol * r00) ++keep;
@@ -2478,6 +2583,7 @@ long rrqr_dev(Ctx& c, long n, long m, const T* A, double tol, bool normalize, st
             c.check_launch();
             T* QP = Qout.template as<T>() + rank * ld;
             gemm<T, false>(c, ZP, ld, keep, Sinv.template as<T>(), keep, nullptr, 0, QP, ld, n, true);
+            lap(2);
             for (int pass = 0; pass < 2; ++pass) {  // CholQR2 clean-up of Q_P
                 gram<T, true>(c, QP, ld, keep, QP, ld, keep, n, Sp.template as<T>(), true, work);
                 CholInfo ci = chol_inv<T, true>(c, Sp.template as<T>(), Sinv.template as<T>(), keep, false);
@@ -2486,6 +2592,7 @@ long rrqr_dev(Ctx& c, long n, long m, const T* A, double tol, bool normalize, st
                 CK(cudaMemcpyAsync(QP, ZP, sizeof(T) * n * keep, cudaMemcpyDeviceToDevice, c.s));
             }
             rank += keep;
+            lap(3);
         }
         // remaining columns (not picked at this level), compacted
         std::vector<char> pk(mr, 0);
@@ -2514,12 +2621,16 @@ long rrqr_dev(Ctx& c, long n, long m, const T* A, double tol, bool normalize, st
             gemm<T, true>(c, Qout.template as<T>(), ld, rank, tmp.template as<T>(), nr, Zp, ld,
                           Zp, ld, n, false);
         }
+        lap(4);
+        VLOG(1, "rrqr level %d: %ld columns, %ld picked, %ld kept, rank %ld", level, mr, nsel, keep, rank);
         remaining = rest;
         ++level;
         if (level > 64) throw SolverError("rrqr: too many levels");
     }
     for (long j = 0; j < m; ++j)
         if (std::find(perm.begin(), perm.end(), j) == perm.end()) perm.push_back(j);
+    VLOG(1, "rrqr phases (ms): gram %.1f pivoted-chol %.1f pivot-block %.1f cholqr2 %.1f deflation %.1f | "
+            "n %ld m %ld rank %ld levels %d", pt.t[0], pt.t[1], pt.t[2], pt.t[3], pt.t[4], n, m, rank, level + 1);
     (void)W;
     return rank;
 }
@@ -2893,6 +3004,18 @@ int rd_op_set_fields(rd_op* o, const double* D, const double* mu, double shift, 
         o->op.d.F = o->op.F.template as<double>();
         op_prepare<<<stencil_grid(o->op.d, 1), 256, 0, c.s>>>(o->op.d, o->op.F.template as<double>());
         c.check_launch();
+        if (o->op.d.N0 % 2 == 0) {
+            o->op.d.Fp = o->op.d.F;
+            o->op.d.ldF = o->op.d.N0;
+        } else {
+            const long rows = (long)o->op.d.N1 * o->op.d.N2, ld = o->op.d.N0 + 1;
+            o->op.Fpad.ensure(sizeof(double) * 4 * rows * ld);
+            pad_fields<<<c.grid_for(4 * rows * ld, 256, 4), 256, 0, c.s>>>(o->op.d.F, n, o->op.d.N0, rows, ld,
+                                                                        o->op.Fpad.template as<double>());
+            c.check_launch();
+            o->op.d.Fp = o->op.Fpad.template as<double>();
+            o->op.d.ldF = ld;
+        }
         o->op.have_fields = true;
         if (where == 0) {
             std::vector<double> Dh(D, D + n), mh(mu, mu + n);

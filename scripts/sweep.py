@@ -34,6 +34,7 @@ def main():
     ap.add_argument("--what", default="stencil,proj,rrqr")
     ap.add_argument("--iters", type=int, default=10)
     ap.add_argument("--quick", action="store_true")
+    ap.add_argument("--ncols", default="1,4,8,16")
     args = ap.parse_args()
     build.build()
     from paper_1602_00138_b200 import romdot as R
@@ -52,7 +53,7 @@ def main():
                 dt = np.complex128 if cplx else np.float64
                 op = R.SchurOperator(g, P.Fields(f.D, f.mu, g.h ** 2 * 0.1 if cplx else 0.0), dt)
                 es = 16 if cplx else 8
-                for ncols in (1, 8):
+                for ncols in [int(v) for v in args.ncols.split(",")]:
                     ms = R.bench_stencil(op, ncols, args.iters)
                     by = ncols * g.n * 2 * es + 32 * g.n
                     gbs = by / (ms * 1e-3) / 1e9
@@ -60,6 +61,19 @@ def main():
                                       "ncols": ncols, "ms": ms, "GBps": round(gbs, 1), "frac": round(gbs / pk, 3)}),
                           flush=True)
                 del op
+    if "refresh" in what:  # the C4 refresh shape: A_i W, 3D 128^3 complex, 96..768 columns
+        g = P.CONFIGS["C4"].grid
+        rng = np.random.default_rng(5)
+        f = P.Fields(D=rng.uniform(0.3, 0.4, g.n), mu=g.h ** 2 * rng.uniform(0.005, 0.05, g.n), shift=g.h ** 2 * 0.1)
+        op = R.SchurOperator(g, f, np.complex128)
+        for ncols in (96, 256, 768):
+            ms = R.bench_stencil(op, ncols, 3)
+            by = ncols * g.n * 2 * 16 + 32 * g.n
+            gbs = by / (ms * 1e-3) / 1e9
+            print(json.dumps({"kernel": "stencil", "case": "C4 refresh A_i W", "d": 3, "N": 128, "n": g.n,
+                              "dtype": "c128", "ncols": ncols, "ms": ms, "GBps": round(gbs, 1),
+                              "frac": round(gbs / pk, 3)}), flush=True)
+        del op
     if "proj" in what:
         for n in (262144, 2097152):
             for k in (8, 32, 64, 128):

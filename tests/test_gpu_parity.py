@@ -30,10 +30,16 @@ def random_fields(grid, seed):
     return P.Fields(D=rng.uniform(0.3, 0.4, grid.n), mu=grid.h ** 2 * rng.uniform(0.005, 0.05, grid.n), shift=0.0)
 
 
-@pytest.mark.parametrize("d,N", [(2, (37, 29)), (3, (11, 9, 13)), (2, (317, 317)), (3, (47, 47, 47))])
+@pytest.mark.parametrize("d,N", [(2, (37, 29)), (3, (11, 9, 13)), (2, (317, 317)), (3, (47, 47, 47)),
+                                 (2, (64, 30)), (3, (48, 40, 44)), (3, (34, 17, 70))])
 @pytest.mark.parametrize("cplx", [False, True])
-@pytest.mark.parametrize("ncols", [1, 3, 9])  # one-column kernel; 4-column groups with a ragged tail
+@pytest.mark.parametrize("ncols", [1, 3, 9])
 def test_stencil_matches_oracle(rd, d, N, cplx, ncols):
+    """ncols = 1: the z-marching one-column kernel; ncols >= 2: the TMA-staged
+    multi-column kernel (stencil_tma.cuh; NC = 4 complex / 8 real columns per
+    block with a ragged last group), except float64 with odd N0 (row pitch not
+    16-byte aligned), which keeps the one-column kernel. Odd N0 complex uses
+    the row-padded coefficient copy."""
     g = P.GridSpec(d=d, N=N, h=1.0 / (N[0] - 1), D_bg=0.33)
     f = random_fields(g, 5)
     if cplx:
@@ -46,6 +52,56 @@ def test_stencil_matches_oracle(rd, d, N, cplx, ncols):
     y_ref = orc.Operator.grid(g, f, dt).apply(x)
     y = rd.SchurOperator(g, f, dt).apply(x)
     assert np.abs(y - y_ref).max() <= 1e-14 * np.abs(y_ref).max()
+
+
+@pytest.mark.parametrize("d,N", [(3, (48, 40, 44)), (2, (317, 317)), (3, (47, 47, 47))])
+@pytest.mark.parametrize("cplx", [False, True])
+def test_multicolumn_stencil_bitwise_equals_one_column(rd, d, N, cplx):
+    """The multi-column kernels keep zmarch's loads, products and summation
+    order per column, so a 13-column apply equals 13 one-column applies bit
+    for bit (same for the opt-in four-column kernel, ROMDOT_STENCIL_MC=1, run
+    in a subprocess because the switch is read once per process)."""
+    g = P.GridSpec(d=d, N=N, h=1.0 / (N[0] - 1), D_bg=0.33)
+    f = random_fields(g, 5)
+    if cplx:
+        f = P.Fields(f.D, f.mu, shift=g.h ** 2 * 0.1)
+    dt = np.complex128 if cplx else np.float64
+    rng = np.random.default_rng(9)
+    x = rng.standard_normal((g.n, 13))
+    if cplx:
+        x = x + 1j * rng.standard_normal((g.n, 13))
+    op = rd.SchurOperator(g, f, dt)
+    ym = op.apply(x)
+    y1 = np.stack([op.apply(np.ascontiguousarray(x[:, j])) for j in range(13)], axis=1)
+    assert np.array_equal(ym, y1)
+
+
+def test_four_column_stencil_opt_in(rd, tmp_path):
+    """ROMDOT_STENCIL_MC=1 (with the TMA kernel off) runs stencil_kernel_mc:
+    3 / 9 columns (ragged last group of 4), 2D and 3D, and 50 groups on a
+    long z axis. (Its grid-chunking branch needs > 65535 blocks in z, which
+    stencil_kz's sizing only reaches at ~2.6e5 columns: not exercised.)"""
+    import os
+    import subprocess
+    import sys
+    code = r'''
+import sys, numpy as np
+sys.path.insert(0, "ROOT"); sys.path.insert(0, "ROOT/oracle")
+import oracle as orc
+from paper_1602_00138_b200 import problem as P, romdot as R
+for d, N, nc in [(3, (11, 9, 13), 3), (3, (11, 9, 13), 9), (2, (37, 29), 9), (3, (8, 8, 2000), 200)]:
+    g = P.GridSpec(d=d, N=N, h=1.0 / (N[0] - 1), D_bg=0.33)
+    rng = np.random.default_rng(5)
+    f = P.Fields(D=rng.uniform(0.3, 0.4, g.n), mu=g.h ** 2 * rng.uniform(0.005, 0.05, g.n), shift=g.h ** 2 * 0.1)
+    x = rng.standard_normal((g.n, nc)) + 1j * rng.standard_normal((g.n, nc))
+    y = R.SchurOperator(g, f, np.complex128).apply(x)
+    yr = orc.Operator.grid(g, f, np.complex128).apply(x)
+    assert np.abs(y - yr).max() <= 1e-14 * np.abs(yr).max(), (d, N, nc)
+print("ok")
+'''.replace("ROOT", os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    env = dict(os.environ, ROMDOT_STENCIL_MC="1", ROMDOT_STENCIL_TMA="0")
+    out = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=600)
+    assert out.returncode == 0 and "ok" in out.stdout, out.stderr[-2000:]
 
 
 def _problem(cfg_name, point=1, omega=0.0):
