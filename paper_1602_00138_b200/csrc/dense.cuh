@@ -629,6 +629,19 @@ __global__ void __launch_bounds__(1024) pivoted_chol(const T* __restrict__ G, in
     if (threadIdx.x == 0) info[0] = k;
 }
 
+// dst[:, t] = src[:, idx[t]] for t < m (one launch for a whole column gather;
+// blockIdx.y = t). src and dst must not overlap.
+template <class T>
+__global__ void gather_columns(const T* __restrict__ src, long ld, const int* __restrict__ idx, int m, long n,
+                               T* __restrict__ dst, long ldd) {
+    const int t = blockIdx.y;
+    if (t >= m) return;
+    const T* sc = src + (size_t)idx[t] * ld;
+    T* dc = dst + (size_t)t * ldd;
+    for (long i = blockIdx.x * (long)blockDim.x + threadIdx.x; i < n; i += (long)gridDim.x * blockDim.x)
+        dc[i] = sc[i];
+}
+
 // Scale column j of X (n x c, ld) by 1/sqrt(nrm2[j]) (nrm2 = squared norms); zero columns untouched.
 template <class T>
 __global__ void scale_columns(T* X, long ld, int c, long n, const double* nrm2) {

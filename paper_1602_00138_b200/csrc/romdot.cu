@@ -2487,36 +2487,65 @@ long rrqr_dev(Ctx& c, long n, long m, const T* A, double tol, bool normalize, st
               std::vector<double>& rdiag_out, DevBuf& Qout, T* inplace = nullptr) {
     constexpr int W = Sc<T>::W;
     const long ld = n;
-    DevBuf Zown, Zb, G, Sp, Sinv, Rrow, pivd, rdg, infod, work, tmp, nrm;
-    // Zp: working copy of the candidate columns (or the caller's buffer when in place)
-    T* Zp = inplace;
+    DevBuf Zown, Zb, G, Sp, Sinv, Rrow, pivd, rdg, infod, work, tmp, nrm, idxd, Zs[2];
+    // Zcur: the working set (the caller's buffer when in place at level 0, then
+    // compacted copies in Zs[0] / Zs[1])
+    T* Zcur = inplace;
     if (!inplace) {
         Zown.ensure(sizeof(T) * n * std::max(1L, m));
         CK(cudaMemcpyAsync(Zown.p, A, sizeof(T) * n * m, cudaMemcpyDeviceToDevice, c.s));
-        Zp = Zown.template as<T>();
+        Zcur = Zown.template as<T>();
     }
-    nrm.ensure(sizeof(double) * std::max(1L, m));
+    nrm.ensure(sizeof(double) * std::max(1L, 2 * m));
     if (normalize && m > 0) {
         for (long j0 = 0; j0 < m; j0 += 1024) {
             const long cc = std::min(1024L, m - j0);
-            col_norms<T><<<c.grid_for(n, 256, 2), 256, sizeof(double) * cc, c.s>>>(Zp + j0 * ld, ld,
+            col_norms<T><<<c.grid_for(n, 256, 2), 256, sizeof(double) * cc, c.s>>>(Zcur + j0 * ld, ld,
                                                                                    (int)cc, n, c.red(),
                                                                                    nrm.template as<double>() + j0);
             c.check_launch();
         }
-        scale_columns<T><<<dim3(c.grid_for(n, 256, 1), (unsigned)m), 256, 0, c.s>>>(Zp, ld, (int)m, n,
+        scale_columns<T><<<dim3(c.grid_for(n, 256, 1), (unsigned)m), 256, 0, c.s>>>(Zcur, ld, (int)m, n,
                                                                                    nrm.template as<double>());
         c.check_launch();
     }
     Qout.ensure(sizeof(T) * n * std::max(1L, m));
-    std::vector<long> remaining(m);
+    idxd.ensure(sizeof(int) * std::max(1L, m));
+    int zs = 0;  // next free compaction buffer
+    // gather columns cols (local indices of Zcur) into a fresh compaction buffer
+    auto compact = [&](const std::vector<int>& cols) -> T* {
+        const long k = (long)cols.size();
+        DevBuf& dst = Zs[zs];
+        zs ^= 1;
+        if (dst.bytes < sizeof(T) * n * k) dst.ensure(sizeof(T) * n * k);
+        CK(cudaMemcpyAsync(idxd.p, cols.data(), sizeof(int) * k, cudaMemcpyHostToDevice, c.s));
+        gather_columns<T><<<dim3(c.grid_for(n, 256, 1), (unsigned)k), 256, 0, c.s>>>(
+            Zcur, ld, idxd.template as<int>(), (int)k, n, dst.template as<T>(), ld);
+        c.check_launch();
+        c.sync();  // cols is host memory of the caller's frame
+        return dst.template as<T>();
+    };
+    auto col_norms_host = [&](const T* X, long k, std::vector<double>& out) {
+        out.resize(k);
+        for (long j0 = 0; j0 < k; j0 += 1024) {
+            const long cc = std::min(1024L, k - j0);
+            col_norms<T><<<c.grid_for(n, 256, 2), 256, sizeof(double) * cc, c.s>>>(
+                X + j0 * ld, ld, (int)cc, n, c.red(), nrm.template as<double>() + j0);
+            c.check_launch();
+        }
+        CK(cudaMemcpyAsync(out.data(), nrm.p, sizeof(double) * k, cudaMemcpyDeviceToHost, c.s));
+        c.sync();
+    };
+    std::vector<long> remaining(m);  // original column of each working-set column
     for (long j = 0; j < m; ++j) remaining[j] = j;
     perm.clear();
     rdiag_out.clear();
+    std::vector<long> dropped;  // residual norm <= tol * R_00: can never be a pivot
     double r00 = -1.0;
     long rank = 0;
     bool done = false;
     int level = 0;
+    long second_passes = 0;
     PhaseTimer pt;  // ROMDOT_VERBOSE >= 1: per-phase wall time (adds syncs)
     const bool timing = verbose() >= 1;
     auto lap = [&](int k) {
@@ -2529,7 +2558,7 @@ long rrqr_dev(Ctx& c, long n, long m, const T* A, double tol, bool normalize, st
     while (!done && !remaining.empty()) {
         const long mr = (long)remaining.size();
         G.ensure(sizeof(T) * mr * mr);
-        gram<T, true>(c, Zp, ld, mr, Zp, ld, mr, n, G.template as<T>(), true, work);
+        gram<T, true>(c, Zcur, ld, mr, Zcur, ld, mr, n, G.template as<T>(), true, work);
         lap(0);
         Rrow.ensure(sizeof(T) * mr * mr);
         pivd.ensure(sizeof(int) * mr);
@@ -2563,13 +2592,15 @@ long rrqr_dev(Ctx& c, long n, long m, const T* A, double tol, bool normalize, st
             rdiag_out.push_back(rdl[k]);
         }
         if (keep < nsel || info[2] > 0.5 || nsel == 0) done = true;
+        T* QP = Qout.template as<T>() + rank * ld;
         if (keep > 0) {
             // Z_P (gathered, pivot order) -> Q_P = Z_P S_PP^-1, then a CholQR pass
             Zb.ensure(sizeof(T) * n * keep);
             T* ZP = Zb.template as<T>();
-            for (long k = 0; k < keep; ++k)
-                CK(cudaMemcpyAsync(ZP + k * ld, Zp + (long)piv[k] * ld, sizeof(T) * n,
-                                   cudaMemcpyDeviceToDevice, c.s));
+            CK(cudaMemcpyAsync(idxd.p, piv.data(), sizeof(int) * keep, cudaMemcpyHostToDevice, c.s));
+            gather_columns<T><<<dim3(c.grid_for(n, 256, 1), (unsigned)keep), 256, 0, c.s>>>(
+                Zcur, ld, idxd.template as<int>(), (int)keep, n, ZP, ld);
+            c.check_launch();
             // S_PP (keep x keep upper) from Rrow rows restricted to the picked columns
             std::vector<T> Rh((size_t)keep * mr);
             CK(cudaMemcpy(Rh.data(), Rrow.p, sizeof(T) * keep * mr, cudaMemcpyDeviceToHost));
@@ -2581,7 +2612,6 @@ long rrqr_dev(Ctx& c, long n, long m, const T* A, double tol, bool normalize, st
             CK(cudaMemcpyAsync(Sp.p, S.data(), sizeof(T) * keep * keep, cudaMemcpyHostToDevice, c.s));
             tri_inv_upper<T><<<1, 1024, 0, c.s>>>(Sp.template as<T>(), Sinv.template as<T>(), (int)keep);
             c.check_launch();
-            T* QP = Qout.template as<T>() + rank * ld;
             gemm<T, false>(c, ZP, ld, keep, Sinv.template as<T>(), keep, nullptr, 0, QP, ld, n, true);
             lap(2);
             for (int pass = 0; pass < 2; ++pass) {  // CholQR2 clean-up of Q_P
@@ -2594,43 +2624,70 @@ long rrqr_dev(Ctx& c, long n, long m, const T* A, double tol, bool normalize, st
             rank += keep;
             lap(3);
         }
-        // remaining columns (not picked at this level), compacted
+        // the columns not picked at this level, compacted (out of place)
         std::vector<char> pk(mr, 0);
         for (long k = 0; k < keep; ++k) pk[piv[k]] = 1;
         std::vector<long> rest;
-        std::vector<long> rest_local;
+        std::vector<int> rest_local;
         for (long i = 0; i < mr; ++i)
             if (!pk[i]) {
                 rest.push_back(remaining[i]);
-                rest_local.push_back(i);
+                rest_local.push_back((int)i);
             }
         if (done || rest.empty()) {
             for (long v : rest) perm.push_back(v);
             break;
         }
-        for (long t = 0; t < (long)rest_local.size(); ++t)
-            if (rest_local[t] != t)
-                CK(cudaMemcpyAsync(Zp + t * ld, Zp + rest_local[t] * ld, sizeof(T) * n,
-                                   cudaMemcpyDeviceToDevice, c.s));
         const long nr = (long)rest.size();
-        // Z_rest <- (I - Q Q^H)^2 Z_rest against every retained direction so far
-        tmp.ensure(sizeof(T) * rank * nr);
-        for (int pass = 0; pass < 2; ++pass) {
-            gram<T, true>(c, Qout.template as<T>(), ld, rank, Zp, ld, nr, n, tmp.template as<T>(), false,
-                          work);
-            gemm<T, true>(c, Qout.template as<T>(), ld, rank, tmp.template as<T>(), nr, Zp, ld,
-                          Zp, ld, n, false);
+        if (keep > 0) Zcur = compact(rest_local);
+        // block CGS against the new block Q_P (the working set is already
+        // orthogonal to the earlier blocks); a second pass against every
+        // retained direction only if some column lost more than half of its
+        // norm^2 (Kahan-Parlett, as the global appends)
+        std::vector<double> nb, na;
+        col_norms_host(Zcur, nr, nb);
+        tmp.ensure(sizeof(T) * std::max(1L, rank) * nr);
+        if (keep > 0) {
+            gram<T, true>(c, QP, ld, keep, Zcur, ld, nr, n, tmp.template as<T>(), false, work);
+            gemm<T, true>(c, QP, ld, keep, tmp.template as<T>(), nr, Zcur, ld, Zcur, ld, n, false);
         }
+        col_norms_host(Zcur, nr, na);
+        bool cancel = false;
+        for (long j = 0; j < nr; ++j) cancel |= na[j] < 0.5 * nb[j];
+        if (cancel) {
+            ++second_passes;
+            gram<T, true>(c, Qout.template as<T>(), ld, rank, Zcur, ld, nr, n, tmp.template as<T>(), false, work);
+            gemm<T, true>(c, Qout.template as<T>(), ld, rank, tmp.template as<T>(), nr, Zcur, ld, Zcur, ld, n,
+                          false);
+            col_norms_host(Zcur, nr, na);
+        }
+        // a column whose residual norm is <= tol * R_00 can never give R_kk >
+        // tol * R_00 (deflation only shrinks it): out of the working set
+        std::vector<int> live;
+        std::vector<long> surv;
+        const double cut = (tol * r00) * (tol * r00);
+        for (long j = 0; j < nr; ++j) {
+            if (na[j] > cut) {
+                live.push_back((int)j);
+                surv.push_back(rest[j]);
+            } else {
+                dropped.push_back(rest[j]);
+            }
+        }
+        if (!live.empty() && (long)live.size() < nr) Zcur = compact(live);
         lap(4);
-        VLOG(1, "rrqr level %d: %ld columns, %ld picked, %ld kept, rank %ld", level, mr, nsel, keep, rank);
-        remaining = rest;
+        VLOG(1, "rrqr level %d: %ld columns, %ld picked, %ld kept, rank %ld, %ld live after deflation%s", level, mr,
+             nsel, keep, rank, (long)live.size(), cancel ? " (second pass)" : "");
+        remaining = surv;
         ++level;
         if (level > 64) throw SolverError("rrqr: too many levels");
     }
+    for (long v : dropped) perm.push_back(v);
     for (long j = 0; j < m; ++j)
         if (std::find(perm.begin(), perm.end(), j) == perm.end()) perm.push_back(j);
     VLOG(1, "rrqr phases (ms): gram %.1f pivoted-chol %.1f pivot-block %.1f cholqr2 %.1f deflation %.1f | "
-            "n %ld m %ld rank %ld levels %d", pt.t[0], pt.t[1], pt.t[2], pt.t[3], pt.t[4], n, m, rank, level + 1);
+            "n %ld m %ld rank %ld levels %d second passes %ld", pt.t[0], pt.t[1], pt.t[2], pt.t[3], pt.t[4], n, m,
+         rank, level + 1, second_passes);
     (void)W;
     return rank;
 }
