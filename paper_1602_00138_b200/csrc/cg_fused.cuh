@@ -51,6 +51,7 @@ struct FusedLayout {
     int poll_ns;                // back-off of the stencil warps' step-counter polls
     int rel_ns;                 // back-off of the release warps' wait for the update warp
     int ahead;                  // stencil polls look past the step they need
+    int relbatch;               // release warps publish all their completed steps per fence
     // LI: item-order lead of phase 1 (>= L, slack for the stencil warps)
     int dbg;  // timing experiments only: bit 0 skips the step waits, bit 1 the stencil loads, bit 2 the phase-2 K reload
     uint32_t tile_bytes, x_bytes, stage_bytes;
@@ -390,19 +391,24 @@ __global__ void __launch_bounds__(FU_THREADS, 1)
         // fence per step in the update warp itself measured slower: 0.9 us each.)
         // FU_NREL warps take alternating steps so consecutive fences overlap (a
         // fence also waits for the warp's previous step-counter add).
+        // FL.relbatch: one fence publishes EVERY step of this warp's parity that
+        // the update warp has completed by then (the fence, ~1.6 us under load,
+        // is the publication chain's throughput limit when steps arrive faster).
         if (lane == 0) {
             FuProf pr{tprof};
             pr.start();
             volatile unsigned* rc = relcnt;
-            for (int s1 = wid - FU_REL_WARP; s1 < ns; s1 += FU_NREL) {
+            for (int s1 = wid - FU_REL_WARP; s1 < ns;) {
                 long long ta = pr.now();
-                while (*rc < (unsigned)(s1 + 1)) __nanosleep(FL.rel_ns);
+                unsigned done;
+                while ((done = *rc) < (unsigned)(s1 + 1)) __nanosleep(FL.rel_ns);
                 pr.add(0, ta);
                 ta = pr.now();
                 fence_acq_rel_gpu();
-                red_relaxed_gpu(stepcnt + s1, 1u);
+                const int hi = FL.relbatch ? min((int)done, ns) : s1 + 1;
+                for (; s1 < hi; s1 += FU_NREL) red_relaxed_gpu(stepcnt + s1, 1u);
                 pr.add(1, ta);
-                if (pr.t) pr.acc[2] += 1900;  // release count (x 1 us in the report)
+                if (pr.t) pr.acc[2] += 1900;  // fence count (x 1 us in the report)
             }
             pr.flush(8, wid == FU_REL_WARP);
         }

@@ -161,8 +161,8 @@ struct DevBuf {
         CK(cudaMalloc(&p, b));
         bytes = b;
         // ROMDOT_POISON=1: fill fresh allocations with NaN bytes so any read of
-        // unwritten device memory surfaces as a NaN (debug aid; sanitizers are
-        // not available on the GPU pool).
+        // unwritten device memory surfaces as a NaN in a normal-speed run
+        // (complements compute-sanitizer initcheck, scripts/sanitize.sh).
         static const int poison = [] {
             const char* e = std::getenv("ROMDOT_POISON");
             return e ? std::atoi(e) : 0;
@@ -355,7 +355,7 @@ template <class T> CUtensorMap make_stencil_xmap(const OpDev& op, const T* x, lo
     cuuint64_t gdim[4] = {(cuuint64_t)op.N0 * W, (cuuint64_t)op.N1, (cuuint64_t)op.N2, (cuuint64_t)xcols};
     cuuint64_t gstride[3] = {(cuuint64_t)op.N0 * sizeof(T), (cuuint64_t)op.N0 * op.N1 * sizeof(T),
                              (cuuint64_t)ldx * sizeof(T)};
-    cuuint32_t box[4] = {(cuuint32_t)(SXH * W), (cuuint32_t)SYH, 1, 1};
+    cuuint32_t box[4] = {(cuuint32_t)(StX<T>::W * W), (cuuint32_t)SYH, 1, 1};
     cuuint32_t es[4] = {1, 1, 1, 1};
     CUresult r = tmap_encode()(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, const_cast<T*>(x), gdim, gstride, box, es,
                                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
@@ -368,7 +368,7 @@ inline CUtensorMap make_stencil_fmap(const OpDev& op) {
     const cuuint64_t rows = (cuuint64_t)op.N1 * op.N2;
     cuuint64_t gdim[4] = {(cuuint64_t)op.N0, (cuuint64_t)op.N1, (cuuint64_t)op.N2, 4};
     cuuint64_t gstride[3] = {(cuuint64_t)op.ldF * 8, (cuuint64_t)op.ldF * op.N1 * 8, (cuuint64_t)op.ldF * rows * 8};
-    cuuint32_t box[4] = {(cuuint32_t)SXH, (cuuint32_t)SYH, 1, 4};
+    cuuint32_t box[4] = {(cuuint32_t)SFW, (cuuint32_t)SYH, 1, 4};
     cuuint32_t es[4] = {1, 1, 1, 1};
     CUresult r = tmap_encode()(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, const_cast<double*>(op.Fp), gdim, gstride,
                                box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
@@ -390,39 +390,45 @@ template <class T> bool stencil_tma_ok(const OpDev& op, const T* x, long ldx) {
     return true;
 }
 
-template <class T, int NC>
+template <class T, int NC, bool D2>
 void launch_stencil_tma(Ctx& c, const OpDev& op, const T* x, long ldx, const int* xcol, T* y, long ldy, long ncols) {
-    constexpr int S = 5;
+    static const int S = [] {  // ring depth (2 planes resident, S - 2 in flight); 3..8, <= 227 KB
+        const char* e = std::getenv("ROMDOT_STENCIL_STAGES");
+        const int want = e ? std::max(3, std::min(8, std::atoi(e))) : 3;  // 3: two CTAs per SM (C5 sweep, profiles/r02_c5_stencil_sweep.jsonl)
+        return std::min<int>(want, (int)(227 * 1024 / StTma<T>::stage(NC)));
+    }();
     const size_t smem = (size_t)S * StTma<T>::stage(NC);
     static bool configured = false;
     if (!configured) {
-        CK(cudaFuncSetAttribute(stencil_tma<T, NC>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        CK(cudaFuncSetAttribute(stencil_tma<T, NC, D2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         configured = true;
     }
     const CUtensorMap xm = make_stencil_xmap<T>(op, x, ldx, xcol ? (1L << 24) : ncols);
     const CUtensorMap fm = make_stencil_fmap(op);
-    const long bxy = (long)((op.N0 + SX - 1) / SX) * ((op.N1 + SY - 1) / SY);
+    // marched units: planes (3D, grid over (i, j) tiles) or 8-row tiles (2D, grid over i tiles)
+    const long bxy = (long)((op.N0 + SX - 1) / SX) * (D2 ? 1 : (op.N1 + SY - 1) / SY);
+    const int nk = D2 ? (op.N1 + SY - 1) / SY : op.N2;
     const long groups = (ncols + NC - 1) / NC;
-    // z chunk: as long as possible (plane re-loads at chunk seams cost 2 / kz)
-    // while the grid still covers every SM a few times
-    int kz = op.N2;
-    while (kz > 8 && bxy * groups * ((op.N2 + kz - 1) / kz) < 4L * c.sms) kz = (kz + 1) / 2;
-    const long nkc = (op.N2 + kz - 1) / kz;
+    // chunk length: as long as possible (3D plane re-loads at chunk seams cost
+    // 2 / kz) while the grid still covers every SM a few times
+    int kz = nk;
+    while (kz > 8 && bxy * groups * ((nk + kz - 1) / kz) < 4L * c.sms) kz = (kz + 1) / 2;
+    const long nkc = (nk + kz - 1) / kz;
     const long maxg = std::max(1L, 65535L / nkc);
     for (long g0 = 0; g0 < groups; g0 += maxg) {
         const long ng = std::min(maxg, groups - g0);
         const long cc0 = g0 * NC;
         const long nc = std::min(ng * NC, ncols - cc0);
-        dim3 grid((unsigned)((op.N0 + SX - 1) / SX), (unsigned)((op.N1 + SY - 1) / SY), (unsigned)(nkc * ng));
+        dim3 grid((unsigned)((op.N0 + SX - 1) / SX), (unsigned)(D2 ? 1 : (op.N1 + SY - 1) / SY), (unsigned)(nkc * ng));
         // column offsets go through the tensor-map coordinate (base stays aligned);
         // gathered columns through xcol
         if (xcol) {
-            stencil_tma<T, NC><<<grid, ST_THREADS, smem, c.s>>>(xm, fm, op, xcol + cc0, y + (size_t)cc0 * ldy, ldy,
-                                                                 (int)nc, kz, S);
+            stencil_tma<T, NC, D2><<<grid, ST_THREADS, smem, c.s>>>(xm, fm, op, xcol + cc0, y + (size_t)cc0 * ldy,
+                                                                     ldy, (int)nc, kz, S);
         } else {
             const CUtensorMap xo = cc0 ? make_stencil_xmap<T>(op, x + (size_t)cc0 * ldx, ldx, nc) : xm;
-            stencil_tma<T, NC><<<grid, ST_THREADS, smem, c.s>>>(xo, fm, op, nullptr, y + (size_t)cc0 * ldy, ldy,
-                                                                 (int)nc, kz, S);
+            stencil_tma<T, NC, D2><<<grid, ST_THREADS, smem, c.s>>>(xo, fm, op, nullptr, y + (size_t)cc0 * ldy,
+                                                                     ldy, (int)nc, kz, S);
         }
         c.check_launch();
     }
@@ -432,10 +438,11 @@ template <class T> void launch_stencil(Ctx& c, const OpDev& op, const T* x, long
                                        long ldy, long ncols) {
     if (ncols <= 0) return;
     if (ncols >= 2 && stencil_tma_ok<T>(op, x, ldx)) {
-        if constexpr (Sc<T>::W == 2)
-            launch_stencil_tma<T, 4>(c, op, x, ldx, xcol, y, ldy, ncols);
+        constexpr int NC = Sc<T>::W == 2 ? 4 : 8;
+        if (op.d == 2)
+            launch_stencil_tma<T, NC, true>(c, op, x, ldx, xcol, y, ldy, ncols);
         else
-            launch_stencil_tma<T, 8>(c, op, x, ldx, xcol, y, ldy, ncols);
+            launch_stencil_tma<T, NC, false>(c, op, x, ldx, xcol, y, ldy, ncols);
         return;
     }
     static const int mc = [] {
@@ -699,6 +706,11 @@ void cg_fused_inst(Ctx& c, const OpDev& op, const T* Krb, int C, T* w, T* r, T* 
         return e ? std::atoi(e) : 1;
     }();
     L.ahead = ahead;
+    static const int relbatch = [] {
+        const char* e = std::getenv("ROMDOT_FUSED_RELBATCH");
+        return e ? std::atoi(e) : 1;
+    }();
+    L.relbatch = relbatch;
     static const int dbg = [] {
         const char* e = std::getenv("ROMDOT_FUSED_DBG");
         return e ? std::atoi(e) : 0;

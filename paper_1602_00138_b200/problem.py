@@ -343,6 +343,12 @@ CONFIGS = {
     # min(K, 2) systems (harness.cpp:224)
     "R5": ProblemConfig("R5", d=2, N=121, n_src=(32,), n_det=(32,), m_rbf=9, n_points=2, omegas=(0.0,), k=10,
                         tol=1e-7, ref_sequence=True),
+    # R5 with another generator seed: over 12 seeds (20160200..20160211) the
+    # checker's criterion-5 ratio spans 0.32 .. 0.69 (median 0.59); this one
+    # gives 4098 / 9887 = 0.414, a case where the reference's own <= 0.5 bar
+    # (acceptance.cpp:325) holds on the checker, so the device must meet it too
+    "R5b": ProblemConfig("R5b", d=2, N=121, n_src=(32,), n_det=(32,), m_rbf=9, n_points=2, omegas=(0.0,), k=10,
+                         tol=1e-7, ref_sequence=True, seed=20160209),
     # small parity configs (oracle finishes in seconds)
     "T2": ProblemConfig("T2", d=2, N=33, n_src=(4,), n_det=(4,), m_rbf=4, n_points=3, omegas=(0.0,), k=6),
     "T2c": ProblemConfig("T2c", d=2, N=33, n_src=(4,), n_det=(4,), m_rbf=4, n_points=2,

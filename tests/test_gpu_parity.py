@@ -408,14 +408,20 @@ def test_per_rhs_recycler_lockstep_parity(rd, cfg):
     assert sum(len(pg_.space(j)) for j in range(lay.n_rhs)) == lay.n_rhs * (c.k + 1) + appends
 
 
-def test_global_basis_beats_per_rhs_recycling(rd):
+@pytest.mark.parametrize("cfg,ours_ref,base_ref,bar", [("R5", 4941, 9634, 0.6), ("R5b", 4098, 9887, 0.5)])
+def test_global_basis_beats_per_rhs_recycling(rd, cfg, ours_ref, base_ref, bar):
     """Acceptance criterion 5 (acceptance.cpp:314-334, cmd_compare_recycling
     harness.cpp:209-252) on R5, its 121^2 / 32+32 / k_eig 10 / tol 1e-7 mirror
     with the reference's parameter sequence: the shared-basis build needs
     about half the inner iterations of per-RHS-only recycling. The reference
-    asserts <= 0.5 on its PaLS phantom; on this level-set phantom the CPU
-    checker gives 4941 / 9634 = 0.513 (CG), which the device must reproduce."""
-    c = P.CONFIGS["R5"]
+    asserts ours * 2 <= baseline (<= 0.5) on its PaLS desk phantom, which is
+    not in the repository. The ratio depends on the phantom: over
+    12 seeds of this generator the CPU checker gives 0.32 .. 0.69 (median
+    0.59). So the test pins the device to the checker's own counts (+-2 per
+    row) and applies the reference's <= 0.5 bar where the checker meets it
+    (R5b, seed 20160209: 0.414); on the default seed (R5: 0.513 on the
+    checker, MINRES 0.53) the bar is 0.6."""
+    c = P.CONFIGS[cfg]
     g, lay = c.grid, c.layout()
     U0, X0 = _shared_seed(c, g, lay)
     gb = rd.GlobalBasis(U0, X0, c.cap)
@@ -425,8 +431,8 @@ def test_global_basis_beats_per_rhs_recycling(rd):
         f = c.fields(pt, w)
         ours += rd.process_system(gb, rd.SchurOperator(g, f, c.dtype), lay, c.tol, s, want_X=False).inner_iterations
         base += pr.solve_system(rd.SchurOperator(g, f, c.dtype), lay, c.tol, s, want_X=False).inner_iterations
-    assert ours / base <= 0.6, (ours, base)
-    assert abs(ours - 4941) <= 2 * 128 and abs(base - 9634) <= 2 * 128, (ours, base)
+    assert ours / base <= bar, (ours, base)
+    assert abs(ours - ours_ref) <= 2 * 128 and abs(base - base_ref) <= 2 * 128, (ours, base)
 
 
 def test_full_config_parity_C1(rd):
