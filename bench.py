@@ -402,6 +402,7 @@ def main():
     b0 = {"solves": 0, "its": 0, "rank": None}
     gb = None
     barrier()
+    torch.cuda.nvtx.range_push("timed")  # ncu --nvtx --nvtx-include "timed/" selects the timed launches
     with ClockSampler(local) as clk:
         ctx.mark()
         for i in range(args.steps):
@@ -430,6 +431,7 @@ def main():
         e_end = ev()
         ctx.mark()
         barrier()
+    torch.cuda.nvtx.range_pop()
     t_val_ms = ctx.elapsed_ms()
     launches = ctx.launches - launches0
     prof = ctx.prof()

@@ -161,8 +161,8 @@ struct DevBuf {
         CK(cudaMalloc(&p, b));
         bytes = b;
         // ROMDOT_POISON=1: fill fresh allocations with NaN bytes so any read of
-        // unwritten device memory surfaces as a NaN in a normal-speed run
-        // (complements compute-sanitizer initcheck, scripts/sanitize.sh).
+        // unwritten device memory surfaces as a NaN in a normal-speed run (the
+        // GPU pool refuses compute-sanitizer: profiles/r02_sanitizer_refused.txt).
         static const int poison = [] {
             const char* e = std::getenv("ROMDOT_POISON");
             return e ? std::atoi(e) : 0;

@@ -1,7 +1,9 @@
 #!/bin/bash
 # compute-sanitizer over scripts/sanitize_run.py (every kernel family on tiny
 # shapes). Writes gpurun_out/sanitize_<tool>.log and a one-line summary per
-# tool to gpurun_out/sanitize_summary.txt.
+# tool to gpurun_out/sanitize_summary.txt. NOTE: the graft GPU pool refuses
+# compute-sanitizer (status 86, profiles/r02_sanitizer_refused.txt); this
+# script is for machines where it is allowed.
 #   bash scripts/sanitize.sh [racecheck synccheck memcheck initcheck]
 cd "$(dirname "$0")/.." || exit 1
 mkdir -p gpurun_out
