@@ -54,6 +54,12 @@ long rd_ctx_launches(rd_ctx* ctx);
  * pair around a batch of back-to-back launches). bytes = algorithmic bytes. */
 void rd_ctx_profile(rd_ctx* ctx, int enable);
 int rd_ctx_prof_get(rd_ctx* ctx, int cls, double* ms, double* bytes, long* samples);
+/* ROMDOT_FUSED_CHECK=1 (debug): cg_fused stamps each row tile with the launch's
+ * epoch when its r' rows are published, and every stencil halo read checks the
+ * stamps of the tiles it reads after acquiring the step counters -- a race
+ * detector for the cross-CTA protocol (a violation fails the solve, status 3).
+ * Totals over the context: fused launches checked and stale reads seen.     */
+void rd_ctx_fused_check(rd_ctx* ctx, long* launches_checked, long* violations);
 /* Raw stream handle (cudaStream_t) for interop. */
 void* rd_ctx_stream(rd_ctx* ctx);
 

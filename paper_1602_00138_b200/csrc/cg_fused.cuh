@@ -220,7 +220,7 @@ template <class T, int CPW>
 __global__ void __launch_bounds__(FU_THREADS, 1)
     cg_fused(OpDev op, const T* __restrict__ Krb, int C, long ntile, FusedLayout FL, T* w, T* r, T* p, T* s, T* y,
              CGState* st, double* hist, GridRed red, double* cbuf, unsigned* stepcnt, const T* __restrict__ G,
-             unsigned long long* tprof) {
+             unsigned long long* tprof, unsigned* chk, unsigned epoch) {
     // Programmatic dependent launch (ROMDOT_FUSED_PDL=1, opt-in): the next
     // iteration's launch may be scheduled as soon as every CTA of this one has
     // started, so its CTAs take the SMs this grid's CTAs free while the last CTA
@@ -463,6 +463,9 @@ __global__ void __launch_bounds__(FU_THREADS, 1)
                 }
                 __syncwarp();
                 if (lane == 0) {
+                    // ROMDOT_FUSED_CHECK: tile epoch, published by the same release
+                    // chain as the r' rows it vouches for
+                    if (chk) chk[16 + (long)sidx * Gd + bid] = epoch;
                     mbar_arrive(&pfree[pbi]);
                     red_release_cta_shared(relcnt, 1u);
                 }
@@ -511,6 +514,23 @@ __global__ void __launch_bounds__(FU_THREADS, 1)
                 if (ok < shi) __nanosleep(FL.poll_ns);
             }
             pr.add(0, ta);
+            if (chk) {
+                // protocol check: every tile this warp's rows read r' from (the row
+                // itself and its six stencil neighbours) must carry this launch's
+                // epoch once the step counters say so; a stale epoch is a halo read
+                // that raced the owner's update (counted in chk[0])
+                for (int rb = 0; rb < RBN; ++rb) {
+                    const long row = t * TR + rb * 32 + lane;
+                    if (row >= n) continue;
+                    const StCoef cq = stencil_coef(op, row);
+                    const long nb[7] = {row, row - 1, row + 1, row - cq.s1, row + cq.s1, row - cq.s2, row + cq.s2};
+                    const bool use[7] = {true, (cq.m & 1) != 0, (cq.m & 2) != 0, (cq.m & 4) != 0,
+                                         (cq.m & 8) != 0, (cq.m & 16) != 0, (cq.m & 32) != 0};
+#pragma unroll
+                    for (int q = 0; q < 7; ++q)
+                        if (use[q] && ld_relaxed_u32(chk + 16 + nb[q] / TR) != epoch) atomicAdd(chk, 1u);
+                }
+            }
             const int slot = FU_NSW * (k & 1) + sw;
             const uint32_t use = (uint32_t)(k >> 1);
             ta = pr.now();

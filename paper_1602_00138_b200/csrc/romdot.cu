@@ -180,6 +180,9 @@ struct Ctx {
     DevBuf partials, counter, scal, cgst, hist, rflag;
     DevBuf fstep;  // per-step counters of the fused iteration (zero between launches)
     DevBuf fprof;  // ROMDOT_FUSED_PROF: per-role cycle sums of cg_fused
+    DevBuf fchk;   // ROMDOT_FUSED_CHECK: [0] stale-halo count, [16 + tile] tile epochs
+    unsigned fchk_epoch = 0;
+    long fchk_violations = 0, fchk_checked = 0;  // totals over the context's solves
     long fprof_launches = 0;
     // print and reset the cg_fused role accounting (average per launch, per warp)
     void fprof_reset() {
@@ -751,9 +754,23 @@ void cg_fused_inst(Ctx& c, const OpDev& op, const T* Krb, int C, T* w, T* r, T* 
     at[1].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = at;
     cfg.numAttrs = pdl ? 2 : 1;
+    static const bool fcheck = [] {
+        const char* e = std::getenv("ROMDOT_FUSED_CHECK");
+        return e && std::atoi(e) != 0;
+    }();
+    unsigned* chk = nullptr;
+    if (fcheck) {
+        const size_t need = sizeof(unsigned) * (16 + ntile + 256);
+        if (c.fchk.bytes < need) {
+            c.fchk.ensure(need);
+            CK(cudaMemsetAsync(c.fchk.p, 0, c.fchk.bytes, c.s));
+        }
+        chk = c.fchk.template as<unsigned>();
+    }
     CK(cudaLaunchKernelEx(&cfg, cg_fused<T, CPW>, op, Krb, C, ntile, L, w, r, p, s, y, st,
                           c.hist.template as<double>(), c.red(), cbuf, c.fstep.template as<unsigned>(), G,
-                          tprof ? c.fprof.template as<unsigned long long>() : (unsigned long long*)nullptr));
+                          tprof ? c.fprof.template as<unsigned long long>() : (unsigned long long*)nullptr, chk,
+                          ++c.fchk_epoch));
     if (tprof) ++c.fprof_launches;
     c.check_launch();
 }
@@ -1401,6 +1418,16 @@ SolveOut recycled_cg(Ctx& c, DevOp& op, const T* U, const T* K, long ncol, const
     const CGState fin = c.st_host[0];
     if (c.prof) c.prof_flush(fin.it);
     c.fprof_report();
+    if (c.fchk.p) {  // ROMDOT_FUSED_CHECK: cross-CTA protocol violations of cg_fused
+        unsigned bad = 0;
+        CK(cudaMemcpy(&bad, c.fchk.p, sizeof(unsigned), cudaMemcpyDeviceToHost));
+        c.fchk_violations += bad;
+        c.fchk_checked += fused ? std::max(0, fin.it - 1) : 0;
+        if (bad) {
+            CK(cudaMemset(c.fchk.p, 0, sizeof(unsigned)));
+            throw SolverError("cg_fused: " + std::to_string(bad) + " stencil halo reads raced their owner's update");
+        }
+    }
     SolveOut out;
     out.iterations = fin.it;
     out.converged = fin.converged != 0;
@@ -3022,6 +3049,10 @@ double rd_ctx_elapsed_ms(rd_ctx* ctx) {
     return ms;
 }
 long rd_ctx_launches(rd_ctx* ctx) { return ctx->c.launches; }
+void rd_ctx_fused_check(rd_ctx* ctx, long* launches_checked, long* violations) {
+    if (launches_checked) *launches_checked = ctx->c.fchk_checked;
+    if (violations) *violations = ctx->c.fchk_violations;
+}
 void rd_ctx_profile(rd_ctx* ctx, int enable) {
     ctx->c.prof = enable != 0;
     for (auto& q : ctx->c.pc) q = Ctx::ProfClass();

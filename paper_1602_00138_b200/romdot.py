@@ -36,7 +36,7 @@ EXPORTS = [
     "rd_bench_stencil", "rd_residual_norms", "rd_basis_compress", "rd_rom_create", "rd_rom_destroy",
     "rd_rom_order", "rd_rom_E", "rd_rom_reduced_system", "rd_rom_transfer", "rd_rom_jacobian",
     "rd_fom_transfer", "rd_fom_jacobian", "rd_per_rhs_create", "rd_per_rhs_solve_system",
-    "rd_romb_write", "rd_romb_info", "rd_romb_read", "rd_basis_save", "rd_bench_gram", "rd_basis_set_rhs_hook", "rd_bench_gemm",
+    "rd_romb_write", "rd_romb_info", "rd_romb_read", "rd_basis_save", "rd_bench_gram", "rd_basis_set_rhs_hook", "rd_bench_gemm", "rd_ctx_fused_check",
 ]
 
 
@@ -92,6 +92,8 @@ def load_library(path: Optional[str] = None):
     L.rd_ctx_elapsed_ms.restype = C.c_double
     L.rd_ctx_launches.argtypes = [vp]
     L.rd_ctx_launches.restype = C.c_long
+    L.rd_ctx_fused_check.argtypes = [vp, lp, lp]
+    L.rd_ctx_fused_check.restype = None
     L.rd_ctx_stream.argtypes = [vp]
     L.rd_ctx_stream.restype = vp
     L.rd_ctx_profile.argtypes = [vp, C.c_int]
@@ -234,6 +236,12 @@ class Context:
             load_library().rd_ctx_prof_get(self.h, i, C.byref(ms), C.byref(by), C.byref(ns))
             out[name] = (ms.value, by.value, ns.value)
         return out
+
+    def fused_check(self):
+        """(fused launches checked, stale halo reads) under ROMDOT_FUSED_CHECK=1."""
+        a, b = C.c_long(), C.c_long()
+        load_library().rd_ctx_fused_check(self.h, C.byref(a), C.byref(b))
+        return a.value, b.value
 
     @property
     def stream(self) -> int:

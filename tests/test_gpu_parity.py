@@ -508,3 +508,36 @@ def test_fused_iteration_matches_unfused(rd, monkeypatch, d, N, cplx, width):
     for res in (a, c):
         assert np.linalg.norm(r0 - op_o.apply(res.correction)) <= 1.01 * tol * np.linalg.norm(b)
     assert np.linalg.norm(c.correction - a.correction) <= 1e-5 * np.linalg.norm(a.correction)
+
+
+def test_fused_iteration_protocol_check(rd):
+    """Race check of cg_fused's cross-CTA protocol (compute-sanitizer is closed
+    on the GPU pool): with ROMDOT_FUSED_CHECK=1 every stencil halo read verifies
+    that the tiles it reads carry the current launch's epoch, stamped by the
+    owning CTA's update warp and published by the same release chain as r'.
+    Runs the T3c build and a C3-grid fused solve (many steps per CTA, plane lag
+    L > 1) in a subprocess; any stale read fails the solve."""
+    import os
+    import subprocess
+    import sys
+    code = r'''
+import sys, numpy as np
+sys.path.insert(0, "ROOT")
+from paper_1602_00138_b200 import problem as P, romdot as R
+ctx = R.default_context()
+for name in ("T3c", "C3"):
+    c = P.CONFIGS[name]
+    g, lay = c.grid, c.layout()
+    f0 = c.fields(0)
+    lam, U0 = R.smallest_eigenpairs(R.SchurOperator(g, f0, np.float64), c.k, 1e-8)
+    X0, _ = R.initial_solutions(R.SchurOperator(g, f0, c.dtype), lay, c.tol)
+    gb = R.GlobalBasis(U0.astype(c.dtype), X0, c.cap)
+    for s, (pt, w) in enumerate(c.systems()[:2], start=1):
+        R.process_system(gb, R.SchurOperator(g, c.fields(pt, w), c.dtype), lay, c.tol, s, want_X=False)
+checked, bad = ctx.fused_check()
+print("checked", checked, "violations", bad)
+assert checked > 1000 and bad == 0
+'''.replace("ROOT", os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    env = dict(os.environ, ROMDOT_FUSED_CHECK="1")
+    out = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=900)
+    assert out.returncode == 0, (out.stdout[-2000:], out.stderr[-3000:])
