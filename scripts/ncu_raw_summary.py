@@ -47,7 +47,7 @@ def load(path):
                     x = float(v.replace(",", ""))
                 except ValueError:
                     continue
-                d[k] = x * SCALE.get(u, 1.0) if k in ("dram_rd", "dram_wr", "t_ms", "sm_mhz") else x
+                d[k] = x * SCALE.get(u, 1.0) if k in ("dram_rd", "dram_wr", "t_ms", "sm_mhz", "smem") else x
         out.append(d)
     return out
 
@@ -61,7 +61,7 @@ def main():
         tr = d.get("dram_rd", 0.0) + d.get("dram_wr", 0.0)
         s = [f"{d.get('name', '?')[:90]}",
              f"duration {t:.3f} ms, grid {int(d.get('grid', 0))} x {int(d.get('block', 0))}, "
-             f"{int(d.get('regs', 0))} regs, dyn smem {d.get('smem', 0):.0f} B, SM clock {d.get('sm_mhz', 0):.0f} MHz",
+             f"{int(d.get('regs', 0))} regs, dyn smem {d.get('smem', 0) / 1e3:.0f} KB, SM clock {d.get('sm_mhz', 0):.0f} MHz",
              f"DRAM read {d.get('dram_rd', 0) / 1e9:.3f} GB + write {d.get('dram_wr', 0) / 1e9:.3f} GB = "
              f"{tr / 1e9:.3f} GB ({tr / (t * 1e-3) / 1e9 if t else 0:.0f} GB/s), "
              f"DRAM throughput {d.get('dram_pct', 0):.1f}% of ncu peak, L2 hit {d.get('l2_hit', 0):.1f}%",
