@@ -47,7 +47,8 @@ def load(path):
                     x = float(v.replace(",", ""))
                 except ValueError:
                     continue
-                d[k] = x * SCALE.get(u, 1.0) if k in ("dram_rd", "dram_wr", "t_ms", "sm_mhz", "smem") else x
+                d[k] = x * SCALE.get(u.split("/")[0] if k == "smem" else u, 1.0) \
+                    if k in ("dram_rd", "dram_wr", "t_ms", "sm_mhz", "smem") else x
         out.append(d)
     return out
 
