@@ -107,11 +107,13 @@ class GridSpec:
 
     @property
     def b_src(self) -> float:
-        return -self.D_bg / (1.0 + self.rho)              # B~ = D2 G^-1 B1 (grid.cpp:153-154)
+        # B~ = D2 (G^-1 B1) (grid.cpp:153-154), in the reference's operation order
+        # (cwiseInverse of g_diag first), so the values equal the reference's bit for bit
+        return -self.D_bg * (1.0 / (1.0 + self.rho))
 
     @property
     def c_det(self) -> float:
-        return -self.rho / (1.0 + self.rho)               # C~ = D1^T G^-1 C1 (grid.cpp:155)
+        return -self.rho * (1.0 / (1.0 + self.rho))       # C~ = D1^T (G^-1 C1) (grid.cpp:155)
 
     def node(self, *idx: int) -> int:
         p, stride = 0, 1
