@@ -48,6 +48,15 @@ int rd_ctx_mark(rd_ctx* ctx);
 double rd_ctx_elapsed_ms(rd_ctx* ctx);
 /* Number of this library's kernel launches issued on the context so far. */
 long rd_ctx_launches(rd_ctx* ctx);
+/* Inner solver of every entry point below that solves (rd_recycled_solve,
+ * rd_initial_solutions, rd_process_system, rd_per_rhs_solve_system):
+ *   0  recycled CG / COCG, device-resident recurrence (default; the hot path);
+ *   1  the reference's recycled MINRES (src/krylov.cpp:17-98 minres_core,
+ *      :147-179 recycled_minres) with its stopping rules -- real operators only
+ *      (ConfigError, status 2, for complex data). Parity path: reproduces the
+ *      reference's BuildLog iteration counts; scalar recurrence on the host.   */
+int rd_ctx_set_solver(rd_ctx* ctx, int solver);
+int rd_ctx_get_solver(rd_ctx* ctx);
 /* Sampled per-kernel-class device timing of the inner iteration (CUDA events on
  * the ctx stream, first iteration of each launch batch). enable resets the counters.
  * cls: 0 cg_stencil_dots, 1 ts_T, 2 ts_NT, 3 cg_update, 4 cg_fused (one event

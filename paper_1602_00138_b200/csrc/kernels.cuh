@@ -861,6 +861,58 @@ __global__ void __launch_bounds__(256) vec_norms(const T* __restrict__ x, long n
     grid_finish(red, 1 + W, out);
 }
 
+// ---- vector pieces of the reference's MINRES (krylov.cpp:17-98), real only ----
+// The reference-faithful parity solver (ctx solver 1): Lanczos scalars live on
+// the host, these kernels do the n-vector work. Rounded operation by operation
+// like the reference's expressions (no FMA contraction).
+// out[0] = a . b
+__global__ void __launch_bounds__(256) vec_dot(const double* __restrict__ a, const double* __restrict__ b, long n,
+                                               GridRed red, double* out) {
+    double h = 0.0;
+    for (long i = blockIdx.x * (long)blockDim.x + threadIdx.x; i < n; i += (long)gridDim.x * blockDim.x)
+        h = __dadd_rn(h, __dmul_rn(a[i], b[i]));
+    __shared__ double s_red[32];
+    __shared__ double s_vals[1];
+    const double s = block_sum(h, s_red);
+    if (threadIdx.x == 0) s_vals[0] = s;
+    __syncthreads();
+    if (!grid_commit(red, s_vals, 1)) return;
+    grid_finish(red, 1, out);
+}
+
+// v = v / s (krylov.cpp:38: v = b / beta1)
+__global__ void __launch_bounds__(256) vec_div(double* v, double s, long n) {
+    for (long i = blockIdx.x * (long)blockDim.x + threadIdx.x; i < n; i += (long)gridDim.x * blockDim.x)
+        v[i] = __ddiv_rn(v[i], s);
+}
+
+// p -= alpha v + beta v_old (krylov.cpp:52)
+__global__ void __launch_bounds__(256) minres_lanczos(double* p, const double* __restrict__ v,
+                                                      const double* __restrict__ v_old, double alpha, double beta,
+                                                      long n) {
+    for (long i = blockIdx.x * (long)blockDim.x + threadIdx.x; i < n; i += (long)gridDim.x * blockDim.x)
+        p[i] = __dsub_rn(p[i], __dadd_rn(__dmul_rn(alpha, v[i]), __dmul_rn(beta, v_old[i])));
+}
+
+// d_new = (v - delta d_old - eps d_oold) / gamma ; x += cphi d_new (krylov.cpp:64-65);
+// then the rotation of krylov.cpp:87-91: v_old = v, v = p / beta_next (when
+// advance), d_oold = d_old, d_old = d_new
+__global__ void __launch_bounds__(256) minres_update(double* x, double* v, double* v_old, const double* __restrict__ p,
+                                                     double* d_old, double* d_oold, double delta, double eps,
+                                                     double gamma, double cphi, double beta_next, int advance, long n) {
+    for (long i = blockIdx.x * (long)blockDim.x + threadIdx.x; i < n; i += (long)gridDim.x * blockDim.x) {
+        const double vi = v[i], d1 = d_old[i], d2 = d_oold[i];
+        const double dn = __ddiv_rn(__dsub_rn(__dsub_rn(vi, __dmul_rn(delta, d1)), __dmul_rn(eps, d2)), gamma);
+        x[i] = __dadd_rn(x[i], __dmul_rn(cphi, dn));
+        if (advance) {
+            v_old[i] = vi;
+            v[i] = __ddiv_rn(p[i], beta_next);
+            d_oold[i] = d1;
+            d_old[i] = dn;
+        }
+    }
+}
+
 // y = x * (1/rho) with rho from device: mode 0 = sqrt(out[0]) (Hermitian norm),
 // mode 1 = complex sqrt of the bilinear x^T x (out[1], out[2]) (real: sqrt(out[1]))
 template <class T> __device__ __forceinline__ T inv_rho(const double* nrm, int mode);

@@ -176,6 +176,7 @@ struct DevBuf {
 struct Ctx {
     int device = 0;
     int sms = 148;
+    int solver = 0;  // 0: recycled CG / COCG (default), 1: the reference's recycled MINRES (real, parity path)
     cudaStream_t s = nullptr;
     DevBuf partials, counter, scal, cgst, hist, rflag;
     DevBuf fstep;  // per-step counters of the fused iteration (zero between launches)
@@ -1457,6 +1458,150 @@ SolveOut recycled_cg(Ctx& c, DevOp& op, const T* U, const T* K, long ncol, const
     return out;
 }
 
+// The reference's recycled MINRES (krylov.cpp:17-98 minres_core, :147-179
+// recycled_minres) on the device, real symmetric operators only: Lanczos on
+// (I - K K^T) A started from the projected rhs, every new Lanczos vector
+// re-projected against K, Paige-Saunders Givens recurrence for the solution,
+// the reference's stopping rules (relres = |phibar| / scale <= tol, NaN
+// breakdown, 50-iteration stagnation window, exhausted Krylov space). This is
+// the PARITY path (ctx solver = 1, rd_ctx_set_solver): it makes the BuildLog of
+// the reference's own solver reproducible on the device. The scalar recurrence
+// runs on the host (two small D2H reads per iteration); the product default is
+// the device-resident CG above. ncol = 0: plain MINRES (krylov.cpp:100-104).
+// g = y + U (K^T rhs - K^T A y) as in recycled_cg (K^T rhs = 0 for every
+// right-hand side the builder passes, where this is krylov.cpp:172).
+inline SolveOut recycled_minres_dev(Ctx& c, DevOp& op, const double* U, const double* K, long ncol, const double* rhs,
+                                    double tol, long maxit, double rhs_scale, double* g, double* y_out, double* image,
+                                    Workspace<double>& ws, bool want_hist) {
+    const long n = op.n();
+    const long npad = padded_rows(n);
+    ws.ensure(npad);
+    double* v = ws.r.template as<double>();
+    double* p = ws.w.template as<double>();
+    double* v_old = ws.p.template as<double>();
+    double* d_old = ws.s.template as<double>();
+    double* d_oold = ws.tmp.template as<double>();
+    double* x = ws.y.template as<double>();
+    double* e = c.sc(0);
+    double* c1 = c.sc(1);
+    double* c2 = c.sc(2);
+    double* nrm = c.sc(3);
+    if (ncol > 1024) throw ConfigError("recycle space wider than 1024 columns");
+    const dim3 gv((unsigned)c.grid_for(n, 256, 4));
+    auto project = [&](double* wv) {  // w -= K (K^T w) (krylov.cpp:153-155)
+        if (ncol == 0) return;
+        ts_T_launch<double, false>(c, K, n, ncol, wv, n, c1);
+        ts_N_launch<double>(c, K, n, ncol, wv, wv, n, c1);
+    };
+    auto fetch = [&](const double* d) {
+        double h;
+        CK(cudaMemcpyAsync(&h, d, sizeof(double), cudaMemcpyDeviceToHost, c.s));
+        c.sync();
+        return h;
+    };
+    auto norm_of = [&](const double* d) {
+        launch_norms<double>(c, d, n, nrm);
+        return std::sqrt(fetch(nrm));
+    };
+    if (ncol > 0) ts_T_launch<double, false>(c, K, n, ncol, rhs, n, e);
+    CK(cudaMemcpyAsync(v, rhs, sizeof(double) * n, cudaMemcpyDeviceToDevice, c.s));
+    project(v);  // r0 (krylov.cpp:157-158)
+    const double scale = rhs_scale > 0.0 ? rhs_scale : norm_of(rhs);
+    const double beta1 = norm_of(v);
+    CK(cudaMemsetAsync(x, 0, sizeof(double) * npad, c.s));
+    CK(cudaMemsetAsync(v_old, 0, sizeof(double) * npad, c.s));
+    CK(cudaMemsetAsync(d_old, 0, sizeof(double) * npad, c.s));
+    CK(cudaMemsetAsync(d_oold, 0, sizeof(double) * npad, c.s));
+    SolveOut out;
+    double relres = 0.0;
+    if (beta1 == 0.0 || scale == 0.0) {  // krylov.cpp:26-30
+        out.converged = true;
+        out.hist.push_back(0.0);
+    } else {
+        relres = beta1 / scale;
+        out.hist.push_back(relres);
+        if (relres <= tol) {
+            out.converged = true;
+        } else {
+            vec_div<<<gv, 256, 0, c.s>>>(v, beta1, n);
+            c.check_launch();
+            double c_old2 = 1.0, s_old2 = 0.0, c_old = 1.0, s_old = 0.0;
+            double phibar = beta1, beta = 0.0, best = relres;
+            int stagnant = 0;
+            for (long k = 1; k <= maxit; ++k) {
+                launch_stencil<double>(c, op.d, v, n, nullptr, p, n, 1);
+                project(p);  // op = (I - K K^T) A (krylov.cpp:161-165)
+                vec_dot<<<gv, 256, 0, c.s>>>(v, p, n, c.red(), nrm);
+                c.check_launch();
+                const double alpha = fetch(nrm);
+                minres_lanczos<<<gv, 256, 0, c.s>>>(p, v, v_old, alpha, beta, n);
+                c.check_launch();
+                project(p);  // reorth (krylov.cpp:53)
+                const double beta_next = norm_of(p);
+                const double eps = s_old2 * beta;
+                const double delta_bar = c_old2 * beta;
+                const double delta = c_old * delta_bar + s_old * alpha;
+                const double gamma_bar = -s_old * delta_bar + c_old * alpha;
+                const double gamma = std::hypot(gamma_bar, beta_next);
+                if (gamma == 0.0) break;  // operator singular on this Krylov space
+                const double cs = gamma_bar / gamma;
+                const double sn = beta_next / gamma;
+                const bool advance = beta_next > 1e-300;
+                minres_update<<<gv, 256, 0, c.s>>>(x, v, v_old, p, d_old, d_oold, delta, eps, gamma, cs * phibar,
+                                                   advance ? beta_next : 1.0, advance ? 1 : 0, n);
+                c.check_launch();
+                phibar = -sn * phibar;
+                relres = std::abs(phibar) / scale;
+                out.iterations = (int)k;
+                out.hist.push_back(relres);
+                if (!std::isfinite(relres)) break;  // NaN breakdown
+                if (relres <= tol) {
+                    out.converged = true;
+                    break;
+                }
+                if (relres < best * (1.0 - 1e-12)) {
+                    best = relres;
+                    stagnant = 0;
+                } else if (++stagnant >= 50) {
+                    break;
+                }
+                if (!advance) break;  // Krylov space exhausted
+                beta = beta_next;
+                c_old2 = c_old;
+                s_old2 = s_old;
+                c_old = cs;
+                s_old = sn;
+            }
+        }
+    }
+    out.final_relres = relres;
+    if (!want_hist) out.hist.resize(std::min<size_t>(out.hist.size(), 1));  // [0] = init relres for the callers
+    CK(cudaMemcpyAsync(y_out, x, sizeof(double) * n, cudaMemcpyDeviceToDevice, c.s));
+    launch_stencil<double>(c, op.d, y_out, n, nullptr, image, n, 1);  // krylov.cpp:170
+    if (ncol > 0) {
+        ts_T_launch<double, false>(c, K, n, ncol, image, n, c1);
+        launch_addsub(c, (int)ncol, c1, e, -1.0, c2);  // c2 = K^T image - e
+        ts_N_launch<double>(c, U, n, ncol, y_out, g, n, c2);  // g = y - U c2
+    } else if (g != y_out) {
+        CK(cudaMemcpyAsync(g, y_out, sizeof(double) * n, cudaMemcpyDeviceToDevice, c.s));
+    }
+    return out;
+}
+
+// Solver selected on the context: 0 CG / COCG (default), 1 the reference's MINRES.
+template <class T>
+SolveOut recycled_solve(Ctx& c, DevOp& op, const T* U, const T* K, long ncol, const T* rhs, double tol, long maxit,
+                        double rhs_scale, T* g, T* y_out, T* image, Workspace<T>& ws, bool want_hist,
+                        bool padded_io = false, const T* Gpre = nullptr) {
+    if (c.solver == 1) {
+        if constexpr (std::is_same<T, double>::value)
+            return recycled_minres_dev(c, op, U, K, ncol, rhs, tol, maxit, rhs_scale, g, y_out, image, ws, want_hist);
+        else
+            throw ConfigError("solver: MINRES (the reference's solver) is real symmetric only; use CG / COCG");
+    }
+    return recycled_cg<T>(c, op, U, K, ncol, rhs, tol, maxit, rhs_scale, g, y_out, image, ws, want_hist, padded_io, Gpre);
+}
+
 // Batched independent CG / COCG on unit right-hand sides b_c = val[c] e_idx[c]
 // (the X0 seed solves, basis.cpp:141-149, and the
 // full-order transfer, rom.cpp:71-96). X (n x m, ld n) receives the solutions;
@@ -2406,8 +2551,8 @@ void process_system(DevBasis<T>& gb, DevOp& op, long nrhs, const long* bidx, con
             lap(3);
             dbg_sum("space K", gb.Kr.template as<T>(), n * cj, c.s);
             dbg_sum("space U", gb.Ur.template as<T>(), n * cj, c.s);
-            const T* Gsp = use_one_pass_projection() ? gb.space_gram(cj) : nullptr;
-            SolveOut so = recycled_cg<T>(c, op, gb.Ur.template as<T>(), gb.Kr.template as<T>(), cj, rhs,
+            const T* Gsp = use_one_pass_projection() && c.solver == 0 ? gb.space_gram(cj) : nullptr;
+            SolveOut so = recycled_solve<T>(c, op, gb.Ur.template as<T>(), gb.Kr.template as<T>(), cj, rhs,
                                          kInnerSafety * tol, maxit, bnorm, Gj, ybuf.template as<T>(),
                                          imbuf.template as<T>(), gb.ws, false, true, Gsp);
             if (!so.converged)
@@ -2488,8 +2633,8 @@ void per_rhs_solve_system(DevBasis<T>& gb, DevOp& op, long nrhs, const long* bid
         const long cj = (long)idx.size();
         gb.factor_rhs_space(op, idx);
         T* Gj = Xdev ? Xdev + (size_t)j * n : gbuf.template as<T>();
-        const T* Gsp = use_one_pass_projection() ? gb.space_gram(cj) : nullptr;
-        SolveOut so = recycled_cg<T>(c, op, gb.Ur.template as<T>(), gb.Kr.template as<T>(), cj, rhs, tol, maxit, bnorm,
+        const T* Gsp = use_one_pass_projection() && c.solver == 0 ? gb.space_gram(cj) : nullptr;
+        SolveOut so = recycled_solve<T>(c, op, gb.Ur.template as<T>(), gb.Kr.template as<T>(), cj, rhs, tol, maxit, bnorm,
                                      Gj, ybuf.template as<T>(), imbuf.template as<T>(), gb.ws, true, true, Gsp);
         CK(cudaMemcpyAsync(rhs + bidx[j], &zero, sizeof(T), cudaMemcpyHostToDevice, c.s));
         c.sync();  // bv / zero are host stack values
@@ -3049,6 +3194,14 @@ double rd_ctx_elapsed_ms(rd_ctx* ctx) {
     return ms;
 }
 long rd_ctx_launches(rd_ctx* ctx) { return ctx->c.launches; }
+
+int rd_ctx_set_solver(rd_ctx* ctx, int solver) {
+    return guard([&] {
+        if (solver != 0 && solver != 1) throw rd::ConfigError("solver: 0 (CG / COCG) or 1 (MINRES)");
+        ctx->c.solver = solver;
+    });
+}
+int rd_ctx_get_solver(rd_ctx* ctx) { return ctx->c.solver; }
 void rd_ctx_fused_check(rd_ctx* ctx, long* launches_checked, long* violations) {
     if (launches_checked) *launches_checked = ctx->c.fchk_checked;
     if (violations) *violations = ctx->c.fchk_violations;
@@ -3176,11 +3329,11 @@ int rd_recycled_solve(rd_op* o, int dtype, const void* U, const void* K, long c,
         SolveOut so;
         if (dtype == 0) {
             Workspace<double> ws;
-            so = recycled_cg<double>(cx, o->op, (const double*)Us.p, (const double*)Ks.p, c, (const double*)rs.p, tol,
+            so = recycled_solve<double>(cx, o->op, (const double*)Us.p, (const double*)Ks.p, c, (const double*)rs.p, tol,
                                      maxit, rhs_scale, (double*)gp, (double*)yp, (double*)ip, ws, hist != nullptr);
         } else {
             Workspace<cplx> ws;
-            so = recycled_cg<cplx>(cx, o->op, (const cplx*)Us.p, (const cplx*)Ks.p, c, (const cplx*)rs.p, tol, maxit,
+            so = recycled_solve<cplx>(cx, o->op, (const cplx*)Us.p, (const cplx*)Ks.p, c, (const cplx*)rs.p, tol, maxit,
                                    rhs_scale, (cplx*)gp, (cplx*)yp, (cplx*)ip, ws, hist != nullptr);
         }
         // correction norm
@@ -3240,6 +3393,33 @@ int rd_initial_solutions(rd_op* o, int dtype, long nrhs, const long* bidx, const
         // 5 n-vectors per column of workspace
         const long chunk = std::max(1L, std::min(nrhs, (long)(24e9 / (5.0 * es * (double)n))));
         long tot = 0;
+        if (cx.solver == 1) {
+            // the reference's seed solves: MINRES column by column at 0.25 tol (basis.cpp:141-149)
+            if (dtype != 0) throw rd::ConfigError("solver: MINRES (the reference's solver) is real symmetric only");
+            Workspace<double> ws;
+            DevBuf rhsb, yb, ib;
+            rhsb.ensure(es * n);
+            yb.ensure(es * n);
+            ib.ensure(es * n);
+            CK(cudaMemsetAsync(rhsb.p, 0, es * n, cx.s));
+            const double zero = 0.0;
+            for (long j = 0; j < nrhs; ++j) {
+                double* rhs = rhsb.template as<double>();
+                CK(cudaMemcpyAsync(rhs + bidx[j], &bval[j], sizeof(double), cudaMemcpyHostToDevice, cx.s));
+                const SolveOut so = recycled_minres_dev(cx, o->op, nullptr, nullptr, 0, rhs, kInnerSafety * tol, 2 * n, 0.0,
+                                                        static_cast<double*>(xp) + (size_t)j * n,
+                                                        yb.template as<double>(), ib.template as<double>(), ws, false);
+                CK(cudaMemcpyAsync(rhs + bidx[j], &zero, sizeof(double), cudaMemcpyHostToDevice, cx.s));
+                cx.sync();
+                if (!so.converged)
+                    throw rd::SolverError("init_basis: MINRES failed on initial solution column " + std::to_string(j));
+                tot += so.iterations;
+            }
+            Xs.finish();
+            cx.sync();
+            if (total_iterations) *total_iterations = tot;
+            return;
+        }
         auto run = [&](auto tag) {
             using T = decltype(tag);
             for (long j0 = 0; j0 < nrhs; j0 += chunk) {

@@ -28,7 +28,7 @@ _SO = os.path.join(_HERE, "libromdot_b200.so")
 
 EXPORTS = [
     "rd_ctx_create", "rd_ctx_destroy", "rd_last_error", "rd_ctx_sync", "rd_ctx_mark", "rd_ctx_elapsed_ms",
-    "rd_ctx_launches", "rd_ctx_stream", "rd_ctx_profile", "rd_ctx_prof_get", "rd_op_create", "rd_op_destroy", "rd_op_set_fields", "rd_op_apply",
+    "rd_ctx_launches", "rd_ctx_set_solver", "rd_ctx_get_solver", "rd_ctx_stream", "rd_ctx_profile", "rd_ctx_prof_get", "rd_op_create", "rd_op_destroy", "rd_op_set_fields", "rd_op_apply",
     "rd_op_lam_max", "rd_recycled_solve", "rd_recycle_space_from_raw", "rd_initial_solutions",
     "rd_smallest_eigenpairs", "rd_basis_create", "rd_basis_destroy", "rd_basis_cols", "rd_basis_factored", "rd_basis_eig_block",
     "rd_basis_get", "rd_basis_device_ptr", "rd_basis_markers", "rd_basis_space", "rd_basis_refresh",
@@ -92,6 +92,8 @@ def load_library(path: Optional[str] = None):
     L.rd_ctx_elapsed_ms.restype = C.c_double
     L.rd_ctx_launches.argtypes = [vp]
     L.rd_ctx_launches.restype = C.c_long
+    L.rd_ctx_set_solver.argtypes = [vp, C.c_int]
+    L.rd_ctx_get_solver.argtypes = [vp]
     L.rd_ctx_fused_check.argtypes = [vp, lp, lp]
     L.rd_ctx_fused_check.restype = None
     L.rd_ctx_stream.argtypes = [vp]
@@ -226,6 +228,17 @@ class Context:
     def profile(self, enable: bool = True):
         load_library().rd_ctx_profile(self.h, int(enable))
 
+    CG, MINRES = 0, 1
+
+    def set_solver(self, solver: int):
+        """0 = recycled CG / COCG (default, the hot path); 1 = the reference's
+        recycled MINRES (krylov.cpp:17-98, 147-179; real operators, parity path)."""
+        _check(load_library().rd_ctx_set_solver(self.h, int(solver)))
+
+    @property
+    def solver(self) -> int:
+        return load_library().rd_ctx_get_solver(self.h)
+
     PROF_CLASSES = ("cg_stencil_dots", "ts_T", "ts_NT", "cg_update", "cg_fused")
 
     def prof(self):
@@ -337,6 +350,18 @@ def recycled_cg(op: SchurOperator, U: Optional[np.ndarray], K: Optional[np.ndarr
     m = min(rep.iterations + 1, hist.size)
     return RecycledResult(g, y, im, SolveReport(rep.iterations, bool(rep.converged), hist[:m].copy(),
                                                 rep.correction_norm, rep.final_relres))
+
+
+def recycled_minres(op: SchurOperator, U: Optional[np.ndarray], K: Optional[np.ndarray], rhs, tol, maxit,
+                    rhs_scale: float = 0.0) -> RecycledResult:
+    """The reference's own inner solver on the device (krylov.cpp:147-179, real
+    operators): `recycled_cg` with the context switched to MINRES for the call."""
+    prev = op.ctx.solver
+    op.ctx.set_solver(Context.MINRES)
+    try:
+        return recycled_cg(op, U, K, rhs, tol, maxit, rhs_scale)
+    finally:
+        op.ctx.set_solver(prev)
 
 
 def recycle_space_from_raw(W: np.ndarray, AW: np.ndarray, ctx: Optional[Context] = None):

@@ -92,6 +92,7 @@ def make_desk():
     corr, ndir, img, rrep = g.recycled_minres(m2, W, AW, rhs, 1e-9, 2 * g.n, float(np.linalg.norm(rhs)))
     out["rm_W"], out["rm_AW"], out["rm_corr"], out["rm_hist"], out["rm_its"] = W, AW, corr, rrep.history, rrep.iterations
     out["rm_corr_norm"] = rrep.correction_norm
+    out["rm_z0"], out["rm_r0"] = ref.initial_guess(W, AW, rhs)  # initial_guess (krylov.cpp:141-145)
     # reduced model on the final basis at a new parameter
     rom = ref.ReducedModel(g, Vf)
     p_new = desk_params(0.17)

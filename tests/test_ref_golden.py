@@ -131,6 +131,8 @@ def test_recycled_minres_matches_reference():  # krylov.cpp:106-115, 147-179
     assert np.allclose(res.report.history, z["rm_hist"], rtol=1e-8, atol=0)
     assert rel(res.correction, z["rm_corr"]) <= 1e-11
     assert abs(res.report.correction_norm - float(z["rm_corr_norm"])) <= 1e-11 * float(z["rm_corr_norm"])
+    z0, r0 = rs.initial_guess(rhs)
+    assert rel(z0, z["rm_z0"]) <= 1e-11 and rel(r0, z["rm_r0"]) <= 1e-12
 
 
 def test_reduced_model_matches_reference():  # rom.cpp:9-67
