@@ -25,6 +25,7 @@
 #include "kernels.cuh"
 #include "ts_tma.cuh"
 #include "cg_fused.cuh"
+#include "bcg_defl.cuh"
 #include "stencil_tma.cuh"
 #include "rom.cuh"
 
@@ -1942,6 +1943,246 @@ constexpr double kInnerSafety = 0.25;  // basis.cpp:27
 // (basis.cpp:168-205) starts RHS j from. Nonzero return aborts the system.
 typedef int (*RhsHook)(void* user, int system_index, long rhs);
 
+// ------------------------------------------- batched deflated solves ---
+// BD_M correction solves of one system in flight (bcg_defl.cuh). The caller
+// owns the order: load(slot, ...) right after factor_rhs_space left the
+// right-hand side's space in gb.Ur / gb.Kr, iterate() a few steps, poll(), then
+// finish(slot, ...) forms image = A y and g = y + U (K^T rhs - K^T image) as
+// recycled_cg does. ROMDOT_BATCH=0 keeps every solve on the one-solve path.
+inline int batch_slots() {  // read per call so a test can compare both paths in one process
+    const char* e = std::getenv("ROMDOT_BATCH");
+    return e ? std::atoi(e) : 1;
+}
+inline int batch_steps() {
+    static const int b = [] {
+        const char* e = std::getenv("ROMDOT_BATCH_STEPS");
+        return std::max(1, e ? std::atoi(e) : 4);
+    }();
+    return b;
+}
+
+template <class T> struct BatchedDeflated {
+    static constexpr int M = BD_M;
+    static constexpr int W = Sc<T>::W;
+    static constexpr int NV = 2 * W + 1;
+    static constexpr int kTS = BD_TCH * BD_NCH;  // slot stride of the trailing coefficient arrays
+    Ctx* ctx = nullptr;
+    long n = 0, npad = 0, kb = 0, tcap = 0, cmax = 0;
+    DevBuf Rb, Wb, Pb, Sb, Yb, Ktb, Utb, Gb, Eb, c1e, c1t, cpe, cpt, stb, krb, part_st, cnt_st, part_tr, cnt_tr, tmp;
+    CGState* hs = nullptr;  // pinned: [0, M) polled states, [M, 2M) init staging
+    BDTrail<T> tr{};
+    BDLayout LT{}, LN{};
+    long ntileT = 0, ntileN = 0;
+    int nstep = 0, kz = 1, gx = 1;
+    dim3 gst;
+    long nbc = 0;
+    int tw[M] = {0};
+    ~BatchedDeflated() {
+        if (hs) cudaFreeHost(hs);
+    }
+    T* col(DevBuf& b, int m) const { return b.template as<T>() + (size_t)m * npad; }
+    T* kt(int m) const { return Ktb.template as<T>() + (size_t)m * tcap * npad; }
+    T* ut(int m) const { return Utb.template as<T>() + (size_t)m * tcap * npad; }
+    double* e_of(int m) const { return Eb.template as<double>() + (size_t)m * cmax * W; }
+
+    static bool supported(long ku, long tmax) { return ku >= 1 && ku <= 64 && tmax <= BD_TCH * BD_NCH; }
+
+    template <int NSTEP> void configure() {
+        int optin = 0;
+        CK(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, ctx->device));
+        cudaFuncAttributes fa;
+        CK(cudaFuncGetAttributes(&fa, bd_T_eig<T>));
+        CK(cudaFuncSetAttribute(bd_T_eig<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                optin - (int)fa.sharedSizeBytes));
+        CK(cudaFuncGetAttributes(&fa, bd_N_eig<T, NSTEP>));
+        CK(cudaFuncSetAttribute(bd_N_eig<T, NSTEP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                optin - (int)fa.sharedSizeBytes));
+        auto stages = [&](int TR, uint32_t xpad) {
+            BDLayout L = bd_layout<T>((int)kb, TR, 2, xpad);
+            const uint32_t per = L.stride_k + ((L.stride_x * M + 127u) & ~127u);
+            const uint32_t fixed = L.total - 2 * per;
+            int S = (int)std::min<long>(8, ((long)optin - 2048 - fixed) / per);
+            if (S < 2) throw ConfigError("batched solves: shared-memory ring too large");
+            return bd_layout<T>((int)kb, TR, S, xpad);
+        };
+        // T pass: 512-byte W segments per slot; N pass: twice the rows (8 row groups per
+        // 64 complex rows, one per consumer warp)
+        const int trT = 32 * (16 / (int)sizeof(T));
+        LT = stages(trT, 64);
+        LN = stages(2 * trT, 16);
+    }
+
+    // per system: the eigen block of gb.Kr (n x ku, ld n) in the row-blocked layout
+    void begin_system(Ctx& c, const OpDev& op, const T* Kb_colmajor, long ku, long tmax) {
+        ctx = &c;
+        n = op.n;
+        npad = padded_rows(n);
+        kb = ku;
+        tcap = std::max(1L, tmax);
+        cmax = kb + tcap;
+        if (!hs) CK(cudaMallocHost(&hs, sizeof(CGState) * 2 * M));
+        const size_t vb = sizeof(T) * npad * M;
+        for (DevBuf* b : {&Rb, &Wb, &Pb, &Sb, &Yb}) {
+            b->ensure(vb);
+            CK(cudaMemsetAsync(b->p, 0, vb, c.s));
+        }
+        tmp.ensure(sizeof(T) * npad * 2);
+        CK(cudaMemsetAsync(tmp.p, 0, sizeof(T) * npad * 2, c.s));
+        Ktb.ensure(sizeof(T) * npad * tcap * M);
+        Utb.ensure(sizeof(T) * npad * tcap * M);
+        CK(cudaMemsetAsync(Ktb.p, 0, sizeof(T) * npad * tcap * M, c.s));
+        CK(cudaMemsetAsync(Utb.p, 0, sizeof(T) * npad * tcap * M, c.s));
+        Gb.ensure(sizeof(T) * cmax * cmax * M);
+        Eb.ensure(sizeof(double) * cmax * W * M);
+        c1e.ensure(sizeof(double) * kb * W * M);
+        cpe.ensure(sizeof(double) * kb * W * M);
+        c1t.ensure(sizeof(double) * kTS * W * M);
+        cpt.ensure(sizeof(double) * kTS * W * M);
+        CK(cudaMemsetAsync(c1t.p, 0, c1t.bytes, c.s));
+        stb.ensure(sizeof(CGState) * M);
+        for (int m = 0; m < M; ++m) {
+            hs[M + m] = CGState{};
+            hs[M + m].done = 1;  // empty slot
+            tr.Kt[m] = kt(m);
+            tr.t[m] = 0;
+            tw[m] = 0;
+        }
+        CK(cudaMemcpyAsync(stb.p, hs + M, sizeof(CGState) * M, cudaMemcpyHostToDevice, c.s));
+        krb.ensure(sizeof(T) * npad * kb);
+        repack_q4<T><<<c.grid_for(npad * kb, 256, 8), 256, 0, c.s>>>(Kb_colmajor, n, (int)kb, n, krb.template as<T>(),
+                                                                    npad);
+        c.check_launch();
+        nstep = kb <= 16 ? 4 : kb <= 32 ? 8 : 16;
+        if (nstep == 4) configure<4>();
+        else if (nstep == 8) configure<8>();
+        else configure<16>();
+        ntileT = npad / LT.TR;
+        ntileN = npad / LN.TR;
+        // stencil + dots: one slice of blocks per slot, about 8 blocks per SM over all slots
+        dim3 g0 = stencil_grid(op, 1);
+        kz = 1;
+        while ((long)g0.x * g0.y * ((op.N2 + kz - 1) / kz) * M > 16L * c.sms && kz < op.N2) kz *= 2;
+        const long nkc = (op.N2 + kz - 1) / kz;
+        gst = dim3(g0.x, g0.y, (unsigned)(nkc * M));
+        nbc = (long)g0.x * g0.y * nkc;
+        part_st.ensure(sizeof(double) * M * nbc * NV);
+        cnt_st.ensure(sizeof(unsigned) * M);
+        CK(cudaMemsetAsync(cnt_st.p, 0, sizeof(unsigned) * M, c.s));
+        gx = (int)std::max(1L, std::min<long>((n + 255) / 256, (long)c.sms));
+        part_tr.ensure(sizeof(double) * M * BD_NCH * gx * BD_TCH * W);
+        cnt_tr.ensure(sizeof(unsigned) * M * BD_NCH);
+        CK(cudaMemsetAsync(cnt_tr.p, 0, sizeof(unsigned) * M * BD_NCH, c.s));
+        c.sync();
+    }
+
+    // Slot m takes the solve whose space [Kb | Kt] / [Ub | Ut] (cj = kb + t columns)
+    // was factored last into Kr / Ur (ld n) and whose Gram is Gsp (cj x cj).
+    // r0 = P rhs by the selective CGS2 of recycled_cg; e = K^T rhs kept for finish().
+    void load(int m, const T* Kr, const T* Ur, long cj, const T* Gsp, const T* rhs, double tol, long maxit,
+              double scale) {
+        Ctx& c = *ctx;
+        const long t = cj - kb;
+        tw[m] = (int)t;
+        tr.t[m] = (int)t;
+        if (t > 0) {
+            CK(cudaMemcpy2DAsync(kt(m), sizeof(T) * npad, Kr + (size_t)kb * n, sizeof(T) * n, sizeof(T) * n, t,
+                                 cudaMemcpyDeviceToDevice, c.s));
+            CK(cudaMemcpy2DAsync(ut(m), sizeof(T) * npad, Ur + (size_t)kb * n, sizeof(T) * n, sizeof(T) * n, t,
+                                 cudaMemcpyDeviceToDevice, c.s));
+        }
+        CK(cudaMemcpyAsync(Gb.template as<T>() + (size_t)m * cmax * cmax, Gsp, sizeof(T) * cj * cj,
+                           cudaMemcpyDeviceToDevice, c.s));
+        launch_norms<T>(c, rhs, n, c.sc(3) + 8);
+        c.rflag.ensure(sizeof(CGState));
+        cgs2_global_selective<T, false>(c, Kr, n, cj, rhs, col(Rb, m), n, e_of(m), c.sc(1), c.sc(2), c.sc(3) + 8,
+                                        c.rflag.template as<CGState>());
+        for (DevBuf* b : {&Wb, &Pb, &Sb, &Yb}) CK(cudaMemsetAsync(col(*b, m), 0, sizeof(T) * npad, c.s));
+        CGState init{};
+        init.scale = scale;
+        init.tol = tol;
+        init.maxit = (int)std::min<long>(maxit, 0x7fffffff);
+        init.hist_cap = 0;
+        hs[M + m] = init;
+        CK(cudaMemcpyAsync(stb.template as<CGState>() + m, hs + M + m, sizeof(CGState), cudaMemcpyHostToDevice, c.s));
+    }
+
+    template <int NSTEP> void step() {
+        Ctx& c = *ctx;
+        CGState* st = stb.template as<CGState>();
+        const OpDev& op = *opd;
+        bcg_stencil_dots<T><<<gst, 256, 0, c.s>>>(op, Rb.template as<T>(), Wb.template as<T>(), npad, st,
+                                                  part_st.template as<double>(), cnt_st.template as<unsigned>(), kz);
+        c.check_launch();
+        const int gridT = (int)std::max(1L, std::min<long>(ntileT, (long)c.sms));
+        const int gridN = (int)std::max(1L, std::min<long>(ntileN, (long)c.sms));
+        bd_T_eig<T><<<gridT, TMA_THREADS, LT.total, c.s>>>(krb.template as<T>(), n, ntileT, LT, Wb.template as<T>(),
+                                                          npad, st, c.red(), c1e.template as<double>());
+        c.check_launch();
+        bd_T_trail<T><<<dim3(gx, M), 256, 0, c.s>>>(tr, Wb.template as<T>(), npad, n, st,
+                                                    part_tr.template as<double>(), cnt_tr.template as<unsigned>(),
+                                                    c1t.template as<double>(), kTS);
+        c.check_launch();
+        bd_coef<T><<<M, 128, sizeof(T) * cmax, c.s>>>(tr, (int)kb, kTS, st, c1e.template as<double>(),
+                                                      c1t.template as<double>(), Gb.template as<T>(), cmax * cmax,
+                                                      cpe.template as<double>(), cpt.template as<double>());
+        c.check_launch();
+        bd_N_eig<T, NSTEP><<<gridN, TMA_THREADS, LN.total, c.s>>>(krb.template as<T>(), n, ntileN, LN,
+                                                                 Wb.template as<T>(), npad, st,
+                                                                 cpe.template as<double>());
+        c.check_launch();
+        bd_update<T><<<dim3(gx, M), 256, 0, c.s>>>(tr, Wb.template as<T>(), Rb.template as<T>(), Pb.template as<T>(),
+                                                   Sb.template as<T>(), Yb.template as<T>(), npad, n, st,
+                                                   cpt.template as<double>(), kTS);
+        c.check_launch();
+    }
+    const OpDev* opd = nullptr;
+    void iterate(const OpDev& op, int steps) {
+        opd = &op;
+        for (int i = 0; i < steps; ++i) {
+            if (nstep == 4) step<4>();
+            else if (nstep == 8) step<8>();
+            else step<16>();
+        }
+    }
+    // states of all slots after the queued steps (synchronises the stream)
+    const CGState* poll() {
+        Ctx& c = *ctx;
+        CK(cudaMemcpyAsync(hs, stb.p, sizeof(CGState) * M, cudaMemcpyDeviceToHost, c.s));
+        c.sync();
+        return hs;
+    }
+    // y (padded column of the slot), image = A y (padded), g = y + U (e - K^T image)
+    void finish(int m, DevOp& op, const T* Kb_cm, const T* Ub_cm, T* g, T* y_out, T* image) {
+        Ctx& c = *ctx;
+        const long t = tw[m];
+        const long cj = kb + t;
+        const T* y = col(Yb, m);
+        double* c1 = c.sc(1);
+        double* c2 = c.sc(2);
+        launch_stencil<T>(c, op.d, y, n, nullptr, image, n, 1);
+        global_T<T, false>(c, Kb_cm, n, kb, image, n, c1);
+        if (t > 0) global_T<T, false>(c, kt(m), npad, t, image, n, c1 + kb * W);
+        launch_addsub(c, (int)(cj * W), c1, e_of(m), -1.0, c2);  // c2 = K^T image - e
+        if (t > 0) {
+            T* g1 = tmp.template as<T>();
+            global_N<T>(c, Ub_cm, n, kb, y, g1, n, c2);
+            global_N<T>(c, ut(m), npad, t, g1, g, n, c2 + kb * W);
+        } else {
+            global_N<T>(c, Ub_cm, n, kb, y, g, n, c2);
+        }
+        if (y_out) CK(cudaMemcpyAsync(y_out, y, sizeof(T) * n, cudaMemcpyDeviceToDevice, c.s));
+        // the slot is empty again
+        hs[M + m] = CGState{};
+        hs[M + m].done = 1;
+        tr.t[m] = 0;
+        tw[m] = 0;
+    }
+    void release(int m) {
+        Ctx& c = *ctx;
+        CK(cudaMemcpyAsync(stb.template as<CGState>() + m, hs + M + m, sizeof(CGState), cudaMemcpyHostToDevice, c.s));
+    }
+};
+
 struct BasisBase {
     virtual ~BasisBase() = default;
     RhsHook hook = nullptr;
@@ -1964,7 +2205,9 @@ template <class T> struct DevBasis : BasisBase {
     DevBuf G00, Gt, Gsp;                     // bilinear Gram of the eigen block / of the current space
     // process_system temporaries, persistent across systems (a multi-GB
     // free + malloc per system costs a device sync and up to ~1 s)
-    DevBuf ps_idx, ps_val, ps_Wc, ps_Rall, ps_Coef, ps_Cpk, ps_rj, ps_wn, ps_y, ps_g, ps_im;
+    DevBuf ps_idx, ps_val, ps_Wc, ps_Rall, ps_Coef, ps_Cpk, ps_rj, ps_wn, ps_y, ps_g, ps_im, ps_nrm;
+    std::unique_ptr<BatchedDeflated<T>> bd;  // batched solves of the independent right-hand sides
+    long stats_batched_rhs = 0;
     // grow-only with 25% slack
     static void grow_to(DevBuf& b, size_t bytes) {
         if (bytes > b.bytes) b.ensure(bytes + bytes / 4);
@@ -2507,7 +2750,116 @@ void process_system(DevBasis<T>& gb, DevOp& op, long nrhs, const long* bidx, con
     }
     DB::grow_to(wn, sizeof(T) * (nrhs + 8));
     lap(2);
+    // ---- independent tail (candidate cap reached: no right-hand side appends any more, so
+    // none changes the state another one starts from; basis.cpp:168-205 with append() == false).
+    // Their global checks run back to back and their correction solves BD_M at a time with
+    // the system's eigen block streamed once for all of them (bcg_defl.cuh). A slot that
+    // finishes is refilled with the next pending right-hand side.
+    auto batched_tail = [&](long j0) {
+        if (!gb.bd) gb.bd = std::make_unique<BatchedDeflated<T>>();
+        BatchedDeflated<T>& bd = *gb.bd;
+        constexpr int M = BatchedDeflated<T>::M;
+        const long rcur = gb.cols, nt = nrhs - j0;
+        long tmax = 0;
+        for (long j = j0; j < nrhs; ++j) tmax = std::max(tmax, (long)gb.spaces[j].size() - gb.ku);
+        if (gb.hook)
+            for (long j = j0; j < nrhs; ++j) {
+                c.sync();
+                if (gb.hook(gb.hook_user, system_index, j) != 0)
+                    throw SolverError("process_system: rhs hook aborted at system " + std::to_string(system_index) +
+                                      ", rhs " + std::to_string(j));
+            }
+        DB::grow_to(gb.ps_nrm, sizeof(double) * 8 * nt);
+        double* nrmd = gb.ps_nrm.template as<double>();
+        for (long j = j0; j < nrhs; ++j) {
+            T* rhs = Rall.template as<T>() + (size_t)j * npad;
+            if (rcur > r0) {  // project out this system's appended columns (in place)
+                DB::grow_to(wn, sizeof(T) * (rcur - r0));
+                row_gather_multi<T, true><<<c.grid_for(rcur - r0, 256, 1), 256, 0, c.s>>>(
+                    gb.Kp(), n, (int)r0, (int)(rcur - r0), idxd.template as<long>() + j,
+                    vald.template as<double>() + j, 1, 1.0, wn.template as<T>(), rcur - r0);
+                c.check_launch();
+                global_N<T>(c, gb.Kp() + (size_t)r0 * n, n, rcur - r0, rhs, rhs, n, (const double*)wn.p);
+            }
+            launch_norms<T>(c, rhs, n, nrmd + 8 * (j - j0));
+            if (Xdev) {
+                row_gather_multi<T, true><<<c.grid_for(rcur, 256, 1), 256, 0, c.s>>>(
+                    gb.Kp(), n, 0, (int)rcur, idxd.template as<long>() + j, vald.template as<double>() + j, 1, -1.0,
+                    Coef.template as<T>() + (size_t)j * capc, capc);
+                c.check_launch();
+            }
+        }
+        std::vector<double> hn(8 * nt);
+        CK(cudaMemcpyAsync(hn.data(), nrmd, sizeof(double) * 8 * nt, cudaMemcpyDeviceToHost, c.s));
+        c.sync();
+        lap(2);
+        std::vector<LogRow> rows;
+        std::vector<long> pending;
+        for (long j = j0; j < nrhs; ++j) {
+            rows.push_back(LogRow{system_index, (int)j, std::sqrt(hn[8 * (j - j0)]) / std::fabs(bval[j]), 0, false});
+            if (rows.back().init_relres <= tol) {
+                if (Xdev) CK(cudaMemsetAsync(Xdev + (size_t)j * n, 0, sizeof(T) * n, c.s));
+            } else {
+                pending.push_back(j);
+            }
+        }
+        if (!pending.empty()) {
+            bd.begin_system(c, op.d, gb.Kr.template as<T>(), gb.ku, tmax);
+            long slot_rhs[M];
+            for (int m = 0; m < M; ++m) slot_rhs[m] = -1;
+            size_t next = 0;
+            int active = 0;
+            auto fill = [&](int m) {
+                if (next >= pending.size()) return false;
+                const long j = pending[next++];
+                auto& idx = gb.spaces[j];
+                gb.factor_rhs_space(op, idx);
+                const T* Gsp = gb.space_gram((long)idx.size());
+                bd.load(m, gb.Kr.template as<T>(), gb.Ur.template as<T>(), (long)idx.size(), Gsp,
+                        Rall.template as<T>() + (size_t)j * npad, kInnerSafety * tol, maxit, std::fabs(bval[j]));
+                slot_rhs[m] = j;
+                ++active;
+                return true;
+            };
+            for (int m = 0; m < M; ++m) fill(m);
+            while (active > 0) {
+                bd.iterate(op.d, batch_steps());
+                const CGState* hs = bd.poll();
+                for (int m = 0; m < M; ++m) {
+                    const long j = slot_rhs[m];
+                    if (j < 0 || !hs[m].done) continue;
+                    if (!hs[m].converged)
+                        throw SolverError("process_system: correction solve failed at system " +
+                                          std::to_string(system_index) + ", rhs " + std::to_string(j));
+                    rows[j - j0].iterations = hs[m].it;
+                    inner_its += hs[m].it;
+                    T* Gj = Xdev ? Xdev + (size_t)j * n : gbuf.template as<T>();
+                    bd.finish(m, op, gb.Kr.template as<T>(), gb.Ur.template as<T>(), Gj, nullptr,
+                              imbuf.template as<T>());
+                    slot_rhs[m] = -1;
+                    --active;
+                    ++gb.stats_batched_rhs;
+                    if (!fill(m)) bd.release(m);
+                }
+            }
+        }
+        lap(4);
+        for (const LogRow& row : rows) {
+            VLOG(2, "system %d rhs %d: init_relres %.3e its %d appended 0 cols %ld (batched)", system_index, row.rhs,
+                 row.init_relres, row.iterations, gb.cols);
+            log.push_back(row);
+        }
+    };
     for (long j = 0; j < nrhs; ++j) {
+        if (batch_slots() && c.solver == 0 && use_one_pass_projection() && gb.cap > 0 && gb.cols >= gb.cap &&
+            nrhs - j >= 2) {
+            long tmax = 0;
+            for (long q = j; q < nrhs; ++q) tmax = std::max(tmax, (long)gb.spaces[q].size() - gb.ku);
+            if (BatchedDeflated<T>::supported(gb.ku, tmax)) {
+                batched_tail(j);
+                break;
+            }
+        }
         if (gb.hook) {
             c.sync();
             if (gb.hook(gb.hook_user, system_index, j) != 0)
