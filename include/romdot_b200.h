@@ -117,6 +117,12 @@ int rd_basis_create(rd_ctx* ctx, int dtype, long n, long ku, long nrhs, const vo
 void rd_basis_destroy(rd_basis* b);
 long rd_basis_cols(rd_basis* b);
 long rd_basis_eig_block(rd_basis* b);
+/* Correction solves of rd_process_system / rd_per_rhs_solve_system that ran in the
+ * batched iteration so far (8 independent right-hand sides of a system in flight,
+ * the system's eigen block streamed once for all of them): the right-hand sides
+ * after the candidate cap stopped the appends, where the reference's loop
+ * (src/basis.cpp:168-205) leaves them independent. ROMDOT_BATCH=0 disables it. */
+long rd_basis_batched_solves(rd_basis* b);
 /* 1 once the image factor (K_img, R, W) exists, i.e. after the first refresh;
  * before it the reference's Kimg_/R_ are empty (include/romdot/basis.hpp:63). */
 int rd_basis_factored(rd_basis* b);

@@ -1,4 +1,5 @@
 """Build the in-tree CUDA library libromdot_b200.so for sm_100a (nvcc)."""
+import glob
 import os
 import subprocess
 import sys
@@ -7,8 +8,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 SO = os.path.join(HERE, "libromdot_b200.so")
 SRCS = [os.path.join(HERE, "csrc", f) for f in ("romdot.cu",)]
-DEPS = SRCS + [os.path.join(HERE, "csrc", f) for f in ("common.cuh", "kernels.cuh", "dense.cuh", "ts_tma.cuh", "cg_fused.cuh", "rom.cuh", "stencil_tma.cuh")] + \
-    [os.path.join(ROOT, "include", "romdot_b200.h")]
+DEPS = SRCS + sorted(glob.glob(os.path.join(HERE, "csrc", "*.cuh"))) + [os.path.join(ROOT, "include", "romdot_b200.h")]
 
 NVCC_FLAGS = ["-O3", "-std=c++17", "-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo",
               "-Xcompiler", "-fPIC", "-shared", "--expt-relaxed-constexpr", "-Xptxas", "-v"]

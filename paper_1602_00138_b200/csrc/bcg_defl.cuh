@@ -282,29 +282,51 @@ __global__ void __launch_bounds__(TMA_THREADS, 1)
     }
 }
 
+// Partial dots of TW trailing columns against w over this block's rows: one
+// row per thread and trip, its 1 + TW loads issued before the first FMA (a
+// double2 is four registers: wider per-thread batches cost occupancy, and the
+// pass needs resident warps more than it needs loads per warp).
+template <class T, int TW>
+__device__ __forceinline__ void bd_trail_dots(const T* __restrict__ Kt, long ld, const T* __restrict__ w, long n,
+                                              T (&acc)[BD_TCH]) {
+    const long stride = (long)gridDim.x * blockDim.x;
+    for (long row = blockIdx.x * (long)blockDim.x + threadIdx.x; row < n; row += stride) {
+        const T wv = w[row];
+        T kv[TW];
+#pragma unroll
+        for (int q = 0; q < TW; ++q) kv[q] = Kt[(size_t)q * ld + row];
+#pragma unroll
+        for (int q = 0; q < TW; ++q) acc[q] = Sc<T>::fma(kv[q], wv, acc[q]);
+    }
+}
+
 // C1t[m][0..t_m) = Kt_m^T W[:, m]: blockIdx.y = slot, thread per row, chunks of
 // BD_TCH columns; per (slot, chunk) deterministic reduction over the blocks.
 template <class T>
-__global__ void __launch_bounds__(256) bd_T_trail(BDTrail<T> tr, const T* __restrict__ Wv, long ld, long n,
+__global__ void __launch_bounds__(256, 4) bd_T_trail(BDTrail<T> tr, const T* __restrict__ Wv, long ld, long n,
                                                   const CGState* __restrict__ st, double* partials,
                                                   unsigned* counters, double* __restrict__ out, int tcap) {
     constexpr int W = Sc<T>::W;
     const int m = blockIdx.y;
     if (st[m].done) return;
     const int t = tr.t[m];
-    const T* __restrict__ Kt = tr.Kt[m];
     const T* __restrict__ w = Wv + (size_t)m * ld;
     __shared__ double s_red[32];
     __shared__ double s_vals[BD_TCH * W];
     for (int ch = 0, t0 = 0; t0 < t; ++ch, t0 += BD_TCH) {
+        const T* __restrict__ Kt = tr.Kt[m] + (size_t)t0 * ld;
         T acc[BD_TCH];
 #pragma unroll
         for (int q = 0; q < BD_TCH; ++q) acc[q] = Sc<T>::zero();
-        for (long row = blockIdx.x * (long)blockDim.x + threadIdx.x; row < n; row += (long)gridDim.x * blockDim.x) {
-            const T wv = w[row];
-#pragma unroll
-            for (int q = 0; q < BD_TCH; ++q)
-                if (t0 + q < t) acc[q] = Sc<T>::fma(Kt[(size_t)(t0 + q) * ld + row], wv, acc[q]);
+        switch (min(t - t0, BD_TCH)) {
+            case 1: bd_trail_dots<T, 1>(Kt, ld, w, n, acc); break;
+            case 2: bd_trail_dots<T, 2>(Kt, ld, w, n, acc); break;
+            case 3: bd_trail_dots<T, 3>(Kt, ld, w, n, acc); break;
+            case 4: bd_trail_dots<T, 4>(Kt, ld, w, n, acc); break;
+            case 5: bd_trail_dots<T, 5>(Kt, ld, w, n, acc); break;
+            case 6: bd_trail_dots<T, 6>(Kt, ld, w, n, acc); break;
+            case 7: bd_trail_dots<T, 7>(Kt, ld, w, n, acc); break;
+            default: bd_trail_dots<T, 8>(Kt, ld, w, n, acc); break;
         }
 #pragma unroll
         for (int q = 0; q < BD_TCH; ++q) {
@@ -348,15 +370,36 @@ __global__ void __launch_bounds__(128) bd_coef(BDTrail<T> tr, int kb, int tcap, 
     __syncthreads();
     const T* Gm = G + (size_t)m * gstride;
     for (int j = threadIdx.x; j < cj; j += blockDim.x) {
-        const T* gc = Gm + (size_t)j * cj;
-        T acc = Sc<T>::zero();
-        for (int i = 0; i < cj; ++i) acc = Sc<T>::fma(gc[i], c1[i], acc);
+        // G is symmetric: walk column j (consecutive threads read consecutive addresses)
+        T a0 = Sc<T>::zero(), a1 = Sc<T>::zero(), a2 = Sc<T>::zero(), a3 = Sc<T>::zero();
+        int i = 0;
+        for (; i + 3 < cj; i += 4) {
+            a0 = Sc<T>::fma(Gm[(size_t)i * cj + j], c1[i], a0);
+            a1 = Sc<T>::fma(Gm[(size_t)(i + 1) * cj + j], c1[i + 1], a1);
+            a2 = Sc<T>::fma(Gm[(size_t)(i + 2) * cj + j], c1[i + 2], a2);
+            a3 = Sc<T>::fma(Gm[(size_t)(i + 3) * cj + j], c1[i + 3], a3);
+        }
+        for (; i < cj; ++i) a0 = Sc<T>::fma(Gm[(size_t)i * cj + j], c1[i], a0);
+        const T acc = Sc<T>::add(Sc<T>::add(a0, a1), Sc<T>::add(a2, a3));
         const T v = Sc<T>::sub(Sc<T>::scale(c1[j], 2.0), acc);
         if (j < kb)
             Sc<T>::put(cpe + ((size_t)m * kb + j) * W, v);
         else
             Sc<T>::put(cpt + ((size_t)m * tcap + j - kb) * W, v);
     }
+}
+
+// Rows of one trip of bd_update with a compile-time trailing width (all loads
+// of the trip issued up front).
+template <class T, int TW>
+__device__ __forceinline__ T bd_trail_row(const T* __restrict__ Kt, long ld, long row, const T* s_c) {
+    T kv[TW > 0 ? TW : 1];
+#pragma unroll
+    for (int q = 0; q < TW; ++q) kv[q] = Kt[(size_t)q * ld + row];
+    T sum = Sc<T>::zero();
+#pragma unroll
+    for (int q = 0; q < TW; ++q) sum = Sc<T>::fma(kv[q], s_c[q], sum);
+    return sum;
 }
 
 // q = W[:, m] - Kt_m c't_m, then the CG / COCG vector updates of slot m
@@ -377,15 +420,26 @@ __global__ void __launch_bounds__(256) bd_update(BDTrail<T> tr, const T* __restr
     const T alpha = ld2<T>(sc->alpha), beta = ld2<T>(sc->beta);
     const size_t off = (size_t)m * ld;
     for (long row = blockIdx.x * (long)blockDim.x + threadIdx.x; row < n; row += (long)gridDim.x * blockDim.x) {
+        const T wv = Wv[off + row], rv = R[off + row], pv = Pv[off + row], sv = Sv[off + row], yv = Y[off + row];
         T sum = Sc<T>::zero();
-        for (int q = 0; q < t; ++q) sum = Sc<T>::fma(Kt[(size_t)q * ld + row], s_c[q], sum);
-        const T q = Sc<T>::sub(Wv[off + row], sum);
-        const T rv = R[off + row];
-        const T pn = Sc<T>::fma(beta, Pv[off + row], rv);
-        const T sn = Sc<T>::fma(beta, Sv[off + row], q);
+        int t0 = 0;
+        for (; t0 + 8 <= t; t0 += 8) sum = Sc<T>::add(sum, bd_trail_row<T, 8>(Kt + (size_t)t0 * ld, ld, row, s_c + t0));
+        switch (t - t0) {
+            case 1: sum = Sc<T>::add(sum, bd_trail_row<T, 1>(Kt + (size_t)t0 * ld, ld, row, s_c + t0)); break;
+            case 2: sum = Sc<T>::add(sum, bd_trail_row<T, 2>(Kt + (size_t)t0 * ld, ld, row, s_c + t0)); break;
+            case 3: sum = Sc<T>::add(sum, bd_trail_row<T, 3>(Kt + (size_t)t0 * ld, ld, row, s_c + t0)); break;
+            case 4: sum = Sc<T>::add(sum, bd_trail_row<T, 4>(Kt + (size_t)t0 * ld, ld, row, s_c + t0)); break;
+            case 5: sum = Sc<T>::add(sum, bd_trail_row<T, 5>(Kt + (size_t)t0 * ld, ld, row, s_c + t0)); break;
+            case 6: sum = Sc<T>::add(sum, bd_trail_row<T, 6>(Kt + (size_t)t0 * ld, ld, row, s_c + t0)); break;
+            case 7: sum = Sc<T>::add(sum, bd_trail_row<T, 7>(Kt + (size_t)t0 * ld, ld, row, s_c + t0)); break;
+            default: break;
+        }
+        const T q = Sc<T>::sub(wv, sum);
+        const T pn = Sc<T>::fma(beta, pv, rv);
+        const T sn = Sc<T>::fma(beta, sv, q);
         Pv[off + row] = pn;
         Sv[off + row] = sn;
-        Y[off + row] = Sc<T>::fma(alpha, pn, Y[off + row]);
+        Y[off + row] = Sc<T>::fma(alpha, pn, yv);
         R[off + row] = Sc<T>::sub(rv, Sc<T>::mul(alpha, sn));
     }
     if (blockIdx.x == 0 && threadIdx.x == 0) {

@@ -2822,7 +2822,10 @@ void process_system(DevBasis<T>& gb, DevOp& op, long nrhs, const long* bidx, con
                 return true;
             };
             for (int m = 0; m < M; ++m) fill(m);
+            long steps = 0, slot_steps = 0;
             while (active > 0) {
+                steps += batch_steps();
+                slot_steps += (long)active * batch_steps();
                 bd.iterate(op.d, batch_steps());
                 const CGState* hs = bd.poll();
                 for (int m = 0; m < M; ++m) {
@@ -2842,6 +2845,8 @@ void process_system(DevBasis<T>& gb, DevOp& op, long nrhs, const long* bidx, con
                     if (!fill(m)) bd.release(m);
                 }
             }
+            VLOG(1, "system %d batched tail: %zu solves, %ld steps of %d slots, %.2f slots busy on average",
+                 system_index, pending.size(), steps, M, steps ? (double)slot_steps / steps : 0.0);
         }
         lap(4);
         for (const LogRow& row : rows) {
@@ -3963,6 +3968,11 @@ int rd_basis_factored(rd_basis* b) {
 long rd_basis_eig_block(rd_basis* b) {
     long v = 0;
     BASIS_DISPATCH(b, v = B.ku);
+    return v;
+}
+long rd_basis_batched_solves(rd_basis* b) {
+    long v = 0;
+    BASIS_DISPATCH(b, v = B.stats_batched_rhs);
     return v;
 }
 void* rd_basis_device_ptr(rd_basis* b, int which) {

@@ -30,7 +30,7 @@ EXPORTS = [
     "rd_ctx_create", "rd_ctx_destroy", "rd_last_error", "rd_ctx_sync", "rd_ctx_mark", "rd_ctx_elapsed_ms",
     "rd_ctx_launches", "rd_ctx_set_solver", "rd_ctx_get_solver", "rd_ctx_stream", "rd_ctx_profile", "rd_ctx_prof_get", "rd_op_create", "rd_op_destroy", "rd_op_set_fields", "rd_op_apply",
     "rd_op_lam_max", "rd_recycled_solve", "rd_recycle_space_from_raw", "rd_initial_solutions",
-    "rd_smallest_eigenpairs", "rd_basis_create", "rd_basis_destroy", "rd_basis_cols", "rd_basis_factored", "rd_basis_eig_block",
+    "rd_smallest_eigenpairs", "rd_basis_create", "rd_basis_destroy", "rd_basis_cols", "rd_basis_factored", "rd_basis_eig_block", "rd_basis_batched_solves",
     "rd_basis_get", "rd_basis_device_ptr", "rd_basis_markers", "rd_basis_space", "rd_basis_refresh",
     "rd_basis_append", "rd_basis_solve_projected", "rd_process_system", "rd_rrqr", "rd_bench_projection",
     "rd_bench_stencil", "rd_residual_norms", "rd_basis_compress", "rd_rom_create", "rd_rom_destroy",
@@ -121,6 +121,8 @@ def load_library(path: Optional[str] = None):
     L.rd_basis_factored.restype = C.c_int
     L.rd_basis_eig_block.argtypes = [vp]
     L.rd_basis_eig_block.restype = C.c_long
+    L.rd_basis_batched_solves.argtypes = [vp]
+    L.rd_basis_batched_solves.restype = C.c_long
     L.rd_basis_get.argtypes = [vp, C.c_int, vp]
     L.rd_basis_device_ptr.argtypes = [vp, C.c_int]
     L.rd_basis_device_ptr.restype = vp
@@ -465,6 +467,11 @@ class GlobalBasis:
     @property
     def eig_block(self) -> int:
         return load_library().rd_basis_eig_block(self.h)
+
+    @property
+    def batched_solves(self) -> int:
+        """Correction solves that ran in the batched iteration (independent RHS after the cap)."""
+        return load_library().rd_basis_batched_solves(self.h)
 
     def _get(self, which, shape):
         out = np.zeros(shape, dtype=self.dtype, order="F")

@@ -541,3 +541,69 @@ assert checked > 1000 and bad == 0
     env = dict(os.environ, ROMDOT_FUSED_CHECK="1")
     out = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=900)
     assert out.returncode == 0, (out.stdout[-2000:], out.stderr[-3000:])
+
+
+# ---- batched correction solves after the candidate cap (bcg_defl.cuh) ----
+# Once the cap stops the appends the reference's loop (basis.cpp:168-205) leaves the
+# remaining right-hand sides independent; the device then runs 8 solves at a time with
+# the system's eigen block streamed once for all of them. Same BuildLog as the one-solve
+# path and as the CPU checker.
+@pytest.mark.parametrize("d,N,k,cplx,nsd,cap_extra", [
+    (3, 20, 12, True, (2, 3), 4),     # complex, eigen block 12 (2 column tiles, one ragged), 12 RHS
+    (2, 48, 20, False, (9,), 6),      # real 2D, eigen block 20, 18 RHS (more than two batches)
+    (3, 24, 40, True, (3, 3), 10),    # complex, eigen block 40 (DMMA steps 16 with a ragged tail), 18 RHS
+    (2, 40, 6, True, (5,), 3),        # one ragged column tile
+])
+def test_batched_tail_matches_one_solve_path_and_oracle(rd, monkeypatch, d, N, k, cplx, nsd, cap_extra):
+    nrhs = 2 * int(np.prod(nsd))
+    c = P.ProblemConfig("bt", d=d, N=N, n_src=nsd, n_det=nsd, m_rbf=4, n_points=2,
+                        omegas=(0.0, 0.1) if cplx else (0.0,), k=k, complex=cplx, cap=k + nrhs + cap_extra)
+    g, lay = c.grid, c.layout()
+    U0, X0 = _shared_seed(c, g, lay)
+    B = lay.dense(g.n, c.dtype)
+    runs = {}
+    for mode in ("0", "1"):
+        monkeypatch.setenv("ROMDOT_BATCH", mode)
+        gb = rd.GlobalBasis(U0, X0, c.cap)
+        out = []
+        for s, (pt, w) in enumerate(c.systems(), start=1):
+            out.append(rd.process_system(gb, rd.SchurOperator(g, c.fields(pt, w), c.dtype), lay, c.tol, s))
+        runs[mode] = (out, gb.batched_solves, gb.cols)
+    (seq, nb0, cols0), (bat, nb1, cols1) = runs["0"], runs["1"]
+    assert nb0 == 0 and nb1 >= 8, (nb0, nb1)         # the batched iteration really ran
+    assert cols0 == cols1 == c.cap
+    gbo = orc.GlobalBasis(U0, X0, c.cap)
+    for s, (pt, w) in enumerate(c.systems(), start=1):
+        a, b = seq[s - 1], bat[s - 1]
+        op_o = orc.Operator.grid(g, c.fields(pt, w), c.dtype)
+        po = orc.process_system(gbo, op_o, lay, c.tol, s)
+        for ra, rb, ro in zip(a.log, b.log, po.log):
+            assert (ra.system, ra.rhs, ra.appended) == (rb.system, rb.rhs, rb.appended) == (ro.system, ro.rhs, ro.appended)
+            assert abs(ra.iterations - rb.iterations) <= 1 and abs(rb.iterations - ro.iterations) <= 2, (ra, rb, ro)
+            assert rb.init_relres == pytest.approx(ra.init_relres, rel=1e-9, abs=1e-14)
+            assert rb.init_relres == pytest.approx(ro.init_relres, rel=1e-6, abs=1e-13)
+        assert np.linalg.norm(b.X - a.X) <= 1e-9 * np.linalg.norm(a.X)
+        assert np.linalg.norm(b.X - po.X) <= 1e-6 * np.linalg.norm(po.X)
+        R = op_o.apply(b.X) - B
+        assert (np.linalg.norm(R, axis=0) <= c.tol * np.linalg.norm(B, axis=0)).all()
+
+
+def test_batched_tail_is_bitwise_deterministic(rd):
+    """Two capped builds give byte-identical solutions and BuildLogs (test_basis.cpp:210-223):
+    a slot's arithmetic does not depend on what the other slots hold."""
+    c = P.CONFIGS["T3c"]
+    g, lay = c.grid, c.layout()
+    U0, X0 = _shared_seed(c, g, lay)
+    outs = []
+    for _ in range(2):
+        gb = rd.GlobalBasis(U0, X0, c.cap)
+        xs, rows = [], []
+        for s, (pt, w) in enumerate(c.systems(), start=1):
+            pr = rd.process_system(gb, rd.SchurOperator(g, c.fields(pt, w), c.dtype), lay, c.tol, s)
+            xs.append(pr.X)
+            rows += [(r.system, r.rhs, r.init_relres, r.iterations, r.appended) for r in pr.log]
+        outs.append((xs, rows, gb.batched_solves))
+    assert outs[0][2] > 0
+    assert outs[0][1] == outs[1][1]
+    for xa, xb in zip(outs[0][0], outs[1][0]):
+        assert np.array_equal(xa, xb)
