@@ -31,7 +31,7 @@
 
 namespace rd {
 
-constexpr int BD_M = 8;       // slots in flight
+constexpr int BD_M = 16;      // slots in flight (two 8-slot DMMA column groups)
 constexpr int BD_TCH = 8;     // trailing columns per bd_T_trail chunk
 constexpr int BD_NCH = 3;     // chunks: trailing width <= 24
 
@@ -44,6 +44,7 @@ struct BDLayout {
     int TR, S, kb;
     uint32_t tile_bytes, x_bytes, stride_k, stride_x;
     uint32_t off_k, off_x, off_vals, off_bar, total;
+    uint32_t cstride;  // N pass: elements between the slots' coefficient rows in shared memory
 };
 
 // TR rows per tile; xpad bytes between the slots' W tiles (bank spread of the
@@ -63,8 +64,10 @@ template <class T> inline BDLayout bd_layout(int kb, int TR, int S, uint32_t xpa
     o += L.stride_k * S;
     L.off_x = o;
     o += al(L.stride_x * BD_M) * S;
-    L.off_vals = o;
-    o += al((uint32_t)BD_M * kb * 2 * sizeof(double));
+    L.off_vals = o;  // T pass: the block's M kb partial sums; N pass: the coefficients (padded rows)
+    // N pass rows cover every column the unrolled DMMA steps touch (4, 8 or 16 steps of 4)
+    L.cstride = (kb <= 16 ? 16u : kb <= 32 ? 32u : 64u) + 4u;
+    o += al((uint32_t)BD_M * L.cstride * 2 * sizeof(double));
     L.off_bar = o;
     o += 2 * S * 8;
     L.total = o;
@@ -159,8 +162,10 @@ __global__ void __launch_bounds__(TMA_THREADS, 1)
         const int j0 = wid * 8;
         const bool warp_on = j0 < kb;
         const bool colok = j0 + fi < kb;
-        const bool bact = act >> fi & 1u;  // B fragment column = slot fi
-        BDAcc<T> acc;
+        // B fragment columns = slots fi and 8 + fi (two 8-slot groups share the A fragment)
+        const bool bact0 = act >> fi & 1u, bact1 = act >> (8 + fi) & 1u;
+        const bool hi = (act >> 8) != 0u;
+        BDAcc<T> acc0, acc1;
         const int nstep = TR >> 2;
         long k = 0;
         for (long t = blockIdx.x; t < ntile; t += gridDim.x, ++k) {
@@ -169,13 +174,25 @@ __global__ void __launch_bounds__(TMA_THREADS, 1)
             mbar_wait(&full[stage], use & 1u);
             if (warp_on) {
                 const T* ks = reinterpret_cast<const T*>(smem + L.off_k + stage * L.stride_k) + (j0 + fi) * 4 + fk;
-                const T* xs =
-                    reinterpret_cast<const T*>(smem + L.off_x + (size_t)stage * xstage + fi * L.stride_x) + fk;
+                const unsigned char* xb = smem + L.off_x + (size_t)stage * xstage;
+                const T* xs0 = reinterpret_cast<const T*>(xb + fi * L.stride_x) + fk;
+                const T* xs1 = reinterpret_cast<const T*>(xb + (8 + fi) * L.stride_x) + fk;
+                if (hi) {
+#pragma unroll 4
+                    for (int s = 0; s < nstep; ++s) {
+                        const T a = colok ? ks[(size_t)s * 4 * kb] : Sc<T>::zero();
+                        const T b0 = bact0 ? xs0[4 * s] : Sc<T>::zero();
+                        const T b1 = bact1 ? xs1[4 * s] : Sc<T>::zero();
+                        acc0.mma(a, b0);
+                        acc1.mma(a, b1);
+                    }
+                } else {
 #pragma unroll 8
-                for (int s = 0; s < nstep; ++s) {
-                    const T a = colok ? ks[(size_t)s * 4 * kb] : Sc<T>::zero();
-                    const T b = bact ? xs[4 * s] : Sc<T>::zero();
-                    acc.mma(a, b);
+                    for (int s = 0; s < nstep; ++s) {
+                        const T a = colok ? ks[(size_t)s * 4 * kb] : Sc<T>::zero();
+                        const T b0 = bact0 ? xs0[4 * s] : Sc<T>::zero();
+                        acc0.mma(a, b0);
+                    }
                 }
             }
             __syncwarp();
@@ -185,7 +202,8 @@ __global__ void __launch_bounds__(TMA_THREADS, 1)
 #pragma unroll
             for (int e = 0; e < 2; ++e) {
                 const int m = 2 * fk + e;
-                Sc<T>::put(vals + ((size_t)m * kb + j0 + fi) * W, acc.get(e));
+                Sc<T>::put(vals + ((size_t)m * kb + j0 + fi) * W, acc0.get(e));
+                Sc<T>::put(vals + ((size_t)(8 + m) * kb + j0 + fi) * W, acc1.get(e));
             }
         }
     }
@@ -225,6 +243,13 @@ __global__ void __launch_bounds__(TMA_THREADS, 1)
     const unsigned act = s_act;
     if (!act) return;
     const int nact = __popc(act);
+    // coefficient rows of all slots (zero for finished slots and padded columns)
+    T* cs = reinterpret_cast<T*>(smem + L.off_vals);
+    for (int e = tid; e < M * (int)L.cstride; e += blockDim.x) {
+        const int m = e / (int)L.cstride, col = e - m * (int)L.cstride;
+        cs[e] = (col < kb && (act >> m & 1u)) ? Sc<T>::get(cpe + ((size_t)m * kb + col) * W) : Sc<T>::zero();
+    }
+    __syncthreads();
     if (wid == TMA_CONSUMERS / 32) {
         if (lane == 0) {
             long k = 0;
@@ -243,13 +268,11 @@ __global__ void __launch_bounds__(TMA_THREADS, 1)
         return;
     }
     const int fi = lane >> 2, fk = lane & 3;
-    // B fragments: coefficient of column 4 s + fk for slot fi
-    T bf[NSTEP];
-#pragma unroll
-    for (int s = 0; s < NSTEP; ++s) {
-        const int col = 4 * s + fk;
-        bf[s] = (col < kb && (act >> fi & 1u)) ? Sc<T>::get(cpe + ((size_t)fi * kb + col) * W) : Sc<T>::zero();
-    }
+    const bool hi = (act >> 8) != 0u;
+    // B fragments (coefficient of column 4 s + fk for slots fi and 8 + fi) are read from the
+    // staged coefficient rows at every step: 2 x NSTEP register copies would not fit
+    const T* cf0 = cs + (size_t)fi * L.cstride + fk;
+    const T* cf1 = cs + (size_t)(8 + fi) * L.cstride + fk;
     const int ngroup = TR >> 3;
     long k = 0;
     for (long t = blockIdx.x; t < ntile; t += gridDim.x, ++k) {
@@ -261,19 +284,31 @@ __global__ void __launch_bounds__(TMA_THREADS, 1)
         for (int g = wid; g < ngroup; g += TMA_CONSUMERS / 32) {
             const int r = 8 * g + fi;
             const T* ks = Ks + (size_t)(r >> 2) * 4 * kb + (r & 3) + 4 * fk;
-            BDAcc<T> acc;
+            BDAcc<T> acc0, acc1;
+            if (hi) {
 #pragma unroll
-            for (int s = 0; s < NSTEP; ++s) {
-                const T a = (4 * s + fk < kb) ? ks[16 * s] : Sc<T>::zero();
-                acc.mma(a, bf[s]);
+                for (int s = 0; s < NSTEP; ++s) {
+                    const T a = (4 * s + fk < kb) ? ks[16 * s] : Sc<T>::zero();
+                    acc0.mma(a, cf0[4 * s]);
+                    acc1.mma(a, cf1[4 * s]);
+                }
+            } else {
+#pragma unroll
+                for (int s = 0; s < NSTEP; ++s) {
+                    const T a = (4 * s + fk < kb) ? ks[16 * s] : Sc<T>::zero();
+                    acc0.mma(a, cf0[4 * s]);
+                }
             }
             const long row = t * TR + r;
 #pragma unroll
             for (int e = 0; e < 2; ++e) {
-                const int m = 2 * fk + e;
-                if ((act >> m & 1u) && row < n) {
-                    const T wv = reinterpret_cast<const T*>(xb + m * L.stride_x)[r];
-                    Wv[(size_t)m * ld + row] = Sc<T>::sub(wv, acc.get(e));
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    const int m = 8 * h + 2 * fk + e;
+                    if ((act >> m & 1u) && row < n) {
+                        const T wv = reinterpret_cast<const T*>(xb + m * L.stride_x)[r];
+                        Wv[(size_t)m * ld + row] = Sc<T>::sub(wv, h ? acc1.get(e) : acc0.get(e));
+                    }
                 }
             }
         }

@@ -1953,6 +1953,10 @@ inline int batch_slots() {  // read per call so a test can compare both paths in
     const char* e = std::getenv("ROMDOT_BATCH");
     return e ? std::atoi(e) : 1;
 }
+inline int batch_width() {  // slots used of BD_M (A/B: ROMDOT_BATCH_SLOTS=8)
+    const char* e = std::getenv("ROMDOT_BATCH_SLOTS");
+    return std::max(1, std::min(BD_M, e ? std::atoi(e) : BD_M));
+}
 inline int batch_steps() {
     static const int b = [] {
         const char* e = std::getenv("ROMDOT_BATCH_STEPS");
@@ -2809,25 +2813,44 @@ void process_system(DevBasis<T>& gb, DevOp& op, long nrhs, const long* bidx, con
             for (int m = 0; m < M; ++m) slot_rhs[m] = -1;
             size_t next = 0;
             int active = 0;
+            double t_space = 0, t_gram = 0, t_load = 0, t_fin = 0, t_iter = 0;  // ROMDOT_VERBOSE >= 1
+            auto tick = [&](double& acc, auto&& fn) {
+                if (!timing) {
+                    fn();
+                    return;
+                }
+                c.sync();
+                const auto a = std::chrono::steady_clock::now();
+                fn();
+                c.sync();
+                acc += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - a).count();
+            };
             auto fill = [&](int m) {
                 if (next >= pending.size()) return false;
                 const long j = pending[next++];
                 auto& idx = gb.spaces[j];
-                gb.factor_rhs_space(op, idx);
-                const T* Gsp = gb.space_gram((long)idx.size());
-                bd.load(m, gb.Kr.template as<T>(), gb.Ur.template as<T>(), (long)idx.size(), Gsp,
-                        Rall.template as<T>() + (size_t)j * npad, kInnerSafety * tol, maxit, std::fabs(bval[j]));
+                tick(t_space, [&] { gb.factor_rhs_space(op, idx); });
+                const T* Gsp = nullptr;
+                tick(t_gram, [&] { Gsp = gb.space_gram((long)idx.size()); });
+                tick(t_load, [&] {
+                    bd.load(m, gb.Kr.template as<T>(), gb.Ur.template as<T>(), (long)idx.size(), Gsp,
+                            Rall.template as<T>() + (size_t)j * npad, kInnerSafety * tol, maxit, std::fabs(bval[j]));
+                });
                 slot_rhs[m] = j;
                 ++active;
                 return true;
             };
-            for (int m = 0; m < M; ++m) fill(m);
+            const int mslots = batch_width();
+            for (int m = 0; m < mslots; ++m) fill(m);
             long steps = 0, slot_steps = 0;
             while (active > 0) {
                 steps += batch_steps();
                 slot_steps += (long)active * batch_steps();
-                bd.iterate(op.d, batch_steps());
-                const CGState* hs = bd.poll();
+                const CGState* hs = nullptr;
+                tick(t_iter, [&] {
+                    bd.iterate(op.d, batch_steps());
+                    hs = bd.poll();
+                });
                 for (int m = 0; m < M; ++m) {
                     const long j = slot_rhs[m];
                     if (j < 0 || !hs[m].done) continue;
@@ -2837,16 +2860,21 @@ void process_system(DevBasis<T>& gb, DevOp& op, long nrhs, const long* bidx, con
                     rows[j - j0].iterations = hs[m].it;
                     inner_its += hs[m].it;
                     T* Gj = Xdev ? Xdev + (size_t)j * n : gbuf.template as<T>();
-                    bd.finish(m, op, gb.Kr.template as<T>(), gb.Ur.template as<T>(), Gj, nullptr,
-                              imbuf.template as<T>());
+                    tick(t_fin, [&] {
+                        bd.finish(m, op, gb.Kr.template as<T>(), gb.Ur.template as<T>(), Gj, nullptr,
+                                  imbuf.template as<T>());
+                    });
                     slot_rhs[m] = -1;
                     --active;
                     ++gb.stats_batched_rhs;
                     if (!fill(m)) bd.release(m);
                 }
             }
-            VLOG(1, "system %d batched tail: %zu solves, %ld steps of %d slots, %.2f slots busy on average",
-                 system_index, pending.size(), steps, M, steps ? (double)slot_steps / steps : 0.0);
+            VLOG(1,
+                 "system %d batched tail: %zu solves, %ld steps of %d slots, %.2f slots busy on average | ms: spaces "
+                 "%.1f space-gram %.1f load %.1f iterate %.1f (%.3f per step) finish %.1f",
+                 system_index, pending.size(), steps, M, steps ? (double)slot_steps / steps : 0.0, t_space, t_gram,
+                 t_load, t_iter, steps ? t_iter / steps : 0.0, t_fin);
         }
         lap(4);
         for (const LogRow& row : rows) {
