@@ -9,7 +9,8 @@
 // then q = A r - K_j c'); with M solves in flight the shared block is streamed
 // once for all of them, so its bytes per solve-iteration fall by M:
 //
-//   bcg_stencil_dots (kernels.cuh)  W[:, m] = A R[:, m], merged dots, alpha/beta   per slot
+//   stencil_tma   W[:, m] = A R[:, m]        all slots, coefficient planes read once
+//   bd_dots       {r^T r, r^T w, r^H r}, alpha / beta / convergence per slot
 //   bd_T_eig      C1e[m] = Kb^T W[:, m]      Kb: 1D bulk TMA ring, once for all m
 //   bd_T_trail    C1t[m] = Kt_m^T W[:, m]
 //   bd_coef       c'_m = 2 c1_m - G_m c1_m   (Gram-corrected second CGS coefficient)
@@ -315,6 +316,67 @@ __global__ void __launch_bounds__(TMA_THREADS, 1)
         __syncwarp();
         if (lane == 0) mbar_arrive(&empty[stage]);
     }
+}
+
+// Merged reduction {r^T r, r^T w, r^H r} of every running slot (blockIdx.y) and,
+// in the slot's last block, its scalar recurrence step (alpha, beta, convergence:
+// cg_recurrence). w = A r comes from the multi-column TMA stencil, which reads the
+// coefficient planes once for all slots.
+template <class T>
+__global__ void __launch_bounds__(256, 4) bd_dots(const T* __restrict__ R, const T* __restrict__ Wv, long ld, long n,
+                                                  CGState* st, double* partials, unsigned* counters) {
+    constexpr int W = Sc<T>::W;
+    constexpr int NV = 2 * W + 1;
+    const int m = blockIdx.y;
+    CGState* sc = st + m;
+    if (sc->done) return;
+    const T* __restrict__ r = R + (size_t)m * ld;
+    const T* __restrict__ w = Wv + (size_t)m * ld;
+    T g = Sc<T>::zero(), dl = Sc<T>::zero();
+    double h = 0.0;
+    const long stride = (long)gridDim.x * blockDim.x;
+    long row = blockIdx.x * (long)blockDim.x + threadIdx.x;
+    for (; row + stride < n; row += 2 * stride) {
+        const T r0 = r[row], w0 = w[row], r1 = r[row + stride], w1 = w[row + stride];
+        g = Sc<T>::fma(r0, r0, g);
+        dl = Sc<T>::fma(r0, w0, dl);
+        h += Sc<T>::abs2(r0);
+        g = Sc<T>::fma(r1, r1, g);
+        dl = Sc<T>::fma(r1, w1, dl);
+        h += Sc<T>::abs2(r1);
+    }
+    if (row < n) {
+        const T r0 = r[row], w0 = w[row];
+        g = Sc<T>::fma(r0, r0, g);
+        dl = Sc<T>::fma(r0, w0, dl);
+        h += Sc<T>::abs2(r0);
+    }
+    __shared__ double s_red[32];
+    __shared__ double s_vals[NV];
+    double v[NV];
+    if constexpr (W == 1) {
+        v[0] = g;
+        v[1] = dl;
+        v[2] = h;
+    } else {
+        v[0] = ((cplx&)g).x;
+        v[1] = ((cplx&)g).y;
+        v[2] = ((cplx&)dl).x;
+        v[3] = ((cplx&)dl).y;
+        v[4] = h;
+    }
+#pragma unroll
+    for (int t = 0; t < NV; ++t) {
+        const double sv = block_sum(v[t], s_red);
+        if (threadIdx.x == 0) s_vals[t] = sv;
+    }
+    __syncthreads();
+    GridRed red{partials + (size_t)m * gridDim.x * NV, counters + m};
+    if (!grid_commit_at(red, s_vals, NV, blockIdx.x, gridDim.x)) return;
+    __shared__ double s_tot[NV];
+    grid_finish(red, NV, s_tot, gridDim.x);
+    if (threadIdx.x != 0) return;
+    cg_recurrence<T>(sc, s_tot, nullptr);
 }
 
 // Partial dots of TW trailing columns against w over this block's rows: one

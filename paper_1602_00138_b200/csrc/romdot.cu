@@ -1983,6 +1983,8 @@ template <class T> struct BatchedDeflated {
     int tw[M] = {0};
     ~BatchedDeflated() {
         if (hs) cudaFreeHost(hs);
+        for (auto& e : pev)
+            if (e) cudaEventDestroy(e);
     }
     T* col(DevBuf& b, int m) const { return b.template as<T>() + (size_t)m * npad; }
     T* kt(int m) const { return Ktb.template as<T>() + (size_t)m * tcap * npad; }
@@ -2050,6 +2052,7 @@ template <class T> struct BatchedDeflated {
             tr.Kt[m] = kt(m);
             tr.t[m] = 0;
             tw[m] = 0;
+            inuse[m] = false;
         }
         CK(cudaMemcpyAsync(stb.p, hs + M, sizeof(CGState) * M, cudaMemcpyHostToDevice, c.s));
         krb.ensure(sizeof(T) * npad * kb);
@@ -2069,7 +2072,7 @@ template <class T> struct BatchedDeflated {
         const long nkc = (op.N2 + kz - 1) / kz;
         gst = dim3(g0.x, g0.y, (unsigned)(nkc * M));
         nbc = (long)g0.x * g0.y * nkc;
-        part_st.ensure(sizeof(double) * M * nbc * NV);
+        part_st.ensure(sizeof(double) * M * std::max<long>(nbc, c.sms) * NV);
         cnt_st.ensure(sizeof(unsigned) * M);
         CK(cudaMemsetAsync(cnt_st.p, 0, sizeof(unsigned) * M, c.s));
         gx = (int)std::max(1L, std::min<long>((n + 255) / 256, (long)c.sms));
@@ -2106,6 +2109,8 @@ template <class T> struct BatchedDeflated {
         init.tol = tol;
         init.maxit = (int)std::min<long>(maxit, 0x7fffffff);
         init.hist_cap = 0;
+        inuse[m] = true;
+        last_it[m] = 0;
         hs[M + m] = init;
         CK(cudaMemcpyAsync(stb.template as<CGState>() + m, hs + M + m, sizeof(CGState), cudaMemcpyHostToDevice, c.s));
     }
@@ -2114,8 +2119,11 @@ template <class T> struct BatchedDeflated {
         Ctx& c = *ctx;
         CGState* st = stb.template as<CGState>();
         const OpDev& op = *opd;
-        bcg_stencil_dots<T><<<gst, 256, 0, c.s>>>(op, Rb.template as<T>(), Wb.template as<T>(), npad, st,
-                                                  part_st.template as<double>(), cnt_st.template as<unsigned>(), kz);
+        // stencil over the slots in use (columns 0 .. top; a finished slot inside the range
+        // is applied too: its R column is finite and its W column is not read again)
+        launch_stencil<T>(c, op, Rb.template as<T>(), npad, nullptr, Wb.template as<T>(), npad, top);
+        bd_dots<T><<<dim3(gx, top), 256, 0, c.s>>>(Rb.template as<T>(), Wb.template as<T>(), npad, n, st,
+                                                   part_st.template as<double>(), cnt_st.template as<unsigned>());
         c.check_launch();
         const int gridT = (int)std::max(1L, std::min<long>(ntileT, (long)c.sms));
         const int gridN = (int)std::max(1L, std::min<long>(ntileN, (long)c.sms));
@@ -2140,19 +2148,61 @@ template <class T> struct BatchedDeflated {
         c.check_launch();
     }
     const OpDev* opd = nullptr;
+    int last_it[M] = {0};        // iteration count of each slot at the previous poll
+    bool inuse[M] = {false};
+    int top = 0;                 // slots [0, top) hold or held a solve in this call
+    cudaEvent_t pev[2] = {nullptr, nullptr};
+    bool sampled = false;
     void iterate(const OpDev& op, int steps) {
+        Ctx& c = *ctx;
         opd = &op;
+        top = 0;
+        for (int m = 0; m < M; ++m)
+            if (inuse[m]) top = m + 1;
+        if (top == 0) return;
+        sampled = c.prof;
+        if (sampled) {
+            if (!pev[0])
+                for (auto& e : pev) CK(cudaEventCreate(&e));
+            CK(cudaEventRecord(pev[0], c.s));
+        }
         for (int i = 0; i < steps; ++i) {
             if (nstep == 4) step<4>();
             else if (nstep == 8) step<8>();
             else step<16>();
         }
+        if (sampled) CK(cudaEventRecord(pev[1], c.s));
     }
-    // states of all slots after the queued steps (synchronises the stream)
+    // states of all slots after the queued steps (synchronises the stream).
+    // Profile class 5 (rd_ctx_profile): device time of the whole call against
+    // the algorithmic bytes of the steps that ran -- per step the eigen block twice
+    // (T and N pass) and the 4 coefficient planes once, per slot-step the trailing
+    // block twice and 15 vector passes (stencil r, w; T passes w, w; N pass w in and
+    // out; update w, r, p, s, y in and r, p, s, y out).
     const CGState* poll() {
         Ctx& c = *ctx;
         CK(cudaMemcpyAsync(hs, stb.p, sizeof(CGState) * M, cudaMemcpyDeviceToHost, c.s));
         c.sync();
+        if (sampled) {
+            float ms = 0.f;
+            CK(cudaEventElapsedTime(&ms, pev[0], pev[1]));
+            const double es = sizeof(T);
+            double bytes = 0.0;
+            int ran = 0;
+            for (int m = 0; m < M; ++m) {
+                const int d = std::max(0, hs[m].it - last_it[m]);
+                ran = std::max(ran, d);
+                bytes += (double)d * es * n * (2.0 * tw[m] + 15.0);
+            }
+            bytes += (double)ran * n * (2.0 * es * kb + 32.0);
+            c.pc[5].ms += ms;
+            c.pc[5].bytes += bytes;
+            c.pc[5].samples += ran;
+            for (int m = 0; m < M; ++m) c.pc[6].samples += std::max(0, hs[m].it - last_it[m]);  // slot-steps
+            c.pc[6].ms += ms;
+            sampled = false;
+        }
+        for (int m = 0; m < M; ++m) last_it[m] = hs[m].it;
         return hs;
     }
     // y (padded column of the slot), image = A y (padded), g = y + U (e - K^T image)
@@ -2176,6 +2226,8 @@ template <class T> struct BatchedDeflated {
         }
         if (y_out) CK(cudaMemcpyAsync(y_out, y, sizeof(T) * n, cudaMemcpyDeviceToDevice, c.s));
         // the slot is empty again
+        inuse[m] = false;
+        last_it[m] = 0;
         hs[M + m] = CGState{};
         hs[M + m].done = 1;
         tr.t[m] = 0;

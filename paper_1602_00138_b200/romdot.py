@@ -241,7 +241,7 @@ class Context:
     def solver(self) -> int:
         return load_library().rd_ctx_get_solver(self.h)
 
-    PROF_CLASSES = ("cg_stencil_dots", "ts_T", "ts_NT", "cg_update", "cg_fused")
+    PROF_CLASSES = ("cg_stencil_dots", "ts_T", "ts_NT", "cg_update", "cg_fused", "bcg_defl_step", "bcg_defl_slot_steps")
 
     def prof(self):
         """{class: (ms_total, algorithmic_bytes_total, samples)} of the sampled launches."""

@@ -24,9 +24,15 @@ for mode in os.environ.get("MODES", "0,1").split(","):
     out = []
     for s, (pt, w) in enumerate(cfg.systems(), start=1):
         op.set_fields(cfg.fields(pt, w))
+        prof = int(os.environ.get("PROF_SYS", "0")) == s
+        if prof:
+            import torch
+            torch.cuda.synchronize(); torch.cuda.profiler.start()
         ctx.sync(); t0 = time.time()
         pr = rd.process_system(gb, op, lay, cfg.tol, s)
         ctx.sync(); dt = time.time() - t0
+        if prof:
+            torch.cuda.synchronize(); torch.cuda.profiler.stop()
         rn = rd.residual_norms(op, lay, pr.X)
         out.append((pr, dt, rn.max()))
         print(f"mode {mode} system {s}: cols {gb.cols} its {pr.inner_iterations} appended {sum(r.appended for r in pr.log)} "
