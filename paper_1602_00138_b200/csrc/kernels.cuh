@@ -538,6 +538,18 @@ __global__ void assemble_space_gram(const T* __restrict__ G00, int ku, const T* 
     }
 }
 
+// Gt (cj x m, ld cj) = [Ce ; Gtt]: Ce = Kb^T Kt (ku x m, ld ku), Gtt = Kt^T Kt (m x m).
+template <class T>
+__global__ void stack_space_gt(const T* __restrict__ Ce, int ku, const T* __restrict__ Gtt, int m,
+                               T* __restrict__ Gt) {
+    const int cj = ku + m;
+    const long tot = (long)cj * m;
+    for (long e = blockIdx.x * (long)blockDim.x + threadIdx.x; e < tot; e += (long)gridDim.x * blockDim.x) {
+        const int i = (int)(e % cj), q = (int)(e / cj);
+        Gt[e] = i < ku ? Ce[(size_t)q * ku + i] : Gtt[(size_t)q * m + (i - ku)];
+    }
+}
+
 // One-pass CGS coefficient against the eigen block (Gram-corrected, as the
 // inner iteration's): Co = 2 C1 - G00 C1, G00 = Kb^T Kb (ku x ku), C1 = Kb^T Kt
 // (ku x m, ld ku); Kt - Kb Co equals the two-pass CGS in exact arithmetic.

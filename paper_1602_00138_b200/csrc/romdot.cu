@@ -1965,35 +1965,26 @@ inline int batch_steps() {
     return b;
 }
 
-template <class T> struct BatchedDeflated {
+// The two DMMA passes over a 4-row-blocked n x kb block Q (bd_T_eig: C = Q^T X,
+// bd_N_eig: X -= Q C) for up to BD_M columns X at once, outside the batched
+// iteration: the per-RHS space factorisation projects a right-hand side's
+// trailing columns off the system's eigen block with them (one 6+ TB/s stream of
+// the block per pass instead of the thin Gram / GEMM kernels' 2-3.5 TB/s).
+// Columns are column-major, ld rows apart, and must cover whole row tiles
+// (rows % (4 * 32 * 16 / sizeof(T)) == 0) because the tiles come by bulk TMA.
+template <class T> struct EigPass {
     static constexpr int M = BD_M;
-    static constexpr int W = Sc<T>::W;
-    static constexpr int NV = 2 * W + 1;
-    static constexpr int kTS = BD_TCH * BD_NCH;  // slot stride of the trailing coefficient arrays
     Ctx* ctx = nullptr;
-    long n = 0, npad = 0, kb = 0, tcap = 0, cmax = 0;
-    DevBuf Rb, Wb, Pb, Sb, Yb, Ktb, Utb, Gb, Eb, c1e, c1t, cpe, cpt, stb, krb, part_st, cnt_st, part_tr, cnt_tr, tmp;
-    CGState* hs = nullptr;  // pinned: [0, M) polled states, [M, 2M) init staging
-    BDTrail<T> tr{};
+    long n = 0, rows = 0, kb = 0;
     BDLayout LT{}, LN{};
-    long ntileT = 0, ntileN = 0;
-    int nstep = 0, kz = 1, gx = 1;
-    dim3 gst;
-    long nbc = 0;
-    int tw[M] = {0};
-    ~BatchedDeflated() {
-        if (hs) cudaFreeHost(hs);
-        for (auto& e : pev)
-            if (e) cudaEventDestroy(e);
+    int nstep = 0;
+    DevBuf flags;  // CGState[M + 1][M]: row t has done = 0 for the first t entries
+
+    static long row_quantum() { return 4L * 32 * (16 / (long)sizeof(T)); }
+    bool usable(long n_, long ku, long cols) const {
+        return ku >= 1 && ku <= 64 && cols >= 1 && cols <= M && n_ % row_quantum() == 0;
     }
-    T* col(DevBuf& b, int m) const { return b.template as<T>() + (size_t)m * npad; }
-    T* kt(int m) const { return Ktb.template as<T>() + (size_t)m * tcap * npad; }
-    T* ut(int m) const { return Utb.template as<T>() + (size_t)m * tcap * npad; }
-    double* e_of(int m) const { return Eb.template as<double>() + (size_t)m * cmax * W; }
-
-    static bool supported(long ku, long tmax) { return ku >= 1 && ku <= 64 && tmax <= BD_TCH * BD_NCH; }
-
-    template <int NSTEP> void configure() {
+    template <int NSTEP> void configure_kernels() {
         int optin = 0;
         CK(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, ctx->device));
         cudaFuncAttributes fa;
@@ -2008,15 +1999,82 @@ template <class T> struct BatchedDeflated {
             const uint32_t per = L.stride_k + ((L.stride_x * M + 127u) & ~127u);
             const uint32_t fixed = L.total - 2 * per;
             int S = (int)std::min<long>(8, ((long)optin - 2048 - fixed) / per);
-            if (S < 2) throw ConfigError("batched solves: shared-memory ring too large");
+            if (S < 2) throw ConfigError("eigen-block passes: shared-memory ring too large");
             return bd_layout<T>((int)kb, TR, S, xpad);
         };
-        // T pass: 512-byte W segments per slot; N pass: twice the rows (8 row groups per
+        // T pass: 512-byte segments per column; N pass: twice the rows (8 row groups per
         // 64 complex rows, one per consumer warp)
         const int trT = 32 * (16 / (int)sizeof(T));
         LT = stages(trT, 64);
         LN = stages(2 * trT, 16);
     }
+    void configure(Ctx& c, long n_, long rows_, long ku) {
+        ctx = &c;
+        n = n_;
+        rows = rows_;
+        kb = ku;
+        nstep = kb <= 16 ? 4 : kb <= 32 ? 8 : 16;
+        if (nstep == 4) configure_kernels<4>();
+        else if (nstep == 8) configure_kernels<8>();
+        else configure_kernels<16>();
+        if (!flags.p) {
+            std::vector<CGState> h((size_t)(M + 1) * M);
+            for (int t = 0; t <= M; ++t)
+                for (int m = 0; m < M; ++m) h[(size_t)t * M + m].done = m < t ? 0 : 1;
+            flags.ensure(sizeof(CGState) * h.size());
+            CK(cudaMemcpy(flags.p, h.data(), sizeof(CGState) * h.size(), cudaMemcpyHostToDevice));
+        }
+    }
+    const CGState* first(int t) const { return flags.template as<CGState>() + (size_t)t * M; }
+    // out[(m kb + j) W] = sum_rows Q[row, j] X[row, m] for the columns m that st leaves running
+    void T_pass(const T* Q4, const T* X, long ld, const CGState* st, double* out) {
+        Ctx& c = *ctx;
+        const long ntile = rows / LT.TR;
+        const int grid = (int)std::max(1L, std::min<long>(ntile, (long)c.sms));
+        bd_T_eig<T><<<grid, TMA_THREADS, LT.total, c.s>>>(Q4, n, ntile, LT, X, ld, st, c.red(), out);
+        c.check_launch();
+    }
+    // X[:, m] -= Q coef[m] (coef[(m kb + j) W])
+    void N_pass(const T* Q4, T* X, long ld, const CGState* st, const double* coef) {
+        Ctx& c = *ctx;
+        const long ntile = rows / LN.TR;
+        const int grid = (int)std::max(1L, std::min<long>(ntile, (long)c.sms));
+        if (nstep == 4)
+            bd_N_eig<T, 4><<<grid, TMA_THREADS, LN.total, c.s>>>(Q4, n, ntile, LN, X, ld, st, coef);
+        else if (nstep == 8)
+            bd_N_eig<T, 8><<<grid, TMA_THREADS, LN.total, c.s>>>(Q4, n, ntile, LN, X, ld, st, coef);
+        else
+            bd_N_eig<T, 16><<<grid, TMA_THREADS, LN.total, c.s>>>(Q4, n, ntile, LN, X, ld, st, coef);
+        c.check_launch();
+    }
+};
+
+template <class T> struct BatchedDeflated {
+    static constexpr int M = BD_M;
+    static constexpr int W = Sc<T>::W;
+    static constexpr int NV = 2 * W + 1;
+    static constexpr int kTS = BD_TCH * BD_NCH;  // slot stride of the trailing coefficient arrays
+    Ctx* ctx = nullptr;
+    long n = 0, npad = 0, kb = 0, tcap = 0, cmax = 0;
+    DevBuf Rb, Wb, Pb, Sb, Yb, Ktb, Utb, Gb, Eb, c1e, c1t, cpe, cpt, stb, krb, part_st, cnt_st, part_tr, cnt_tr, tmp;
+    CGState* hs = nullptr;  // pinned: [0, M) polled states, [M, 2M) init staging
+    BDTrail<T> tr{};
+    EigPass<T> ep;
+    int kz = 1, gx = 1;
+    dim3 gst;
+    long nbc = 0;
+    int tw[M] = {0};
+    ~BatchedDeflated() {
+        if (hs) cudaFreeHost(hs);
+        for (auto& e : pev)
+            if (e) cudaEventDestroy(e);
+    }
+    T* col(DevBuf& b, int m) const { return b.template as<T>() + (size_t)m * npad; }
+    T* kt(int m) const { return Ktb.template as<T>() + (size_t)m * tcap * npad; }
+    T* ut(int m) const { return Utb.template as<T>() + (size_t)m * tcap * npad; }
+    double* e_of(int m) const { return Eb.template as<double>() + (size_t)m * cmax * W; }
+
+    static bool supported(long ku, long tmax) { return ku >= 1 && ku <= 64 && tmax <= BD_TCH * BD_NCH; }
 
     // per system: the eigen block of gb.Kr (n x ku, ld n) in the row-blocked layout
     void begin_system(Ctx& c, const OpDev& op, const T* Kb_colmajor, long ku, long tmax) {
@@ -2059,12 +2117,7 @@ template <class T> struct BatchedDeflated {
         repack_q4<T><<<c.grid_for(npad * kb, 256, 8), 256, 0, c.s>>>(Kb_colmajor, n, (int)kb, n, krb.template as<T>(),
                                                                     npad);
         c.check_launch();
-        nstep = kb <= 16 ? 4 : kb <= 32 ? 8 : 16;
-        if (nstep == 4) configure<4>();
-        else if (nstep == 8) configure<8>();
-        else configure<16>();
-        ntileT = npad / LT.TR;
-        ntileN = npad / LN.TR;
+        ep.configure(c, n, npad, kb);
         // stencil + dots: one slice of blocks per slot, about 8 blocks per SM over all slots
         dim3 g0 = stencil_grid(op, 1);
         kz = 1;
@@ -2115,7 +2168,7 @@ template <class T> struct BatchedDeflated {
         CK(cudaMemcpyAsync(stb.template as<CGState>() + m, hs + M + m, sizeof(CGState), cudaMemcpyHostToDevice, c.s));
     }
 
-    template <int NSTEP> void step() {
+    void step() {
         Ctx& c = *ctx;
         CGState* st = stb.template as<CGState>();
         const OpDev& op = *opd;
@@ -2125,11 +2178,7 @@ template <class T> struct BatchedDeflated {
         bd_dots<T><<<dim3(gx, top), 256, 0, c.s>>>(Rb.template as<T>(), Wb.template as<T>(), npad, n, st,
                                                    part_st.template as<double>(), cnt_st.template as<unsigned>());
         c.check_launch();
-        const int gridT = (int)std::max(1L, std::min<long>(ntileT, (long)c.sms));
-        const int gridN = (int)std::max(1L, std::min<long>(ntileN, (long)c.sms));
-        bd_T_eig<T><<<gridT, TMA_THREADS, LT.total, c.s>>>(krb.template as<T>(), n, ntileT, LT, Wb.template as<T>(),
-                                                          npad, st, c.red(), c1e.template as<double>());
-        c.check_launch();
+        ep.T_pass(krb.template as<T>(), Wb.template as<T>(), npad, st, c1e.template as<double>());
         bd_T_trail<T><<<dim3(gx, M), 256, 0, c.s>>>(tr, Wb.template as<T>(), npad, n, st,
                                                     part_tr.template as<double>(), cnt_tr.template as<unsigned>(),
                                                     c1t.template as<double>(), kTS);
@@ -2138,10 +2187,7 @@ template <class T> struct BatchedDeflated {
                                                       c1t.template as<double>(), Gb.template as<T>(), cmax * cmax,
                                                       cpe.template as<double>(), cpt.template as<double>());
         c.check_launch();
-        bd_N_eig<T, NSTEP><<<gridN, TMA_THREADS, LN.total, c.s>>>(krb.template as<T>(), n, ntileN, LN,
-                                                                 Wb.template as<T>(), npad, st,
-                                                                 cpe.template as<double>());
-        c.check_launch();
+        ep.N_pass(krb.template as<T>(), Wb.template as<T>(), npad, st, cpe.template as<double>());
         bd_update<T><<<dim3(gx, M), 256, 0, c.s>>>(tr, Wb.template as<T>(), Rb.template as<T>(), Pb.template as<T>(),
                                                    Sb.template as<T>(), Yb.template as<T>(), npad, n, st,
                                                    cpt.template as<double>(), kTS);
@@ -2166,11 +2212,7 @@ template <class T> struct BatchedDeflated {
                 for (auto& e : pev) CK(cudaEventCreate(&e));
             CK(cudaEventRecord(pev[0], c.s));
         }
-        for (int i = 0; i < steps; ++i) {
-            if (nstep == 4) step<4>();
-            else if (nstep == 8) step<8>();
-            else step<16>();
-        }
+        for (int i = 0; i < steps; ++i) step();
         if (sampled) CK(cudaEventRecord(pev[1], c.s));
     }
     // states of all slots after the queued steps (synchronises the stream).
@@ -2263,6 +2305,9 @@ template <class T> struct DevBasis : BasisBase {
     // free + malloc per system costs a device sync and up to ~1 s)
     DevBuf ps_idx, ps_val, ps_Wc, ps_Rall, ps_Coef, ps_Cpk, ps_rj, ps_wn, ps_y, ps_g, ps_im, ps_nrm;
     std::unique_ptr<BatchedDeflated<T>> bd;  // batched solves of the independent right-hand sides
+    EigPass<T> ep;                            // DMMA passes over the system's eigen block (space factorisation)
+    DevBuf Kq4, Uq4, Gtt, Cee;                // 4-row-blocked copies of Kr / Ur's leading ku columns; Gram pieces
+    bool ep_ready = false;
     long stats_batched_rhs = 0;
     // grow-only with 25% slack
     static void grow_to(DevBuf& b, size_t bytes) {
@@ -2566,6 +2611,21 @@ template <class T> struct DevBasis : BasisBase {
         // space Gram, used by the one-pass inner projection)
         G00.ensure(sizeof(T) * ku * ku);
         gram<T, false>(c, Kb, n, ku, Kb, n, ku, n, G00.template as<T>(), true, gwork);
+        // 4-row-blocked copies for the DMMA passes of factor_rhs_space / space_gram
+        static const int use_ep = [] {
+            const char* e = std::getenv("ROMDOT_RHS_DMMA");
+            return e ? std::atoi(e) : 1;
+        }();
+        ep_ready = use_ep && ep.usable(n, ku, 1);
+        if (ep_ready) {
+            ep.configure(c, n, n, ku);
+            Kq4.ensure(sizeof(T) * n * ku);
+            Uq4.ensure(sizeof(T) * n * ku);
+            repack_q4<T><<<c.grid_for(n * ku, 256, 8), 256, 0, c.s>>>(Kb, n, (int)ku, n, Kq4.template as<T>(), n);
+            c.check_launch();
+            repack_q4<T><<<c.grid_for(n * ku, 256, 8), 256, 0, c.s>>>(Ub, n, (int)ku, n, Uq4.template as<T>(), n);
+            c.check_launch();
+        }
     }
 
     // G = K^T K of the space factored last (ku + m columns): G00 plus the thin
@@ -2578,10 +2638,27 @@ template <class T> struct DevBasis : BasisBase {
         T* Kb = Kr.template as<T>();
         const T* Kt = Kb + (size_t)ku * n;
         Gt.ensure(sizeof(T) * cj * m);
-        for (long t0 = 0; t0 < m; t0 += 8) {
-            const long b = std::min(8L, m - t0);
-            gram<T, false>(c, Kb, n, cj, Kt + (size_t)t0 * n, n, b, n, Gt.template as<T>() + (size_t)t0 * cj, false,
-                           gwork);
+        if (ep_ready && ep.usable(n, ku, m)) {
+            // [Kb Kt]^T Kt in two pieces: Kb^T Kt by the DMMA T pass (one stream of the eigen
+            // block), Kt^T Kt by the thin Gram over the trailing columns only
+            Cee.ensure(sizeof(double) * Sc<T>::W * ku * BD_M);
+            Gtt.ensure(sizeof(T) * m * m);
+            ep.T_pass(Kq4.template as<T>(), Kt, n, ep.first((int)m), Cee.template as<double>());
+            for (long t0 = 0; t0 < m; t0 += 8) {
+                const long b = std::min(8L, m - t0);
+                gram<T, false>(c, Kt, n, m, Kt + (size_t)t0 * n, n, b, n, Gtt.template as<T>() + (size_t)t0 * m, false,
+                               gwork);
+            }
+            stack_space_gt<T><<<c.grid_for(cj * m, 256, 1), 256, 0, c.s>>>(Cee.template as<T>(), (int)ku,
+                                                                            Gtt.template as<T>(), (int)m,
+                                                                            Gt.template as<T>());
+            c.check_launch();
+        } else {
+            for (long t0 = 0; t0 < m; t0 += 8) {
+                const long b = std::min(8L, m - t0);
+                gram<T, false>(c, Kb, n, cj, Kt + (size_t)t0 * n, n, b, n, Gt.template as<T>() + (size_t)t0 * cj,
+                               false, gwork);
+            }
         }
         assemble_space_gram<T><<<c.grid_for(cj * cj, 256, 1), 256, 0, c.s>>>(
             ku > 0 ? G00.template as<T>() : nullptr, (int)ku, Gt.template as<T>(), (int)cj, Gsp.template as<T>());
@@ -2629,12 +2706,30 @@ template <class T> struct DevBasis : BasisBase {
                 double* na = c.sc(11);
                 col_norms<T><<<c.grid_for(n, 256, 2), 256, sizeof(double) * m, c.s>>>(Kt, n, (int)m, n, c.red(), nb);
                 c.check_launch();
-                gram<T, false>(c, Kb, n, ku, Kt, n, m, n, C1, false, gwork);
+                // the three passes over the eigen block: bd_T_eig / bd_N_eig (DMMA, one bulk-TMA
+                // stream of the 4-row-blocked block per pass) when the shape allows, else the
+                // thin Gram / GEMM kernels
+                const bool dm = ep_ready && ep.usable(n, ku, m);
+                auto T_pass = [&](T* Cout) {
+                    if (dm)
+                        ep.T_pass(Kq4.template as<T>(), Kt, n, ep.first((int)m), (double*)Cout);
+                    else
+                        gram<T, false>(c, Kb, n, ku, Kt, n, m, n, Cout, false, gwork);
+                };
+                auto N_pass = [&](const T* Cin) {
+                    if (dm) {
+                        ep.N_pass(Kq4.template as<T>(), Kt, n, ep.first((int)m), (const double*)Cin);
+                        ep.N_pass(Uq4.template as<T>(), Ut, n, ep.first((int)m), (const double*)Cin);
+                    } else {
+                        gemm<T, true>(c, Kb, n, ku, Cin, m, Kt, n, Kt, n, n, false);
+                        gemm<T, true>(c, Ub, n, ku, Cin, m, Ut, n, Ut, n, n, false);
+                    }
+                };
+                T_pass(C1);
                 onepass_coef<T><<<c.grid_for(ku * m, 256, 1), 256, 0, c.s>>>(G00.template as<T>(), (int)ku, C1,
                                                                                (int)m, C2);
                 c.check_launch();
-                gemm<T, true>(c, Kb, n, ku, C2, m, Kt, n, Kt, n, n, false);
-                gemm<T, true>(c, Ub, n, ku, C2, m, Ut, n, Ut, n, n, false);
+                N_pass(C2);
                 col_norms<T><<<c.grid_for(n, 256, 2), 256, sizeof(double) * m, c.s>>>(Kt, n, (int)m, n, c.red(), na);
                 c.check_launch();
                 std::vector<double> hn(2 * m);
@@ -2645,9 +2740,8 @@ template <class T> struct DevBasis : BasisBase {
                 for (long t = 0; t < m; ++t) cancel |= hn[m + t] < 0.5 * hn[t];
                 if (cancel) {
                     ++stats_rhs_second_pass;
-                    gram<T, false>(c, Kb, n, ku, Kt, n, m, n, C1, false, gwork);
-                    gemm<T, true>(c, Kb, n, ku, C1, m, Kt, n, Kt, n, n, false);
-                    gemm<T, true>(c, Ub, n, ku, C1, m, Ut, n, Ut, n, n, false);
+                    T_pass(C1);
+                    N_pass(C1);
                 }
             } else {
                 gram<T, false>(c, Kb, n, ku, Kt, n, m, n, C1, false, gwork);
