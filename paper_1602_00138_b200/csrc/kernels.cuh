@@ -538,6 +538,32 @@ __global__ void assemble_space_gram(const T* __restrict__ G00, int ku, const T* 
     }
 }
 
+// X <- X S for a small upper-triangular S (m x m, column-major, ld m) staged in
+// shared memory: thread per row, the row's MW leading entries in registers, in
+// place. The CholQR step of the per-RHS trailing block (X = Kt or Ut, S = the
+// inverse of the bilinear Cholesky factor of Kt^T Kt).
+template <class T, int MW>
+__global__ void __launch_bounds__(256) tri_right_inplace(T* __restrict__ X, long ld, int m, const T* __restrict__ S,
+                                                         long n) {
+    __shared__ T s_S[MW * MW];
+    for (int e = threadIdx.x; e < m * m; e += blockDim.x) s_S[e] = S[e];
+    __syncthreads();
+    for (long row = blockIdx.x * (long)blockDim.x + threadIdx.x; row < n; row += (long)gridDim.x * blockDim.x) {
+        T x[MW];
+#pragma unroll
+        for (int i = 0; i < MW; ++i) x[i] = i < m ? X[(size_t)i * ld + row] : Sc<T>::zero();
+#pragma unroll
+        for (int j = MW - 1; j >= 0; --j) {
+            if (j < m) {
+                T y = Sc<T>::zero();
+#pragma unroll
+                for (int i = 0; i <= j; ++i) y = Sc<T>::fma(x[i], s_S[j * m + i], y);
+                X[(size_t)j * ld + row] = y;
+            }
+        }
+    }
+}
+
 // Gt (cj x m, ld cj) = [Ce ; Gtt]: Ce = Kb^T Kt (ku x m, ld ku), Gtt = Kt^T Kt (m x m).
 template <class T>
 __global__ void stack_space_gt(const T* __restrict__ Ce, int ku, const T* __restrict__ Gtt, int m,

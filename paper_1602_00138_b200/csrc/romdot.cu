@@ -10,6 +10,7 @@
 #include <algorithm>
 #include <chrono>
 #include <cmath>
+#include <complex>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -1965,6 +1966,60 @@ inline int batch_steps() {
     return b;
 }
 
+// Bilinear Cholesky of a small Gram on the host: S upper triangular with
+// S^T S = G (no conjugation: G = Kt^T Kt of a complex-symmetric recycle block;
+// for real data the ordinary Cholesky), Sinv = S^-1, and the 1-norm condition
+// estimate of S. m <= 24. Returns false when a pivot is not finite or vanishes.
+template <class T> bool chol_bilinear_host(const std::vector<T>& G, long m, std::vector<T>& Sinv, double& kappa1) {
+    using Z = std::complex<double>;
+    auto toz = [](T v) {
+        if constexpr (Sc<T>::W == 1) return Z(v, 0.0);
+        else return Z(v.x, v.y);
+    };
+    auto fromz = [](Z v) {
+        if constexpr (Sc<T>::W == 1) return (T)v.real();
+        else return make_double2(v.real(), v.imag());
+    };
+    std::vector<Z> S((size_t)m * m, Z(0.0)), Si((size_t)m * m, Z(0.0));
+    double gmax = 0.0;
+    for (long j = 0; j < m; ++j) gmax = std::max(gmax, std::abs(toz(G[j + j * m])));
+    for (long j = 0; j < m; ++j) {
+        for (long i = 0; i <= j; ++i) {
+            Z v = toz(G[i + j * m]);
+            for (long k = 0; k < i; ++k) v -= S[k + i * m] * S[k + j * m];
+            if (i < j) {
+                S[i + j * m] = v / S[i + i * m];
+            } else {
+                if (!std::isfinite(v.real()) || !std::isfinite(v.imag()) || std::abs(v) <= 1e-28 * gmax) return false;
+                S[j + j * m] = std::sqrt(v);
+            }
+        }
+    }
+    for (long j = 0; j < m; ++j) {  // Si = S^-1 (upper), column by column
+        Si[j + j * m] = Z(1.0) / S[j + j * m];
+        for (long i = j - 1; i >= 0; --i) {
+            Z v(0.0);
+            for (long k = i + 1; k <= j; ++k) v += S[i + k * m] * Si[k + j * m];
+            Si[i + j * m] = -v / S[i + i * m];
+        }
+    }
+    double n1 = 0.0, n2 = 0.0;
+    for (long j = 0; j < m; ++j) {
+        double a = 0.0, b = 0.0;
+        for (long i = 0; i <= j; ++i) {
+            a += std::abs(S[i + j * m]);
+            b += std::abs(Si[i + j * m]);
+        }
+        n1 = std::max(n1, a);
+        n2 = std::max(n2, b);
+    }
+    kappa1 = n1 * n2;
+    if (!std::isfinite(kappa1)) return false;
+    Sinv.resize((size_t)m * m);
+    for (size_t e = 0; e < Sinv.size(); ++e) Sinv[e] = fromz(Si[e]);
+    return true;
+}
+
 // The two DMMA passes over a 4-row-blocked n x kb block Q (bd_T_eig: C = Q^T X,
 // bd_N_eig: X -= Q C) for up to BD_M columns X at once, outside the batched
 // iteration: the per-RHS space factorisation projects a right-hand side's
@@ -2308,7 +2363,7 @@ template <class T> struct DevBasis : BasisBase {
     EigPass<T> ep;                            // DMMA passes over the system's eigen block (space factorisation)
     DevBuf Kq4, Uq4, Gtt, Cee;                // 4-row-blocked copies of Kr / Ur's leading ku columns; Gram pieces
     bool ep_ready = false;
-    long stats_batched_rhs = 0;
+    long stats_batched_rhs = 0, stats_rhs_cgs_fallback = 0;
     // grow-only with 25% slack
     static void grow_to(DevBuf& b, size_t bytes) {
         if (bytes > b.bytes) b.ensure(bytes + bytes / 4);
@@ -2756,6 +2811,51 @@ template <class T> struct DevBasis : BasisBase {
                 gemm<T, true>(c, Ub, n, ku, C1, m, Ut, n, Ut, n, n, false);
                 dbg_sum(" frs Ut", Ut, n * m, c.s);
             }
+        }
+        // Trailing block: bilinear CholQR. G = Kt^T Kt (thin Gram over the m trailing columns),
+        // S^T S = G factored on the host (m <= 24), Kt <- Kt S^-1 and Ut <- Ut S^-1 in place;
+        // repeated while the factor's condition estimate says the pass lost digits (the rule of
+        // the eigen block above). A dozen launches instead of nine per column; same span and
+        // triangular structure as the column-by-column CGS2 below, which stays the fallback
+        // when the factor breaks down (ROMDOT_RHS_CHOLQR=0: always CGS2).
+        static const int cholqr = [] {
+            const char* e = std::getenv("ROMDOT_RHS_CHOLQR");
+            return e ? std::atoi(e) : 1;
+        }();
+        if (cholqr && m >= 2 && m <= 24) {
+            bool ok = true;
+            Gtt.ensure(sizeof(T) * 2 * m * m);
+            T* Gd_ = Gtt.template as<T>();
+            T* Sd_ = Gd_ + (size_t)m * m;
+            std::vector<T> hG((size_t)m * m), hS;
+            for (int pass = 0; pass < 3 && ok; ++pass) {
+                for (long t0 = 0; t0 < m; t0 += 8) {
+                    const long b = std::min(8L, m - t0);
+                    gram<T, false>(c, Kt, n, m, Kt + (size_t)t0 * n, n, b, n, Gd_ + (size_t)t0 * m, false, gwork);
+                }
+                CK(cudaMemcpyAsync(hG.data(), Gd_, sizeof(T) * m * m, cudaMemcpyDeviceToHost, c.s));
+                c.sync();
+                double kappa = 0.0;
+                if (!chol_bilinear_host<T>(hG, m, hS, kappa)) {
+                    ok = false;
+                    break;
+                }
+                CK(cudaMemcpyAsync(Sd_, hS.data(), sizeof(T) * m * m, cudaMemcpyHostToDevice, c.s));
+                const int grid = c.grid_for(n, 256, 8);
+                auto apply = [&](T* X) {
+                    if (m <= 4) tri_right_inplace<T, 4><<<grid, 256, 0, c.s>>>(X, n, (int)m, Sd_, n);
+                    else if (m <= 8) tri_right_inplace<T, 8><<<grid, 256, 0, c.s>>>(X, n, (int)m, Sd_, n);
+                    else if (m <= 16) tri_right_inplace<T, 16><<<grid, 256, 0, c.s>>>(X, n, (int)m, Sd_, n);
+                    else tri_right_inplace<T, 24><<<grid, 256, 0, c.s>>>(X, n, (int)m, Sd_, n);
+                    c.check_launch();
+                };
+                apply(Kt);
+                apply(Ut);
+                c.sync();  // hS is read by the copy above
+                if (kappa <= 20.0) break;  // this pass left O(kappa^2 eps) of non-orthogonality
+            }
+            if (ok) return;
+            ++stats_rhs_cgs_fallback;
         }
         double* coef = c.sc(6);
         double* nrm = c.sc(7);
