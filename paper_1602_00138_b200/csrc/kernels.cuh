@@ -414,65 +414,6 @@ __global__ void __launch_bounds__(256) cg_stencil_dots(OpDev op, const T* __rest
     cg_recurrence<T>(st, s_tot, hist);
 }
 
-// Batched independent CG / COCG (X0 seed solves, full-order transfer): column
-// c of R/Wv (ld) is its own solve with state st[c]. blockIdx.z = c * nkc + k
-// chunk; each column's blocks commit to their own partial slots and counter,
-// and the column's last block runs its scalar step. Converged columns return.
-// The assembled coefficients are re-read per column from L2 (64 MB at 128^3).
-template <class T>
-__global__ void __launch_bounds__(256) bcg_stencil_dots(OpDev op, const T* __restrict__ R, T* __restrict__ Wv, long ld,
-                                                        CGState* st, double* partials, unsigned* counters, int kz) {
-    constexpr int W = Sc<T>::W;
-    constexpr int NV = 2 * W + 1;
-    const int nkc = (op.N2 + kz - 1) / kz;
-    const int c = blockIdx.z / nkc;
-    const int kc = blockIdx.z - c * nkc;
-    CGState* sc = st + c;
-    if (sc->done) return;
-    const T* r = R + (size_t)c * ld;
-    T* w = Wv + (size_t)c * ld;
-    T g = Sc<T>::zero(), dl = Sc<T>::zero();
-    double h = 0.0;
-    const int i = blockIdx.x * 32 + (threadIdx.x & 31);
-    const int j = blockIdx.y * 8 + (threadIdx.x >> 5);
-    const int k0 = kc * kz, k1 = min(op.N2, k0 + kz);
-    if (i < op.N0 && j < op.N1)
-        zmarch<T>(op, r, i, j, k0, k1, [&](long p, const T& rp, const T& wp) {
-            w[p] = wp;
-            g = Sc<T>::fma(rp, rp, g);
-            dl = Sc<T>::fma(rp, wp, dl);
-            h += Sc<T>::abs2(rp);
-        });
-    __shared__ double s_red[32];
-    __shared__ double s_vals[NV];
-    double v[NV];
-    if constexpr (W == 1) {
-        v[0] = g;
-        v[1] = dl;
-        v[2] = h;
-    } else {
-        v[0] = ((cplx&)g).x;
-        v[1] = ((cplx&)g).y;
-        v[2] = ((cplx&)dl).x;
-        v[3] = ((cplx&)dl).y;
-        v[4] = h;
-    }
-#pragma unroll
-    for (int t = 0; t < NV; ++t) {
-        const double sv = block_sum(v[t], s_red);
-        if (threadIdx.x == 0) s_vals[t] = sv;
-    }
-    __syncthreads();
-    const unsigned nbc = gridDim.x * gridDim.y * nkc;
-    const unsigned b = blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * kc);
-    GridRed red{partials + (size_t)c * nbc * NV, counters + c};
-    if (!grid_commit_at(red, s_vals, NV, b, nbc)) return;
-    __shared__ double s_tot[NV];
-    grid_finish(red, NV, s_tot, nbc);
-    if (threadIdx.x != 0) return;
-    cg_recurrence<T>(sc, s_tot, nullptr);
-}
-
 // Batched CG update, blockIdx.y = column: p = r + beta p ; s = w + beta s ;
 // y += alpha p ; r -= alpha s (thread per row).
 template <class T>

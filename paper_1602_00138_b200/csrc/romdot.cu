@@ -1650,29 +1650,34 @@ std::vector<CGState> batched_cg(Ctx& c, DevOp& op, long m, const long* bidx, con
     CK(cudaMemcpyAsync(stb.p, hs, sizeof(CGState) * m, cudaMemcpyHostToDevice, c.s));
     CK(cudaStreamSynchronize(c.s));
     CGState* st = stb.template as<CGState>();
-    // stencil grid: one column per block slice; enough blocks per column to fill the GPU
-    dim3 g0 = stencil_grid(op.d, 1);
-    int kz = 1;
-    while ((long)g0.x * g0.y * ((op.d.N2 + kz - 1) / kz) * m > 16L * c.sms && kz < op.d.N2) kz *= 2;
-    const long nkc = (op.d.N2 + kz - 1) / kz;
-    if (nkc * m > 65535) throw ConfigError("batched CG: too many columns for one launch");
-    const dim3 gst(g0.x, g0.y, (unsigned)(nkc * m));
-    const long nbc = (long)g0.x * g0.y * nkc;
-    part.ensure(sizeof(double) * m * nbc * NV);
     cnt.ensure(sizeof(unsigned) * m);
     CK(cudaMemsetAsync(cnt.p, 0, sizeof(unsigned) * m, c.s));
     const long gxu = std::max(1L, std::min<long>((n + 255) / 256, std::max(8L, 32L * c.sms / m)));
     const dim3 gup((unsigned)gxu, (unsigned)m);
     const int batch = 8;
+    // W = A R for all columns through the multi-column TMA stencil (coefficient planes read
+    // once per column group instead of once per column), then the per-column merged dots and
+    // scalar steps (bd_dots). Columns outside [lo, hi) have finished (polled states).
+    const int gxd = (int)std::max(1L, std::min<long>((n + 255) / 256, (long)c.sms));
+    part.ensure(sizeof(double) * m * gxd * NV);
+    long lo = 0, hi = m;
     auto launch_batch = [&]() {
+        if (hi <= lo) return;
         for (int b = 0; b < batch; ++b) {
-            bcg_stencil_dots<T><<<gst, 256, 0, c.s>>>(op.d, Rb.template as<T>(), Wb.template as<T>(), n, st,
-                                                      part.template as<double>(), cnt.template as<unsigned>(), kz);
+            launch_stencil<T>(c, op.d, Rb.template as<T>() + (size_t)lo * n, n, nullptr,
+                              Wb.template as<T>() + (size_t)lo * n, n, hi - lo);
+            bd_dots<T><<<dim3(gxd, (unsigned)(hi - lo)), 256, 0, c.s>>>(
+                Rb.template as<T>() + (size_t)lo * n, Wb.template as<T>() + (size_t)lo * n, n, n, st + lo,
+                part.template as<double>(), cnt.template as<unsigned>() + lo);
             c.check_launch();
             bcg_update<T><<<gup, 256, 0, c.s>>>(Rb.template as<T>(), Pb.template as<T>(), Sb.template as<T>(), X,
                                                 Wb.template as<T>(), n, n, st);
             c.check_launch();
         }
+    };
+    auto shrink = [&](const CGState* h) {
+        while (lo < hi && h[lo].done) ++lo;
+        while (hi > lo && h[hi - 1].done) --hi;
     };
     auto all_done = [&](const CGState* h) {
         for (long j = 0; j < m; ++j)
@@ -1691,6 +1696,7 @@ std::vector<CGState> batched_cg(Ctx& c, DevOp& op, long m, const long* bidx, con
         CK(cudaEventSynchronize(c.ev[slot]));
         if (all_done(hs + slot * m)) break;
         if (++guard > maxit / batch + 8) break;
+        shrink(hs + slot * m);
         launch_batch();
         CK(cudaMemcpyAsync(hs + slot * m, st, sizeof(CGState) * m, cudaMemcpyDeviceToHost, c.s));
         CK(cudaEventRecord(c.ev[slot], c.s));
@@ -2115,9 +2121,7 @@ template <class T> struct BatchedDeflated {
     CGState* hs = nullptr;  // pinned: [0, M) polled states, [M, 2M) init staging
     BDTrail<T> tr{};
     EigPass<T> ep;
-    int kz = 1, gx = 1;
-    dim3 gst;
-    long nbc = 0;
+    int gx = 1;
     int tw[M] = {0};
     ~BatchedDeflated() {
         if (hs) cudaFreeHost(hs);
@@ -2173,17 +2177,10 @@ template <class T> struct BatchedDeflated {
                                                                     npad);
         c.check_launch();
         ep.configure(c, n, npad, kb);
-        // stencil + dots: one slice of blocks per slot, about 8 blocks per SM over all slots
-        dim3 g0 = stencil_grid(op, 1);
-        kz = 1;
-        while ((long)g0.x * g0.y * ((op.N2 + kz - 1) / kz) * M > 16L * c.sms && kz < op.N2) kz *= 2;
-        const long nkc = (op.N2 + kz - 1) / kz;
-        gst = dim3(g0.x, g0.y, (unsigned)(nkc * M));
-        nbc = (long)g0.x * g0.y * nkc;
-        part_st.ensure(sizeof(double) * M * std::max<long>(nbc, c.sms) * NV);
+        gx = (int)std::max(1L, std::min<long>((n + 255) / 256, (long)c.sms));
+        part_st.ensure(sizeof(double) * M * gx * NV);
         cnt_st.ensure(sizeof(unsigned) * M);
         CK(cudaMemsetAsync(cnt_st.p, 0, sizeof(unsigned) * M, c.s));
-        gx = (int)std::max(1L, std::min<long>((n + 255) / 256, (long)c.sms));
         part_tr.ensure(sizeof(double) * M * BD_NCH * gx * BD_TCH * W);
         cnt_tr.ensure(sizeof(unsigned) * M * BD_NCH);
         CK(cudaMemsetAsync(cnt_tr.p, 0, sizeof(unsigned) * M * BD_NCH, c.s));

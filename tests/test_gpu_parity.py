@@ -273,13 +273,13 @@ def test_device_eigen_seed_matches_oracle(rd, cfg):
     assert np.linalg.norm(U.T @ U - np.eye(c.k)) <= 1e-7
 
 
-@pytest.mark.parametrize("m,want", [(64, 64), (256, 219)])
-def test_rrqr_known_rank_decay_09(rd, m, want):
-    """C5 RRQR shape at small n: A = Q diag(0.9^j) P (seeded permutation),
-    rank at 1e-10 is 64 / 219; same rank and R diagonal as the
-    oracle's Householder QRCP."""
+@pytest.mark.parametrize("m,want,n", [(64, 64, 4000), (256, 219, 4000), (1024, 219, 16384)])
+def test_rrqr_known_rank_decay_09(rd, m, want, n):
+    """C5 RRQR shapes at small n: A = Q diag(0.9^j) P (seeded permutation),
+    rank at 1e-10 is 64 / 219 / 219; same rank, R diagonal and
+    retained span (principal angles) as the oracle's Householder QRCP -- the
+    m = 1024 case runs the multi-level path (805 columns dropped below tol)."""
     rng = np.random.default_rng(3)
-    n = 4000
     Q, _ = np.linalg.qr(rng.standard_normal((n, m)))
     A = (Q * (0.9 ** np.arange(m)))[:, rng.permutation(m)]
     rk, perm, rdiag, Qg = rd.rrqr(A, 1e-10, normalize=False)
@@ -473,6 +473,9 @@ def test_partial_lockstep_device_seed_C2(rd):
     (2, (317, 317), True, 33),      # 2D: lag of one x-line
     (3, (12, 12, 12), True, 9),     # tiny: fewer tiles than SMs, one step
     (2, (33, 33), False, 6),
+    (3, (64, 64, 64), True, 72),    # the widths C4 runs (c = 65..81): 10 columns per consumer warp
+    (3, (64, 64, 64), True, 96),    # 12 columns per warp
+    (3, (64, 64, 64), True, 128),   # the widest instantiation (16 per warp)
 ])
 def test_fused_iteration_matches_unfused(rd, monkeypatch, d, N, cplx, width):
     """cg_fused (update of iteration i + stencil/dots/K^T w of i+1 in one launch,
