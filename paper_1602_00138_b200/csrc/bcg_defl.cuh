@@ -324,7 +324,8 @@ __global__ void __launch_bounds__(TMA_THREADS, 1)
 // coefficient planes once for all slots.
 template <class T>
 __global__ void __launch_bounds__(256, 4) bd_dots(const T* __restrict__ R, const T* __restrict__ Wv, long ld, long n,
-                                                  CGState* st, double* partials, unsigned* counters) {
+                                                  CGState* st, double* partials, unsigned* counters,
+                                                  double* hist0 /* [slot]: relres of iteration 0, or null */) {
     constexpr int W = Sc<T>::W;
     constexpr int NV = 2 * W + 1;
     const int m = blockIdx.y;
@@ -376,7 +377,7 @@ __global__ void __launch_bounds__(256, 4) bd_dots(const T* __restrict__ R, const
     __shared__ double s_tot[NV];
     grid_finish(red, NV, s_tot, gridDim.x);
     if (threadIdx.x != 0) return;
-    cg_recurrence<T>(sc, s_tot, nullptr);
+    cg_recurrence<T>(sc, s_tot, hist0 ? hist0 + m : nullptr);  // hist_cap = 1: only iteration 0 is recorded
 }
 
 // Partial dots of TW trailing columns against w over this block's rows: one

@@ -1668,7 +1668,7 @@ std::vector<CGState> batched_cg(Ctx& c, DevOp& op, long m, const long* bidx, con
                               Wb.template as<T>() + (size_t)lo * n, n, hi - lo);
             bd_dots<T><<<dim3(gxd, (unsigned)(hi - lo)), 256, 0, c.s>>>(
                 Rb.template as<T>() + (size_t)lo * n, Wb.template as<T>() + (size_t)lo * n, n, n, st + lo,
-                part.template as<double>(), cnt.template as<unsigned>() + lo);
+                part.template as<double>(), cnt.template as<unsigned>() + lo, nullptr);
             c.check_launch();
             bcg_update<T><<<gup, 256, 0, c.s>>>(Rb.template as<T>(), Pb.template as<T>(), Sb.template as<T>(), X,
                                                 Wb.template as<T>(), n, n, st);
@@ -2117,14 +2117,16 @@ template <class T> struct BatchedDeflated {
     static constexpr int kTS = BD_TCH * BD_NCH;  // slot stride of the trailing coefficient arrays
     Ctx* ctx = nullptr;
     long n = 0, npad = 0, kb = 0, tcap = 0, cmax = 0;
-    DevBuf Rb, Wb, Pb, Sb, Yb, Ktb, Utb, Gb, Eb, c1e, c1t, cpe, cpt, stb, krb, part_st, cnt_st, part_tr, cnt_tr, tmp;
+    DevBuf Rb, Wb, Pb, Sb, Yb, Ktb, Utb, Gb, Eb, c1e, c1t, cpe, cpt, stb, krb, part_st, cnt_st, part_tr, cnt_tr, tmp, h0;
     CGState* hs = nullptr;  // pinned: [0, M) polled states, [M, 2M) init staging
+    double* h0h = nullptr;  // pinned: relres of iteration 0 per slot (first residual of the solve)
     BDTrail<T> tr{};
     EigPass<T> ep;
     int gx = 1;
     int tw[M] = {0};
     ~BatchedDeflated() {
         if (hs) cudaFreeHost(hs);
+        if (h0h) cudaFreeHost(h0h);
         for (auto& e : pev)
             if (e) cudaEventDestroy(e);
     }
@@ -2144,6 +2146,9 @@ template <class T> struct BatchedDeflated {
         tcap = std::max(1L, tmax);
         cmax = kb + tcap;
         if (!hs) CK(cudaMallocHost(&hs, sizeof(CGState) * 2 * M));
+        if (!h0h) CK(cudaMallocHost(&h0h, sizeof(double) * M));
+        h0.ensure(sizeof(double) * M);
+        CK(cudaMemsetAsync(h0.p, 0, sizeof(double) * M, c.s));
         const size_t vb = sizeof(T) * npad * M;
         for (DevBuf* b : {&Rb, &Wb, &Pb, &Sb, &Yb}) {
             b->ensure(vb);
@@ -2213,7 +2218,7 @@ template <class T> struct BatchedDeflated {
         init.scale = scale;
         init.tol = tol;
         init.maxit = (int)std::min<long>(maxit, 0x7fffffff);
-        init.hist_cap = 0;
+        init.hist_cap = 1;  // bd_dots records the first residual (hist0[slot])
         inuse[m] = true;
         last_it[m] = 0;
         hs[M + m] = init;
@@ -2228,7 +2233,8 @@ template <class T> struct BatchedDeflated {
         // is applied too: its R column is finite and its W column is not read again)
         launch_stencil<T>(c, op, Rb.template as<T>(), npad, nullptr, Wb.template as<T>(), npad, top);
         bd_dots<T><<<dim3(gx, top), 256, 0, c.s>>>(Rb.template as<T>(), Wb.template as<T>(), npad, n, st,
-                                                   part_st.template as<double>(), cnt_st.template as<unsigned>());
+                                                   part_st.template as<double>(), cnt_st.template as<unsigned>(),
+                                                   h0.template as<double>());
         c.check_launch();
         ep.T_pass(krb.template as<T>(), Wb.template as<T>(), npad, st, c1e.template as<double>());
         bd_T_trail<T><<<dim3(gx, M), 256, 0, c.s>>>(tr, Wb.template as<T>(), npad, n, st,
@@ -2276,6 +2282,7 @@ template <class T> struct BatchedDeflated {
     const CGState* poll() {
         Ctx& c = *ctx;
         CK(cudaMemcpyAsync(hs, stb.p, sizeof(CGState) * M, cudaMemcpyDeviceToHost, c.s));
+        CK(cudaMemcpyAsync(h0h, h0.p, sizeof(double) * M, cudaMemcpyDeviceToHost, c.s));
         c.sync();
         if (sampled) {
             float ms = 0.f;
@@ -3251,8 +3258,81 @@ void per_rhs_solve_system(DevBasis<T>& gb, DevOp& op, long nrhs, const long* bid
         CK(cudaMemsetAsync(b->p, 0, sizeof(T) * npad, c.s));
     }
     const T zero = Sc<T>::zero();
-    for (long j = 0; j < nrhs; ++j) {
+    for (long j = 0; j < nrhs; ++j)
         if (bidx[j] < 0 || bidx[j] >= n) throw ConfigError("baseline recycling: rhs index out of range");
+    // Every right-hand side of this comparator is independent of the others (its space holds
+    // its own directions only and nothing is shared, basis.cpp:221-264), so the solves run
+    // BD_M at a time with the eigen block streamed once for all of them (bcg_defl.cuh). The
+    // new directions are appended afterwards in right-hand-side order, so V and the index
+    // lists are the ones the one-at-a-time loop below leaves.
+    long tmax = 0;
+    for (const auto& sp : gb.spaces) tmax = std::max(tmax, (long)sp.size() - gb.ku);
+    if (batch_slots() && c.solver == 0 && use_one_pass_projection() && nrhs >= 2 &&
+        BatchedDeflated<T>::supported(gb.ku, tmax)) {
+        using DB = DevBasis<T>;
+        if (!gb.bd) gb.bd = std::make_unique<BatchedDeflated<T>>();
+        BatchedDeflated<T>& bd = *gb.bd;
+        constexpr int M = BatchedDeflated<T>::M;
+        DB::grow_to(gb.ps_Rall, sizeof(T) * n * nrhs);  // the y_m of every right-hand side, kept until the appends
+        T* Yall = gb.ps_Rall.template as<T>();
+        bd.begin_system(c, op.d, gb.Kr.template as<T>(), gb.ku, tmax);
+        std::vector<LogRow> rows(nrhs);
+        long slot_rhs[M];
+        for (int m = 0; m < M; ++m) slot_rhs[m] = -1;
+        long next = 0;
+        int active = 0;
+        T* rhs = rhsb.template as<T>();
+        auto fill = [&](int m) {
+            if (next >= nrhs) return false;
+            const long j = next++;
+            const T bv = Sc<T>::from(bval[j]);
+            CK(cudaMemcpyAsync(rhs + bidx[j], &bv, sizeof(T), cudaMemcpyHostToDevice, c.s));
+            auto& idx = gb.spaces[j];
+            gb.factor_rhs_space(op, idx);
+            const T* Gsp = gb.space_gram((long)idx.size());
+            bd.load(m, gb.Kr.template as<T>(), gb.Ur.template as<T>(), (long)idx.size(), Gsp, rhs, tol, maxit,
+                    std::fabs(bval[j]));
+            CK(cudaMemcpyAsync(rhs + bidx[j], &zero, sizeof(T), cudaMemcpyHostToDevice, c.s));
+            c.sync();  // bv is a stack value
+            slot_rhs[m] = j;
+            ++active;
+            return true;
+        };
+        const int mslots = batch_width();
+        for (int m = 0; m < mslots; ++m) fill(m);
+        while (active > 0) {
+            bd.iterate(op.d, batch_steps());
+            const CGState* hs = bd.poll();
+            for (int m = 0; m < M; ++m) {
+                const long j = slot_rhs[m];
+                if (j < 0 || !hs[m].done) continue;
+                if (!hs[m].converged)
+                    throw SolverError("baseline recycling: solve failed at system " + std::to_string(system_index) +
+                                      ", rhs " + std::to_string(j));
+                rows[j] = LogRow{system_index, (int)j, bd.h0h[m], hs[m].it, false};
+                T* Gj = Xdev ? Xdev + (size_t)j * n : gbuf.template as<T>();
+                bd.finish(m, op, gb.Kr.template as<T>(), gb.Ur.template as<T>(), Gj, Yall + (size_t)j * n,
+                          imbuf.template as<T>());
+                slot_rhs[m] = -1;
+                --active;
+                ++gb.stats_batched_rhs;
+                if (!fill(m)) bd.release(m);
+            }
+        }
+        for (long j = 0; j < nrhs; ++j) {
+            if (rows[j].iterations > 0) {
+                gb.append_raw(Yall + (size_t)j * n, kColCorrection);
+                gb.spaces[j].push_back((int)(gb.cols - 1));
+                rows[j].appended = true;
+                ++appends;
+                inner_its += rows[j].iterations;
+            }
+            log.push_back(rows[j]);
+        }
+        c.sync();
+        return;
+    }
+    for (long j = 0; j < nrhs; ++j) {
         const double bnorm = std::fabs(bval[j]);
         const T bv = Sc<T>::from(bval[j]);
         T* rhs = rhsb.template as<T>();

@@ -610,3 +610,30 @@ def test_batched_tail_is_bitwise_deterministic(rd):
     assert outs[0][1] == outs[1][1]
     for xa, xb in zip(outs[0][0], outs[1][0]):
         assert np.array_equal(xa, xb)
+
+
+@pytest.mark.parametrize("cfg", ["T3c", "T2"])
+def test_per_rhs_recycler_batched_matches_one_solve_path(rd, monkeypatch, cfg):
+    """The per-RHS-only comparator's right-hand sides are always independent
+    (basis.cpp:221-264), so its solves run batched; same BuildLog, solutions,
+    stored directions and index lists as one solve at a time."""
+    c = P.CONFIGS[cfg]
+    g, lay = c.grid, c.layout()
+    U0, X0 = _shared_seed(c, g, lay)
+    runs = {}
+    for mode in ("0", "1"):
+        monkeypatch.setenv("ROMDOT_BATCH", mode)
+        rec = rd.PerRhsRecycler(U0, X0)
+        out = [rec.solve_system(rd.SchurOperator(g, c.fields(pt, w), c.dtype), lay, c.tol, s)
+               for s, (pt, w) in enumerate(c.systems(), start=1)]
+        runs[mode] = (out, rec.batched_solves, rec.cols, [rec.space(j) for j in range(lay.n_rhs)], rec.V)
+    (a, n0, cols0, sp0, V0), (b, n1, cols1, sp1, V1) = runs["0"], runs["1"]
+    assert n0 == 0 and n1 == lay.n_rhs * len(c.systems())
+    assert cols0 == cols1 and sp0 == sp1
+    for pa, pb in zip(a, b):
+        for ra, rb in zip(pa.log, pb.log):
+            assert (ra.system, ra.rhs, ra.appended) == (rb.system, rb.rhs, rb.appended)
+            assert abs(ra.iterations - rb.iterations) <= 1
+            assert rb.init_relres == pytest.approx(ra.init_relres, rel=1e-9, abs=1e-14)
+        assert np.linalg.norm(pb.X - pa.X) <= 1e-8 * np.linalg.norm(pa.X)
+    assert np.linalg.norm(V1 - V0) <= 1e-6 * np.linalg.norm(V0)
