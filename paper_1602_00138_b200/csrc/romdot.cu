@@ -3058,6 +3058,11 @@ void process_system(DevBasis<T>& gb, DevOp& op, long nrhs, const long* bidx, con
             }
         }
         if (!pending.empty()) {
+            // longest first: the iteration count grows with the initial residual, and the last
+            // slots to drain run alone (results do not depend on the order; rows stay in RHS order)
+            std::stable_sort(pending.begin(), pending.end(), [&](long a, long b) {
+                return rows[a - j0].init_relres > rows[b - j0].init_relres;
+            });
             bd.begin_system(c, op.d, gb.Kr.template as<T>(), gb.ku, tmax);
             long slot_rhs[M];
             for (int m = 0; m < M; ++m) slot_rhs[m] = -1;
