@@ -130,7 +130,16 @@ template <class T> static void dbg_sum(const char* tag, const T* p, long count, 
     unsigned long long x = 1469598103934665603ull;
     const unsigned char* b = reinterpret_cast<const unsigned char*>(h.data());
     for (size_t i = 0; i < sizeof(T) * (size_t)count; ++i) x = (x ^ b[i]) * 1099511628211ull;
-    std::fprintf(stderr, "[romdot-sum] %s %016llx\n", tag, x);
+    long nonfinite = 0;  // with ROMDOT_POISON=1: reads of never-written device memory surface here
+    const double* dv = reinterpret_cast<const double*>(h.data());
+    std::string where;
+    for (size_t i = 0; i < sizeof(T) * (size_t)count / sizeof(double); ++i)
+        if (!std::isfinite(dv[i])) {
+            if (nonfinite < 12) where += " " + std::to_string(i);
+            ++nonfinite;
+        }
+    std::fprintf(stderr, "[romdot-sum] %s %016llx%s\n", tag, x,
+                 nonfinite ? (" NONFINITE " + std::to_string(nonfinite) + " at doubles" + where).c_str() : "");
 }
 
 template <class T> constexpr int dt_of();
@@ -169,7 +178,13 @@ struct DevBuf {
             const char* e = std::getenv("ROMDOT_POISON");
             return e ? std::atoi(e) : 0;
         }();
-        if (poison) CK(cudaMemset(p, 0xFF, b));
+        if (poison) {
+            // cudaMemset on device memory returns before the fill has run, and the fill sits on
+            // the legacy default stream, which the library's non-blocking stream does not wait
+            // for: without the sync the NaN fill can land AFTER the first writes to the buffer
+            CK(cudaMemset(p, 0xFF, b));
+            CK(cudaDeviceSynchronize());
+        }
     }
     template <class T> T* as() const { return static_cast<T*>(p); }
 };
@@ -3222,8 +3237,12 @@ void process_system(DevBasis<T>& gb, DevOp& op, long nrhs, const long* bidx, con
         DB::grow_to(Cpk, sizeof(T) * rf * nrhs);
         CK(cudaMemcpy2DAsync(Cpk.p, sizeof(T) * rf, Coef.p, sizeof(T) * capc, sizeof(T) * rf, nrhs,
                              cudaMemcpyDeviceToDevice, c.s));
+        dbg_sum("X corrections", Xdev, n * nrhs, c.s);
+        dbg_sum("X coefficients", Cpk.template as<T>(), rf * nrhs, c.s);
         gb.materialize_W();
+        dbg_sum("X W", gb.Wp(), n * rf, c.s);
         gemm<T, true>(c, gb.Wp(), n, rf, Cpk.template as<T>(), nrhs, Xdev, n, Xdev, n, n, false);
+        dbg_sum("X assembled", Xdev, n * nrhs, c.s);
     }
     c.sync();
     dbg_flush(c.s);
