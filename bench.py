@@ -542,7 +542,7 @@ def main():
         if "bcg_defl_step" in classes:
             bc = classes["bcg_defl_step"]
             roofline["batched"] = {
-                "kernel": "bcg_defl step (bcg_stencil_dots, bd_T_eig, bd_T_trail, bd_coef, bd_N_eig, bd_update)",
+                "kernel": "bcg_defl step (stencil_tma, bd_dots, bd_T_eig, bd_T_trail, bd_coef, bd_N_eig, bd_update)",
                 "achieved": round(bc["GBps"], 1), "frac": round(bc["GBps"] / peak, 4), "steps": bc["samples"],
                 "ms_per_step": round(bc["ms_per_launch"], 4), "share_of_step": round(batched_ms / t_val_ms, 3),
                 "solve_iterations": batched_its,

@@ -61,7 +61,7 @@ int rd_ctx_get_solver(rd_ctx* ctx);
  * the ctx stream, first iteration of each launch batch). enable resets the counters.
  * cls: 0 cg_stencil_dots, 1 ts_T, 2 ts_NT, 3 cg_update, 4 cg_fused (one event
  * pair around a batch of back-to-back launches), 5 one step of the batched
- * iteration (six launches; samples = steps), 6 the same time with samples =
+ * iteration (seven launches; samples = steps), 6 the same time with samples =
  * slot-steps (inner iterations done by the batched path). bytes = algorithmic. */
 void rd_ctx_profile(rd_ctx* ctx, int enable);
 int rd_ctx_prof_get(rd_ctx* ctx, int cls, double* ms, double* bytes, long* samples);
